@@ -1,0 +1,221 @@
+"""oracle -- TEST INFRASTRUCTURE, NOT PRODUCT CODE.
+
+ctypes front end of ``oracle/ktanh_oracle.c``: a plain, slow, scalar CPU
+implementation of K-TanH (arXiv 1909.07729) written from PAPER.md.  Only
+``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` leg may import this package.  It never imports the
+product package ``paper_1909_07729_b200`` and shares no code with it.
+
+numpy is used for array plumbing only; all of the method's arithmetic is
+in the C file (each function there cites its PAPER.md passage).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ktanh_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+OPS = {"tanh": 0, "sigmoid": 1, "swish": 2, "gelu": 3}
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (binary64, no FP contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp%d" % os.getpid()
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+             "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB)
+            ip = ctypes.POINTER(ctypes.c_int)
+            u16p = ctypes.POINTER(ctypes.c_uint16)
+            u32p = ctypes.POINTER(ctypes.c_uint32)
+            L.kto_bf16_decode.argtypes = [ctypes.c_uint16]
+            L.kto_bf16_decode.restype = ctypes.c_double
+            L.kto_bf16_encode_rne.argtypes = [ctypes.c_double]
+            L.kto_bf16_encode_rne.restype = ctypes.c_uint16
+            L.kto_table1.argtypes = [ip, ip, ip]
+            L.kto_table1.restype = None
+            L.kto_ktanh_bf16.argtypes = [ctypes.c_uint16, ip, ip, ip]
+            L.kto_ktanh_bf16.restype = ctypes.c_uint16
+            L.kto_ktanh_f32.argtypes = [ctypes.c_uint32, ip, ip, ip]
+            L.kto_ktanh_f32.restype = ctypes.c_uint32
+            L.kto_map_bf16.argtypes = [ctypes.c_int, u16p, u16p, ctypes.c_size_t, ip, ip, ip]
+            L.kto_map_bf16.restype = None
+            L.kto_map_f32.argtypes = [ctypes.c_int, u32p, u32p, ctypes.c_size_t, ip, ip, ip]
+            L.kto_map_f32.restype = None
+            L.kto_map_bf16_at.argtypes = [ctypes.c_int, u16p, ctypes.POINTER(ctypes.c_uint64),
+                                          u16p, ctypes.c_size_t, ip, ip, ip]
+            L.kto_map_bf16_at.restype = None
+            L.kto_lstm_gates_bf16.argtypes = [u16p, u16p, ctypes.c_size_t, ctypes.c_size_t,
+                                              ctypes.c_int, ip, ip, ip]
+            L.kto_lstm_gates_bf16.restype = None
+            L.kto_bounds.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip]
+            L.kto_bounds.restype = None
+            L.kto_build_lut.argtypes = [ctypes.c_int, ip, ip, ip, ctypes.POINTER(ctypes.c_double)]
+            L.kto_build_lut.restype = None
+            L.kto_interval_sse.argtypes = [ctypes.c_int, ip, ip, ip]
+            L.kto_interval_sse.restype = ctypes.c_double
+            L.kto_overflow_flag.argtypes = []
+            L.kto_overflow_flag.restype = ctypes.c_int
+            L.kto_gelu_consts.argtypes = [ctypes.c_int]
+            L.kto_gelu_consts.restype = ctypes.c_uint32
+            _lib = L
+    return _lib
+
+
+class Lut:
+    """Three 32-entry integer tables (T_E, T_r, T_b), Alg. 1 line 1."""
+
+    def __init__(self, E, r, b):
+        self.E = np.ascontiguousarray(E, dtype=np.int32)
+        self.r = np.ascontiguousarray(r, dtype=np.int32)
+        self.b = np.ascontiguousarray(b, dtype=np.int32)
+        assert self.E.shape == self.r.shape == self.b.shape == (32,)
+
+    def ptrs(self):
+        ip = ctypes.POINTER(ctypes.c_int)
+        return (self.E.ctypes.data_as(ip), self.r.ctypes.data_as(ip), self.b.ctypes.data_as(ip))
+
+    def rows(self):
+        return [(int(self.E[t]), int(self.r[t]), int(self.b[t])) for t in range(32)]
+
+
+def table1() -> Lut:
+    """The oracle's own transcription of Table 1."""
+    E = np.zeros(32, np.int32); r = np.zeros(32, np.int32); b = np.zeros(32, np.int32)
+    ip = ctypes.POINTER(ctypes.c_int)
+    lib().kto_table1(E.ctypes.data_as(ip), r.ctypes.data_as(ip), b.ctypes.data_as(ip))
+    return Lut(E, r, b)
+
+
+def build_lut(bmin_zero: bool = False):
+    """Sec. 2.4 optimizer (reading R*); returns (Lut, per-interval integer score)."""
+    E = np.zeros(32, np.int32); r = np.zeros(32, np.int32); b = np.zeros(32, np.int32)
+    sse = np.zeros(32, np.float64)
+    ip = ctypes.POINTER(ctypes.c_int)
+    lib().kto_build_lut(int(bmin_zero), E.ctypes.data_as(ip), r.ctypes.data_as(ip),
+                        b.ctypes.data_as(ip), sse.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return Lut(E, r, b), sse
+
+
+def bounds(r: int, v: int):
+    lo = ctypes.c_int(); hi = ctypes.c_int()
+    lib().kto_bounds(r, v, ctypes.byref(lo), ctypes.byref(hi))
+    return lo.value, hi.value
+
+
+def interval_sse(t: int, lut: Lut) -> float:
+    return lib().kto_interval_sse(t, *lut.ptrs())
+
+
+def overflow_flag() -> bool:
+    return bool(lib().kto_overflow_flag())
+
+
+def gelu_consts():
+    return lib().kto_gelu_consts(0), lib().kto_gelu_consts(1)
+
+
+def bf16_decode(w: int) -> float:
+    return lib().kto_bf16_decode(int(w))
+
+
+def bf16_encode_rne(x: float) -> int:
+    return int(lib().kto_bf16_encode_rne(float(x)))
+
+
+def _lut(lut):
+    return table1() if lut is None else lut
+
+
+def map_bf16(op: str, x_u16: np.ndarray, lut: Lut | None = None) -> np.ndarray:
+    """y = op(x) for a uint16 array of BF16 bit patterns (any shape)."""
+    lut = _lut(lut)
+    x = np.ascontiguousarray(x_u16, dtype=np.uint16)
+    y = np.empty_like(x)
+    u16p = ctypes.POINTER(ctypes.c_uint16)
+    lib().kto_map_bf16(OPS[op], x.ctypes.data_as(u16p), y.ctypes.data_as(u16p), x.size, *lut.ptrs())
+    return y
+
+
+def map_f32(op: str, x_u32: np.ndarray, lut: Lut | None = None) -> np.ndarray:
+    """y = op(x) for a uint32 array of FP32 bit patterns (any shape)."""
+    lut = _lut(lut)
+    x = np.ascontiguousarray(x_u32, dtype=np.uint32)
+    y = np.empty_like(x)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    lib().kto_map_f32(OPS[op], x.ctypes.data_as(u32p), y.ctypes.data_as(u32p), x.size, *lut.ptrs())
+    return y
+
+
+def map_bf16_at(op: str, x_u16: np.ndarray, idx: np.ndarray, lut: Lut | None = None) -> np.ndarray:
+    """Sampled evaluation: y[j] = op(x[idx[j]])."""
+    lut = _lut(lut)
+    x = np.ascontiguousarray(x_u16.reshape(-1), dtype=np.uint16)
+    idx = np.ascontiguousarray(idx, dtype=np.uint64)
+    y = np.empty(idx.shape, np.uint16)
+    u16p = ctypes.POINTER(ctypes.c_uint16)
+    lib().kto_map_bf16_at(OPS[op], x.ctypes.data_as(u16p),
+                          idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                          y.ctypes.data_as(u16p), idx.size, *lut.ptrs())
+    return y
+
+
+def lstm_gates_bf16(x_u16: np.ndarray, hidden: int, tanh_quarter: int = 2,
+                    lut: Lut | None = None) -> np.ndarray:
+    """[rows, 4*hidden] BF16 gate block: K-TanH on quarter `tanh_quarter`, K-Sigmoid elsewhere."""
+    lut = _lut(lut)
+    x = np.ascontiguousarray(x_u16, dtype=np.uint16)
+    assert x.size % (4 * hidden) == 0
+    rows = x.size // (4 * hidden)
+    y = np.empty_like(x)
+    u16p = ctypes.POINTER(ctypes.c_uint16)
+    lib().kto_lstm_gates_bf16(x.ctypes.data_as(u16p), y.ctypes.data_as(u16p), rows, hidden,
+                              tanh_quarter, *lut.ptrs())
+    return y
+
+
+def all_bf16() -> np.ndarray:
+    return np.arange(65536, dtype=np.uint32).astype(np.uint16)
+
+
+def bf16_to_f64(w: np.ndarray) -> np.ndarray:
+    """Exact decode of BF16 bit patterns (via the F32 embedding)."""
+    with np.errstate(invalid="ignore"):
+        return (np.asarray(w, dtype=np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def error_sweep(lut: Lut | None = None):
+    """Table 2 accuracy columns: max |K-TanH(x) - tanh(x)| and max
+    relative error over every finite BF16 x (relative error over x != 0)."""
+    w = all_bf16()
+    xv = bf16_to_f64(w)
+    finite = np.isfinite(xv)
+    y = bf16_to_f64(map_bf16("tanh", w, lut))
+    ref = np.tanh(xv)
+    err = np.abs(y - ref)
+    err[~finite] = 0.0
+    nz = finite & (xv != 0)
+    rel = np.zeros_like(err)
+    rel[nz] = err[nz] / np.abs(ref[nz])
+    i = int(np.argmax(err)); j = int(np.argmax(rel))
+    return {"max_abs": float(err[i]), "argmax_abs": int(w[i]),
+            "max_rel": float(rel[j]), "argmax_rel": int(w[j])}

@@ -1,0 +1,453 @@
+/*
+ * oracle/ktanh_oracle.c -- TEST INFRASTRUCTURE, NOT PRODUCT CODE.
+ *
+ * A plain, slow, scalar CPU implementation of K-TanH (Kundu et al.,
+ * "K-TanH: Efficient TanH for Deep Learning", arXiv 1909.07729), written
+ * from /root/reference/PAPER.md.  Every function cites the passage it
+ * follows ("PAPER.md:L (section / Alg. / Eq. / Table)").
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load, call or execute anything in oracle/.
+ * It shares no code, header, table or constant generator with the CUDA
+ * path in paper_1909_07729_b200/ and it never imports it.
+ *
+ * Precision: the K-TanH core is integer-only (as the paper defines it);
+ * every floating-point step that is not a "decision" is done in IEEE
+ * binary64.  The one decision made in floating point -- the argument
+ * u = sqrt(2/pi)(x + a x^3) of the K-GELU, whose rounding picks the LUT
+ * entry -- is taken in binary32 with the op order written in
+ * gelu_arg_f32() below (reading R-GELU-ARG), because the CUDA
+ * path takes that decision in binary32.
+ *
+ * Compile: gcc -O2 -std=c11 -ffp-contract=off -fPIC -shared -lm
+ * (-ffp-contract=off: no silent a*b+c contraction anywhere).
+ *
+ * Parity status of each function:
+ *   kto_bf16_decode / kto_bf16_encode_rne ..... pinned (round trip, nearest)
+ *   kto_ktanh_bf16 ............................ pinned (Table 2 error bound,
+ *                                               invariants, value-domain check)
+ *   kto_ktanh_f32 ............................. pinned (BF16 closed-form relation,
+ *                                               error bound, invariants)
+ *   kto_ksigmoid_* ............................ pinned (exact rational (1+t)/2)
+ *   kto_kswish_* / kto_kgelu_* ................ pinned (special cases + error bound)
+ *   kto_build_lut (Sec. 2.4 optimizer) ........ pinned (Table 1 match counts,
+ *                                               SSE dominance, Table 2 ablation)
+ *   kto_bounds ................................ pinned (exhaustive no-overflow)
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <string.h>
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+/* ------------------------------------------------------------------ */
+/* Number format, PAPER.md:80-81 (Sec. 1): x = (-1)^s 2^E (1 + M/2^p),   */
+/* BFloat16 (s,E,M) = (1,8,7), Float32 (1,8,23), E bias-added.          */
+/* ------------------------------------------------------------------ */
+
+/* Exact real value of a BF16 bit pattern (E=0 subnormal, E=255 inf/NaN). */
+double kto_bf16_decode(uint16_t w)
+{
+    int s = (w >> 15) & 1;
+    int E = (w >> 7) & 0xFF;
+    int M = w & 0x7F;
+    double v;
+    if (E == 0xFF) {
+        v = (M == 0) ? INFINITY : NAN;
+    } else if (E == 0) {
+        v = ldexp((double)M / 128.0, -126);          /* subnormal */
+    } else {
+        v = ldexp(1.0 + (double)M / 128.0, E - 127);  /* normal */
+    }
+    return s ? -v : v;
+}
+
+/* Round a binary64 value to the nearest BF16, ties to even.            */
+/* NaN -> 0x7FC0 (canonical quiet NaN), overflow -> +-inf.              */
+uint16_t kto_bf16_encode_rne(double x)
+{
+    if (isnan(x)) return 0x7FC0;
+    uint16_t s = signbit(x) ? 0x8000 : 0;
+    double a = fabs(x);
+    if (isinf(a)) return s | 0x7F80;
+    if (a == 0.0) return s;
+    int k;
+    frexp(a, &k);             /* a = f 2^k, f in [0.5,1) => a in [2^(k-1), 2^k) */
+    int e = k - 1;            /* unbiased exponent of a                           */
+    double quantum;           /* spacing of BF16 numbers around a                 */
+    if (e < -126) quantum = ldexp(1.0, -133);       /* subnormal spacing 2^-126/2^7 */
+    else          quantum = ldexp(1.0, e - 7);
+    double q = a / quantum;   /* exact: division by a power of two                */
+    double nq = nearbyint(q); /* default rounding mode: nearest, ties to even     */
+    long n = (long)nq;
+    long bits;
+    if (e < -126) {
+        bits = n;                                   /* E=0, M=n; n=128 -> 0x0080 */
+    } else {
+        bits = ((long)(e + 127) << 7) + (n - 128);  /* n=256 carries into E      */
+    }
+    if (bits >= 0x7F80) bits = 0x7F80;              /* overflow -> inf           */
+    return (uint16_t)(s | (uint16_t)bits);
+}
+
+static float f32_from_bits(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+static uint32_t bits_from_f32(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+
+/* ------------------------------------------------------------------ */
+/* Parameter tables T_E, T_r, T_b (Alg. 1 line 1).         */
+/* Table 1, transcribed here independently of the     */
+/* CUDA path, index t = 5-bit string "e1 e0 m6 m5 m4".                   */
+/* ------------------------------------------------------------------ */
+typedef struct { int E[32]; int r[32]; int b[32]; } kto_lut;
+
+/* rows in the order printed in Table 1: left column then right column */
+static const struct { int t; int E, r, b; } TABLE1_ROWS[32] = {
+    /* left column */
+    {0x07, 126, 6, 126}, {0x06, 126, 6, 126}, {0x05, 126, 6, 126}, {0x04, 126, 6, 126},
+    {0x03, 126, 4, 123}, {0x02, 126, 4, 123}, {0x01, 126, 4, 122}, {0x00, 126, 2, 119},
+    {0x1F, 126, 4, 110}, {0x1E, 126, 2,  89}, {0x1D, 126, 2,  89}, {0x1C, 126, 2,  88},
+    {0x1B, 126, 1,  73}, {0x1A, 126, 1,  73}, {0x19, 126, 1,  72}, {0x18, 126, 0,  65},
+    /* right column */
+    {0x17, 126, 1,   4}, {0x16, 126, 1,   4}, {0x15, 126, 1,   4}, {0x14, 126, 1,   3},
+    {0x13, 126, 1,   2}, {0x12, 126, 1,  -1}, {0x11, 126, 1,  -4}, {0x10, 125, 0, 112},
+    {0x0F, 125, 0, -18}, {0x0E, 125, 0, -15}, {0x0D, 125, 0, -12}, {0x0C, 125, 0, -10},
+    {0x0B, 125, 0,  -7}, {0x0A, 125, 0,  -6}, {0x09, 125, 0,  -4}, {0x08, 125, 1,   1},
+};
+
+void kto_table1(int *E, int *r, int *b)
+{
+    for (int i = 0; i < 32; ++i) {
+        int t = TABLE1_ROWS[i].t;
+        E[t] = TABLE1_ROWS[i].E;
+        r[t] = TABLE1_ROWS[i].r;
+        b[t] = TABLE1_ROWS[i].b;
+    }
+}
+
+/* Thresholds, PAPER.md:144 (Sec. 2.3): T1 = 0.25, T2 = 3.75. */
+static const double T1 = 0.25;
+static const double T2 = 3.75;
+
+/* Index t (Alg. 1 line 6; Sec. 2.4):      */
+/* "2 LSBs of exponent and 3 MSBs of mantissa"; the exponent bits are the  */
+/* high bits of t (layout fixed by Table 1, reading A1).         */
+static int index_t(int E, int M_top3) { return ((E & 3) << 3) | M_top3; }
+
+/* Set when a table entry pushes M_o outside [0, 2^q - 1] (an invalid LUT). */
+static int g_overflow = 0;
+int kto_overflow_flag(void) { int f = g_overflow; g_overflow = 0; return f; }
+
+/* ------------------------------------------------------------------ */
+/* Algorithm 1, K-TanH, BFloat16.                      */
+/* ------------------------------------------------------------------ */
+uint16_t kto_ktanh_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    /* line 1: x_i = (s_i, E_i, M_i) */
+    int s = (x >> 15) & 1;
+    int E = (x >> 7) & 0xFF;
+    int M = x & 0x7F;
+    double ax = fabs(kto_bf16_decode(x));
+    /* NaN: Alg. 1 is silent; reading A6 passes the input through. */
+    if (isnan(ax)) return x;
+    /* line 3: |x_i| < T1  ->  y_o = x_i */
+    if (ax < T1) return x;
+    /* line 4: |x_i| > T2  ->  (s_i, E_bias, 0), i.e. +-1 (incl. +-inf, reading A5) */
+    if (ax > T2) return (uint16_t)((s << 15) | (127 << 7) | 0);
+    /* line 6: bit string t from lower bits of E_i and higher bits of M_i */
+    int t = index_t(E, M >> 4);
+    /* line 7: theta_t = (E_t, r_t, b_t) */
+    int Et = TE[t], rt = Tr[t], bt = Tb[t];
+    /* line 8: s_o = s_i, E_o = E_t, M_o = (M_i >> r_t) + b_t */
+    int Mo = (M >> rt) + bt;
+    if (Mo < 0 || Mo > 127) g_overflow = 1;
+    /* line 9 */
+    return (uint16_t)((s << 15) | ((Et & 0xFF) << 7) | (Mo & 0x7F));
+}
+
+/* ------------------------------------------------------------------ */
+/* Algorithm 1 on Float32, native reading A8 ("compatible    */
+/* with multiple such data formats"): same T1/T2 and 5-bit index from    */
+/* (E & 3, top 3 of the 23-bit mantissa); line 8 with p = 23:            */
+/* M_o = (M_i >> r_t) + b_t * 2^(23-7)  (b_t is in units of 2^-7).        */
+/* ------------------------------------------------------------------ */
+uint32_t kto_ktanh_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    uint32_t s = x >> 31;
+    int E = (int)((x >> 23) & 0xFF);
+    int32_t M = (int32_t)(x & 0x7FFFFF);
+    double ax = fabs((double)f32_from_bits(x));
+    if (isnan(ax)) return x;                              /* A6 */
+    if (ax < T1) return x;                                /* line 3 */
+    if (ax > T2) return (s << 31) | (127u << 23);         /* line 4 */
+    int t = index_t(E, (int)(M >> 20));                   /* line 6 */
+    int Et = TE[t], rt = Tr[t], bt = Tb[t];               /* line 7 */
+    int32_t Mo = (M >> rt) + bt * 65536;                  /* line 8, p = 23 */
+    if (Mo < 0 || Mo > 0x7FFFFF) g_overflow = 1;
+    return (s << 31) | ((uint32_t)(Et & 0xFF) << 23) | ((uint32_t)Mo & 0x7FFFFF);
+}
+
+/* ------------------------------------------------------------------ */
+/* Derived activations, PAPER.md:60-71 (Sec. 1).                          */
+/*   Sigmoid(x) = (1 + TanH(x/2))/2   (parentheses garbled in the paper,  */
+/*                                     reading A7)                        */
+/*   Swish(x)   = x * Sigmoid(x)                                          */
+/*   GELU(x)   ~= x/2 (1 + TanH(sqrt(2/pi)(x + a x^3))),  a = 0.044715    */
+/* The TanH is K-TanH on the format's own bits: its argument is rounded   */
+/* (RNE) to the format first; the outer affine step is done in binary64   */
+/* and rounded once to the format.                                        */
+/* ------------------------------------------------------------------ */
+
+/* GELU argument, decision precision binary32 (reading R-GELU-ARG):       */
+/*   C0 = f32(sqrt(2/pi)), C1 = f32(sqrt(2/pi) * a)                        */
+/*   u  = x * fma(C1, x*x, C0)        == sqrt(2/pi)(x + a x^3) in exact math */
+static float gelu_arg_f32(float x)
+{
+    const double a = 0.044715;
+    const float C0 = (float)sqrt(2.0 / M_PI);
+    const float C1 = (float)(sqrt(2.0 / M_PI) * a);
+    float x2 = x * x;
+    float p = fmaf(C1, x2, C0);
+    float u = x * p;
+    return u;
+}
+
+uint32_t kto_gelu_consts(int which)   /* for the pin tests: bit patterns of C0, C1 */
+{
+    const double a = 0.044715;
+    float C0 = (float)sqrt(2.0 / M_PI);
+    float C1 = (float)(sqrt(2.0 / M_PI) * a);
+    return which == 0 ? bits_from_f32(C0) : bits_from_f32(C1);
+}
+
+uint16_t kto_ksigmoid_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    double xv = kto_bf16_decode(x);
+    uint16_t h = kto_bf16_encode_rne(xv / 2.0);          /* x/2 in BF16 */
+    uint16_t t = kto_ktanh_bf16(h, TE, Tr, Tb);          /* K-TanH(x/2) */
+    double tv = kto_bf16_decode(t);
+    return kto_bf16_encode_rne((1.0 + tv) / 2.0);
+}
+
+uint32_t kto_ksigmoid_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    double xv = (double)f32_from_bits(x);
+    float h = (float)(xv / 2.0);                          /* x/2 in F32 (RNE) */
+    uint32_t t = kto_ktanh_f32(bits_from_f32(h), TE, Tr, Tb);
+    double tv = (double)f32_from_bits(t);
+    return bits_from_f32((float)((1.0 + tv) / 2.0));
+}
+
+uint16_t kto_kswish_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    double xv = kto_bf16_decode(x);
+    uint16_t h = kto_bf16_encode_rne(xv / 2.0);
+    uint16_t t = kto_ktanh_bf16(h, TE, Tr, Tb);
+    double tv = kto_bf16_decode(t);
+    return kto_bf16_encode_rne(xv * (1.0 + tv) / 2.0);   /* x * Sigmoid(x) */
+}
+
+uint32_t kto_kswish_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    double xv = (double)f32_from_bits(x);
+    float h = (float)(xv / 2.0);
+    uint32_t t = kto_ktanh_f32(bits_from_f32(h), TE, Tr, Tb);
+    double tv = (double)f32_from_bits(t);
+    return bits_from_f32((float)(xv * (1.0 + tv) / 2.0));
+}
+
+uint16_t kto_kgelu_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    double xv = kto_bf16_decode(x);
+    float u = gelu_arg_f32((float)xv);                   /* exact widening of x */
+    uint16_t ub = kto_bf16_encode_rne((double)u);        /* argument in BF16 */
+    uint16_t t = kto_ktanh_bf16(ub, TE, Tr, Tb);
+    double tv = kto_bf16_decode(t);
+    return kto_bf16_encode_rne(xv / 2.0 * (1.0 + tv));
+}
+
+uint32_t kto_kgelu_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    float xf = f32_from_bits(x);
+    float u = gelu_arg_f32(xf);
+    uint32_t t = kto_ktanh_f32(bits_from_f32(u), TE, Tr, Tb);
+    double tv = (double)f32_from_bits(t);
+    return bits_from_f32((float)((double)xf / 2.0 * (1.0 + tv)));
+}
+
+/* ------------------------------------------------------------------ */
+/* Array entry points (loops over the scalar functions above).            */
+/* op: 0 tanh, 1 sigmoid, 2 swish, 3 gelu                                 */
+/* ------------------------------------------------------------------ */
+void kto_map_bf16(int op, const uint16_t *x, uint16_t *y, size_t n,
+                  const int *TE, const int *Tr, const int *Tb)
+{
+    for (size_t i = 0; i < n; ++i) {
+        switch (op) {
+        case 0: y[i] = kto_ktanh_bf16(x[i], TE, Tr, Tb); break;
+        case 1: y[i] = kto_ksigmoid_bf16(x[i], TE, Tr, Tb); break;
+        case 2: y[i] = kto_kswish_bf16(x[i], TE, Tr, Tb); break;
+        default: y[i] = kto_kgelu_bf16(x[i], TE, Tr, Tb); break;
+        }
+    }
+}
+
+void kto_map_f32(int op, const uint32_t *x, uint32_t *y, size_t n,
+                 const int *TE, const int *Tr, const int *Tb)
+{
+    for (size_t i = 0; i < n; ++i) {
+        switch (op) {
+        case 0: y[i] = kto_ktanh_f32(x[i], TE, Tr, Tb); break;
+        case 1: y[i] = kto_ksigmoid_f32(x[i], TE, Tr, Tb); break;
+        case 2: y[i] = kto_kswish_f32(x[i], TE, Tr, Tb); break;
+        default: y[i] = kto_kgelu_f32(x[i], TE, Tr, Tb); break;
+        }
+    }
+}
+
+/* Strided gather variant for sampled full-size checks: y[j] = f(x[idx[j]]). */
+void kto_map_bf16_at(int op, const uint16_t *x, const uint64_t *idx, uint16_t *y, size_t m,
+                     const int *TE, const int *Tr, const int *Tb)
+{
+    for (size_t j = 0; j < m; ++j) kto_map_bf16(op, &x[idx[j]], &y[j], 1, TE, Tr, Tb);
+}
+
+/* LSTM gate block (BASELINE.json config 4; GNMT LSTM):      */
+/* x is [rows, 4*hidden]; quarter q of each row is K-TanH if q ==          */
+/* tanh_quarter (the cell candidate g) else K-Sigmoid (gates i, f, o).     */
+void kto_lstm_gates_bf16(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,
+                         int tanh_quarter, const int *TE, const int *Tr, const int *Tb)
+{
+    size_t width = 4 * hidden;
+    for (size_t row = 0; row < rows; ++row) {
+        for (size_t col = 0; col < width; ++col) {
+            size_t i = row * width + col;
+            int q = (int)(col / hidden);
+            y[i] = (q == tanh_quarter) ? kto_ktanh_bf16(x[i], TE, Tr, Tb)
+                                       : kto_ksigmoid_bf16(x[i], TE, Tr, Tb);
+        }
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* Sec. 2.4 bounds, with p = 7 mantissa bits and       */
+/* s = 3 index bits of the mantissa, v = mantissa_idx_val:                 */
+/*   b_max = 2^p - 1 - floor(((v+1) 2^(p-s) - 1) / 2^r)                    */
+/*   b_min = -v * floor(2^(p-s-r))          (Eq. 3; reading A16)           */
+/* ------------------------------------------------------------------ */
+void kto_bounds(int r, int v, int *bmin, int *bmax)
+{
+    const int p = 7, s = 3;
+    *bmax = (1 << p) - 1 - (int)floor((double)((v + 1) * (1 << (p - s)) - 1) / ldexp(1.0, r));
+    *bmin = -v * (int)floor(ldexp(1.0, p - s - r));
+}
+
+/* ------------------------------------------------------------------ */
+/* Sec. 2.4 optimizer, Steps 1-3, reading R*:           */
+/*  Step 1: y_i = tanh(x_i) in binary64, (E_i, M_i) =   */
+/*     fields of RNE_bf16(y_i) (reading A12).                              */
+/*  Step 2: for each candidate E in {min(E_i, 126)}     */
+/*     (reading A15), M^_j = M_j if E = E_j, 0 if E > E_j, 2^q - 1 if      */
+/*     E < E_j; pick the E minimising sum (y_i - y^_i)^2 against the       */
+/*     unrounded y_i; ties -> smaller E.                                   */
+/*  Step 3 (Eq. 2): for r = 0..r_max (= p = 7):          */
+/*     b* = mean(M^_i - m_i / 2^r) (real division as printed, A13),        */
+/*     b = floor(b* + 1/2) (A14), clamped to [b_min, b_max]; score         */
+/*     sum (M^_i - ((m_i >> r) + b))^2; keep the minimum, ties -> smaller r */
+/*     (A17).  bmin_zero != 0 is the Sec. 3.1 ablation.      */
+/* Returns the per-interval minimum score in sse_out (may be NULL).         */
+/* ------------------------------------------------------------------ */
+void kto_build_lut(int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
+{
+    const int q = 7;
+    for (int t = 0; t < 32; ++t) {
+        /* the positive BF16 inputs of interval t with T1 <= x <= T2 */
+        double xs[16], ys[16];
+        int ms[16], Ei[16], Mi[16], cnt = 0;
+        for (int w = 0; w < 0x7F80; ++w) {
+            double xv = kto_bf16_decode((uint16_t)w);
+            if (xv < T1 || xv > T2) continue;
+            int E = (w >> 7) & 0xFF, M = w & 0x7F;
+            if (index_t(E, M >> 4) != t) continue;
+            xs[cnt] = xv;
+            ms[cnt] = M;
+            cnt++;
+        }
+        /* Step 1 */
+        for (int i = 0; i < cnt; ++i) {
+            ys[i] = tanh(xs[i]);
+            uint16_t yb = kto_bf16_encode_rne(ys[i]);
+            Ei[i] = (yb >> 7) & 0xFF;
+            Mi[i] = yb & 0x7F;
+        }
+        /* Step 2 */
+        int bestE = -1;
+        double bestSSE = INFINITY;
+        int Mhat_best[16];
+        for (int c = 0; c < cnt; ++c) {
+            int E = Ei[c] < 126 ? Ei[c] : 126;
+            double sse = 0.0;
+            int Mhat[16];
+            for (int j = 0; j < cnt; ++j) {
+                if (E == Ei[j]) Mhat[j] = Mi[j];
+                else if (E > Ei[j]) Mhat[j] = 0;
+                else Mhat[j] = (1 << q) - 1;
+                double yhat = ldexp(1.0 + Mhat[j] / 128.0, E - 127);
+                sse += (ys[j] - yhat) * (ys[j] - yhat);
+            }
+            if (sse < bestSSE || (sse == bestSSE && E < bestE)) {
+                bestSSE = sse;
+                bestE = E;
+                memcpy(Mhat_best, Mhat, sizeof(Mhat));
+            }
+        }
+        /* Step 3 */
+        int v = t & 7;
+        int bestR = -1, bestB = 0;
+        long bestScore = -1;
+        for (int r = 0; r <= 7; ++r) {
+            double bstar = 0.0;
+            for (int j = 0; j < cnt; ++j) bstar += Mhat_best[j] - ms[j] / ldexp(1.0, r);
+            bstar /= cnt;
+            int b = (int)floor(bstar + 0.5);
+            int bmin, bmax;
+            kto_bounds(r, v, &bmin, &bmax);
+            if (bmin_zero) bmin = 0;
+            if (b < bmin) b = bmin;
+            if (b > bmax) b = bmax;
+            long score = 0;
+            for (int j = 0; j < cnt; ++j) {
+                long d = Mhat_best[j] - ((ms[j] >> r) + b);
+                score += d * d;
+            }
+            if (bestScore < 0 || score < bestScore) {
+                bestScore = score;
+                bestR = r;
+                bestB = b;
+            }
+        }
+        TE[t] = bestE;
+        Tr[t] = bestR;
+        Tb[t] = bestB;
+        if (sse_out) sse_out[t] = (double)bestScore;
+    }
+}
+
+/* End-to-end squared error of one interval of a LUT against binary64 tanh */
+/* (used by the dominance pin: the optimizer's rows vs the printed rows).  */
+double kto_interval_sse(int t, const int *TE, const int *Tr, const int *Tb)
+{
+    double sse = 0.0;
+    for (int w = 0; w < 0x7F80; ++w) {
+        double xv = kto_bf16_decode((uint16_t)w);
+        if (xv < T1 || xv > T2) continue;
+        int E = (w >> 7) & 0xFF, M = w & 0x7F;
+        if (index_t(E, M >> 4) != t) continue;
+        double yv = kto_bf16_decode(kto_ktanh_bf16((uint16_t)w, TE, Tr, Tb));
+        double d = yv - tanh(xv);
+        sse += d * d;
+    }
+    return sse;
+}

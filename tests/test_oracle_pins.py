@@ -1,0 +1,406 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Every test here runs without a GPU.  None of them re-types the oracle's own
+formula: each checks the oracle against a value the paper prints (Table 1,
+Table 2, the threshold bit patterns), a closed form, an invariant, an exact
+rational computation, or brute force.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import read_golden
+
+W = O.all_bf16()
+XV = O.bf16_to_f64(W)
+FINITE = np.isfinite(XV)
+NAN = np.isnan(XV)
+
+
+def ktanh_all(lut=None):
+    return O.map_bf16("tanh", W, lut)
+
+
+# --------------------------------------------------------------------------
+# Table 1 / thresholds as printed
+# --------------------------------------------------------------------------
+def test_table1_transcription_matches_golden(golden_table1):
+    """Two independent transcriptions of Table 1 agree."""
+    T = O.table1()
+    E, r, b = golden_table1
+    assert list(T.E) == E and list(T.r) == r and list(T.b) == b
+
+
+def test_threshold_bit_patterns():
+    """T1=(0,01111101,0000000)=0.25, T2=(0,10000000,1110000)=3.75."""
+    rows = {row[0]: row for row in read_golden("thresholds.txt")}
+    for name in ("T1", "T2"):
+        _, val, s, e, m = rows[name]
+        w = (int(s) << 15) | (int(e, 2) << 7) | int(m, 2)
+        assert O.bf16_decode(w) == float(val)
+        assert O.bf16_encode_rne(float(val)) == w
+
+
+# --------------------------------------------------------------------------
+# BF16 codec: round trip and nearest-even, brute force
+# --------------------------------------------------------------------------
+def test_codec_round_trip_all_patterns():
+    for w in range(65536):
+        v = O.bf16_decode(w)
+        if math.isnan(v):
+            assert O.bf16_encode_rne(v) == 0x7FC0
+        else:
+            assert O.bf16_encode_rne(v) == w
+
+
+def test_encode_is_nearest_even_bruteforce():
+    rng = np.random.default_rng(0)
+    finite = [w for w in range(0x7F80)]  # positive finite patterns
+    for _ in range(3000):
+        w = int(rng.choice(finite[:-1]))
+        lo, hi = O.bf16_decode(w), O.bf16_decode(w + 1)
+        f = rng.random()
+        x = lo + (hi - lo) * f
+        for xx in (x, (lo + hi) / 2):      # random point and the exact midpoint
+            got = O.bf16_encode_rne(xx)
+            dlo, dhi = abs(xx - lo), abs(hi - xx)
+            if dlo < dhi:
+                want = w
+            elif dhi < dlo:
+                want = w + 1
+            else:
+                want = w if (w & 1) == 0 else w + 1
+            assert got == want, (hex(w), xx)
+            assert O.bf16_encode_rne(-xx) == want | 0x8000
+
+
+# --------------------------------------------------------------------------
+# Algorithm 1 invariants, exhaustive over all 65,536 BF16 patterns
+# --------------------------------------------------------------------------
+def test_bypass_identity_below_T1():
+    """Alg. 1 line 3: |x| < T1 -> y = x bit for bit (incl. +-0, subnormals)."""
+    y = ktanh_all()
+    m = FINITE & (np.abs(XV) < 0.25)
+    assert m.sum() == 2 * 16000
+    assert np.array_equal(y[m], W[m])
+
+
+def test_saturation_above_T2():
+    """Alg. 1 line 4: |x| > T2 -> (s, E_bias, 0) = +-1, incl. +-inf."""
+    y = ktanh_all()
+    m = ~NAN & (np.abs(XV) > 3.75)
+    assert m.sum() == 2 * 16144
+    want = np.where(W[m] & 0x8000, 0xBF80, 0x3F80).astype(np.uint16)
+    assert np.array_equal(y[m], want)
+
+
+def test_thresholds_take_table_path():
+    """Strict inequalities (reading A2): T1 and T2 themselves go through lines 6-8."""
+    y = ktanh_all()
+    assert y[0x3E80] != 0x3E80 and 0.25 < O.bf16_decode(y[0x3E80]) < math.tanh(0.25) + 0.0167
+    assert y[0x4070] != 0x3F80 and abs(O.bf16_decode(y[0x4070]) - math.tanh(3.75)) < 0.0167
+    assert np.count_nonzero(FINITE & (np.abs(XV) >= 0.25) & (np.abs(XV) <= 3.75)) == 2 * (4 * 128 - 15)
+
+
+def test_nan_passthrough():
+    """Reading A6: NaN inputs are returned unchanged."""
+    y = ktanh_all()
+    assert NAN.sum() == 254
+    assert np.array_equal(y[NAN], W[NAN])
+
+
+def test_odd_symmetry_and_range():
+    y = ktanh_all()
+    neg = ktanh_all()[W ^ 0x8000]
+    assert np.array_equal(neg[~NAN], (y ^ 0x8000)[~NAN])
+    yv = O.bf16_to_f64(y)
+    assert np.all(np.abs(yv[~NAN]) <= 1.0)
+
+
+def test_error_bound_table2():
+    """Table 2: K-TanH max |err| <= 1.67e-2, rel err <= 3.03%."""
+    g = dict((k, float(v)) for k, v in read_golden("table2_ktanh.txt"))
+    s = O.error_sweep()
+    assert s["max_abs"] <= g["max_err_e-2"] * 1e-2
+    assert s["max_rel"] <= g["rel_err_pct"] / 100
+    # tighter than the printed bound (Table 1 is better than the printed row)
+    assert s["max_abs"] < 0.009
+
+
+def test_value_domain_reconstruction(golden_table1):
+    """Alg. 1 lines 6-8 re-derived in the value domain: for every table-path x,
+    y = sign(x) 2^(E_t-127) (1 + ((m >> r_t) + b_t)/128) where e = floor(log2|x|),
+    m = (|x|/2^e - 1) 128 and t = ((e+127) mod 4) 8 + floor(m/16), using the golden Table 1."""
+    E, r, b = golden_table1
+    y = ktanh_all()
+    for w in range(65536):
+        x = XV[w]
+        if not (np.isfinite(x) and 0.25 <= abs(x) <= 3.75):
+            continue
+        ax = abs(x)
+        e = math.floor(math.log2(ax))
+        m = int(round((ax / 2.0 ** e - 1.0) * 128))
+        t = ((e + 127) % 4) * 8 + m // 16
+        val = 2.0 ** (E[t] - 127) * (1 + ((m >> r[t]) + b[t]) / 128)
+        assert O.bf16_decode(y[w]) == math.copysign(val, x), hex(w)
+
+
+def test_monotone_piecewise_and_bounded_drops():
+    """Monotonicity (north_star invariant) holds within each region of Alg. 1
+    (bypass, each of the 32 intervals, saturation); across interval boundaries
+    any decrease is bounded by 2 x the Table 2 error bound (both neighbours lie
+    within 1.67e-2 of the increasing tanh)."""
+    pos = np.arange(0x0000, 0x7F81)           # +0 .. +inf, increasing in value
+    y = O.bf16_to_f64(ktanh_all()[pos])
+    xv = XV[pos]
+    region = np.where(xv < 0.25, -1, np.where(xv > 3.75, 99, (pos >> 4) & 31))
+    d = np.diff(y)
+    same = region[1:] == region[:-1]
+    assert np.all(d[same] >= 0)
+    assert np.all(d[~same] >= -2 * 0.0167)
+    # negative side mirrors by odd symmetry (checked above)
+
+
+# --------------------------------------------------------------------------
+# Sec. 2.4 bounds, exhaustive
+# --------------------------------------------------------------------------
+def test_bounds_prevent_overflow_exhaustive():
+    for r in range(8):
+        for v in range(8):
+            lo, hi = O.bounds(r, v)
+            ms = range(16 * v, 16 * v + 16)
+            for b in range(lo, hi + 1):
+                for m in ms:
+                    assert 0 <= (m >> r) + b <= 127
+            # b_max is tight: one more overflows at the interval's top mantissa
+            assert ((16 * v + 15) >> r) + hi + 1 == 128
+            if r <= 4:   # b_min = -v 2^(4-r) is tight where 2^(4-r) is an integer
+                assert ((16 * v) >> r) + lo == 0
+
+
+def test_table1_respects_bounds():
+    T = O.table1()
+    for t in range(32):
+        lo, hi = O.bounds(int(T.r[t]), t & 7)
+        assert lo <= T.b[t] <= hi, t
+    ktanh_all(T)
+    assert not O.overflow_flag()
+
+
+# --------------------------------------------------------------------------
+# Sec. 2.4 optimizer vs Table 1 and vs Table 2's printed accuracy
+# --------------------------------------------------------------------------
+def test_optimizer_reproduces_table1():
+    """Reading R* (DESIGN.md): >= 26 of 32 rows exact; rows 00100-00111 are
+    functionally identical (same output on every table-path input); every
+    differing row has an end-to-end SSE no larger than the printed row."""
+    T = O.table1()
+    R, _ = O.build_lut(False)
+    exact = [t for t in range(32) if R.rows()[t] == T.rows()[t]]
+    assert len(exact) >= 26
+    yT, yR = ktanh_all(T), ktanh_all(R)
+    for t in range(32):
+        sel = FINITE & (np.abs(XV) >= 0.25) & (np.abs(XV) <= 3.75) & (((W >> 4) & 31) == t)
+        functional = np.array_equal(yT[sel], yR[sel])
+        if t in (4, 5, 6, 7):
+            assert functional, t
+        if not functional:
+            assert O.interval_sse(t, R) <= O.interval_sse(t, T) * (1 + 1e-12), t
+    assert not O.overflow_flag()
+
+
+def test_ablation_reproduces_table2_printed_accuracy():
+    """Sec. 3.1: the b_min = 0 table.  Its exhaustive error
+    rounds to exactly the printed Table 2 K-TanH row, 1.67e-2 and 3.03%
+    (PAPER.md:275)."""
+    g = dict((k, float(v)) for k, v in read_golden("table2_ktanh.txt"))
+    A, _ = O.build_lut(True)
+    s = O.error_sweep(A)
+    assert round(s["max_abs"] * 100, 2) == g["max_err_e-2"]
+    assert round(s["max_rel"] * 100, 2) == g["rel_err_pct"]
+    # and the ablated table is worse than the optimized one
+    assert s["max_abs"] > O.error_sweep(O.build_lut(False)[0])["max_abs"]
+
+
+def test_optimizer_deterministic():
+    a = O.build_lut(False)[0].rows()
+    b = O.build_lut(False)[0].rows()
+    assert a == b
+
+
+# --------------------------------------------------------------------------
+# FP32 native reading (A8)
+# --------------------------------------------------------------------------
+def test_f32_closed_form_relation_to_bf16():
+    """For BF16-exact inputs (low 16 bits zero), Alg. 1 line 8 with p = 23 gives
+    M23_o = (M23 >> r) + b 2^16 = ((m7 >> r) + b) 2^16 + (m7 mod 2^r) 2^(16-r),
+    so f32_out = widen(bf16_out) + ((m7 mod 2^r) << (16 - r)) on the table path
+    and f32_out = widen(bf16_out) elsewhere."""
+    T = O.table1()
+    xb = W[~NAN]
+    x32 = xb.astype(np.uint32) << 16
+    y32 = O.map_f32("tanh", x32)
+    y16 = O.map_bf16("tanh", xb).astype(np.uint32) << 16
+    xv = XV[~NAN]
+    table = (np.abs(xv) >= 0.25) & (np.abs(xv) <= 3.75)
+    m7 = (xb & 0x7F).astype(np.uint32)
+    rt = T.r[(xb >> 4) & 31].astype(np.uint32)
+    extra = np.where(table, (m7 & ((1 << rt) - 1)) << (16 - rt), 0).astype(np.uint32)
+    assert np.array_equal(y32, y16 + extra)
+
+
+def test_f32_invariants_and_error_bound():
+    rng = np.random.default_rng(1)
+    u = np.concatenate([rng.integers(0, 2**32, 400000, dtype=np.uint64).astype(np.uint32),
+                        (np.arange(1 << 20, dtype=np.uint64) << 12).astype(np.uint32)])
+    y = O.map_f32("tanh", u)
+    xv = u.view(np.float32).astype(np.float64)
+    yv = y.view(np.float32).astype(np.float64)
+    nan = np.isnan(xv)
+    assert np.array_equal(y[nan], u[nan])
+    byp = ~nan & (np.abs(xv) < 0.25)
+    assert np.array_equal(y[byp], u[byp])
+    sat = ~nan & (np.abs(xv) > 3.75)
+    assert np.array_equal(y[sat], np.where(u[sat] >> 31, 0xBF800000, 0x3F800000).astype(np.uint32))
+    fin = np.isfinite(xv)
+    assert np.max(np.abs(yv[fin] - np.tanh(xv[fin]))) <= 0.0167
+    ny = O.map_f32("tanh", u ^ np.uint32(0x80000000))
+    assert np.array_equal(ny[~nan], (y ^ np.uint32(0x80000000))[~nan])
+    assert not O.overflow_flag()
+
+
+# --------------------------------------------------------------------------
+# Derived activations
+# --------------------------------------------------------------------------
+def _frac_bf16(w):
+    return Fraction(O.bf16_decode(int(w)))
+
+
+def _rne_bf16_fraction(q: Fraction) -> int:
+    """Exact RNE of a rational to BF16 by brute force over the candidate grid."""
+    if q == 0:
+        return 0
+    s = 0x8000 if q < 0 else 0
+    a = abs(q)
+    lo, hi = 0, 0x7F80           # binary search the largest pattern <= a
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        if Fraction(O.bf16_decode(mid)) <= a:
+            lo = mid
+        else:
+            hi = mid
+    if Fraction(O.bf16_decode(lo)) == a:
+        return s | lo
+    dlo = a - Fraction(O.bf16_decode(lo))
+    dhi = Fraction(O.bf16_decode(lo + 1)) - a
+    pick = lo if dlo < dhi else lo + 1 if dhi < dlo else (lo if lo % 2 == 0 else lo + 1)
+    return s | pick
+
+
+def test_ksigmoid_exact_rational():
+    """K-Sigmoid(x) = RNE((1 + t)/2) computed in exact rationals, t = K-TanH(RNE(x/2))."""
+    ys = O.map_bf16("sigmoid", W)
+    ts = O.map_bf16("tanh", np.array([_rne_bf16_fraction(_frac_bf16(w) / 2) if FINITE[w] else 0
+                                      for w in range(65536)], np.uint16))
+    for w in range(0, 65536, 7):
+        if NAN[w] or not FINITE[w]:
+            continue
+        want = _rne_bf16_fraction((1 + _frac_bf16(ts[w])) / 2)
+        assert ys[w] == want, hex(w)
+
+
+def test_ksigmoid_special_values_and_bound():
+    ys = O.map_bf16("sigmoid", W)
+    assert ys[0x0000] == 0x3F00 and ys[0x8000] == 0x3F00       # sigmoid(0) = 1/2
+    assert ys[0x7F80] == 0x3F80 and ys[0xFF80] == 0x0000       # +-inf -> 1, 0
+    assert np.all(np.isnan(O.bf16_to_f64(ys[NAN])))
+    yv = O.bf16_to_f64(ys)[FINITE]
+    ref = 1 / (1 + np.exp(-XV[FINITE]))
+    # |(1+t)/2 - (1+tanh(x/2))/2| <= eps/2 (+ |tanh(RNE(x/2)) - tanh(x/2)| = 0 for
+    # |x/2| >= 2^-125) + half an output ulp (<= 2^-9)
+    assert np.max(np.abs(yv - ref)) <= 0.0167 / 2 + 2 ** -9
+
+
+def test_kswish_kgelu_special_values():
+    y_sw = O.map_bf16("swish", W)
+    y_ge = O.map_bf16("gelu", W)
+    assert y_sw[0x0000] == 0x0000 and y_ge[0x0000] == 0x0000
+    xv = XV
+    big = FINITE & (xv > 4)
+    assert np.array_equal(y_ge[big], W[big])                    # t saturates to +1: x/2 * 2 = x
+    neg = FINITE & (xv < -4)
+    assert np.all(O.bf16_to_f64(y_ge[neg]) == 0.0)              # t = -1: x/2 * 0 = 0
+    assert y_ge[0x7F80] == 0x7F80                              # GELU(+inf) = +inf
+    assert np.isnan(O.bf16_to_f64(y_ge[0xFF80]))               # -inf/2 * 0 = NaN (A21)
+    assert np.all(np.isnan(O.bf16_to_f64(y_sw[NAN]))) and np.all(np.isnan(O.bf16_to_f64(y_ge[NAN])))
+
+
+def test_kswish_error_bound():
+    """|K-Swish - Swish| <= |x|/2 (eps_K + |h - x/2|) + half ulp(y), eps_K = 1.67e-2."""
+    y = O.bf16_to_f64(O.map_bf16("swish", W))
+    m = FINITE & (np.abs(XV) <= 64)
+    x = XV[m]
+    ref = x / (1 + np.exp(-x))
+    h = O.bf16_to_f64(np.array([O.bf16_encode_rne(v / 2) for v in x]))
+    ulp = np.maximum(np.abs(ref), 2.0 ** -126) * 2.0 ** -8
+    bound = np.abs(x) / 2 * (0.0167 + np.abs(h - x / 2)) + ulp
+    assert np.all(np.abs(y[m] - ref) <= bound)
+
+
+def test_kgelu_error_bound():
+    """|K-GELU - GELU_tanh| <= |x|/2 (eps_K + |u_bf16 - u|) + half ulp(y), where
+    GELU_tanh is PAPER.md:69's tanh form in binary64 with a from tests/golden/gelu_a.txt."""
+    a = float(read_golden("gelu_a.txt")[0][1])
+    y = O.bf16_to_f64(O.map_bf16("gelu", W))
+    m = FINITE & (np.abs(XV) <= 64)
+    x = XV[m]
+    u = math.sqrt(2 / math.pi) * (x + a * x ** 3)
+    ref = x / 2 * (1 + np.tanh(u))
+    ub = np.array([O.bf16_decode(O.bf16_encode_rne(v)) for v in u])
+    ulp = np.maximum(np.abs(ref), 2.0 ** -126) * 2.0 ** -8
+    bound = np.abs(x) / 2 * (0.0167 + np.abs(ub - u) + 1e-6 * np.abs(u)) + ulp
+    assert np.all(np.abs(y[m] - ref) <= bound)
+    # and the whole |x| <= 5 range is within 2.5e-2 of the exact (erf) GELU
+    m5 = FINITE & (np.abs(XV) <= 5)
+    x5 = XV[m5]
+    exact = np.array([v / 2 * (1 + math.erf(v / math.sqrt(2))) for v in x5])
+    assert np.max(np.abs(O.bf16_to_f64(O.map_bf16("gelu", W))[m5] - exact)) <= 2.5e-2
+
+
+def test_gelu_argument_constants():
+    """C0 = f32(sqrt(2/pi)) and C1 = f32(sqrt(2/pi) a): checked against numpy's float32 rounding."""
+    a = float(read_golden("gelu_a.txt")[0][1])
+    c0, c1 = O.gelu_consts()
+    assert c0 == int(np.array([math.sqrt(2 / math.pi)], np.float32).view(np.uint32)[0])
+    assert c1 == int(np.array([math.sqrt(2 / math.pi) * a], np.float32).view(np.uint32)[0])
+
+
+def test_f32_derived_consistency():
+    """FP32 derived ops on BF16-exact inputs stay within the BF16 results' error
+    budget, and K-Sigmoid f32 is exactly RN32((1+t)/2) for t = K-TanH_f32(x/2)."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(20000).astype(np.float32) * 3
+    u = x.view(np.uint32)
+    s = O.map_f32("sigmoid", u).view(np.float32).astype(np.float64)
+    t = O.map_f32("tanh", (x / np.float32(2)).view(np.uint32)).view(np.float32)
+    want = np.array([float(np.float32(float(Fraction(float(v)) / 2 + Fraction(1, 2)))) for v in t])
+    assert np.array_equal(s, want)
+    ge = O.map_f32("gelu", u).view(np.float32).astype(np.float64)
+    xd = x.astype(np.float64)
+    ref = xd / 2 * (1 + np.tanh(math.sqrt(2 / math.pi) * (xd + 0.044715 * xd ** 3)))
+    assert np.all(np.abs(ge - ref) <= np.abs(xd) / 2 * 0.0167 + 1e-6)
+
+
+def test_lstm_gate_routing():
+    """Config 4 routing: quarter 2 (g) is K-TanH, quarters 0, 1, 3 K-Sigmoid."""
+    rng = np.random.default_rng(4)
+    H = 16
+    x = rng.integers(0, 65536, size=(5, 4 * H)).astype(np.uint16)
+    y = O.lstm_gates_bf16(x, H, 2)
+    for q in range(4):
+        sl = slice(q * H, (q + 1) * H)
+        want = O.map_bf16("tanh" if q == 2 else "sigmoid", x[:, sl])
+        assert np.array_equal(y[:, sl], want)
