@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""bench.py -- K-TanH hot path on B200: Gelem/s and achieved HBM GB/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ktanh|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
+        --master-addr 127.0.0.1 --master-port P bench.py --gpus N ...
+
+Metric (BASELINE.json): "K-TanH Gelem/s and achieved HBM GB/s vs ~8 TB/s
+peak at 1/2/4/8 B200".  The headline workload is BASELINE.json configs[1]:
+BF16 K-TanH over a flat 2^24-element tensor ~ N(0, 2^2), one library call
+(= one kernel) per step.  Every rank processes its own independent tensor
+(seed + rank, weak scaling, no collective on the data path); `value` is the
+elements of all ranks / the max over ranks of the timed region.
+
+Timing: W warm-up steps, then windows of exactly K steps, each bracketed by
+a barrier and cuda synchronize, timed with CUDA events on the launching
+stream; the K launches of a window are replayed from a CUDA graph (the
+library calls are capturable).  Inputs smaller than L2 rotate through
+buffer sets totalling > 4x L2 so every step reads cold HBM.  nvidia-smi
+clocks are sampled during the timed windows.  Reported: the median window.
+
+`--impl reference` times the CPU oracle (oracle/, the scalar C
+implementation of the paper's algorithm) on the host cores on a bounded
+sample of the same workload; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+import workloads as WL
+
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+NOMINAL_HBM_GBS = 8000.0    # BASELINE.json north_star "~8 TB/s"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def mark(self):
+        return len(self.lines)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.t:
+                self.t.join(timeout=2)
+
+    def summary(self, lo=0, hi=None):
+        rows = [l.split(", ") for l in self.lines[lo:hi] if l.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ steps --
+class Step:
+    """One pass of the hot path over one batch: a single library call."""
+
+    def __init__(self, kt, cfg_key, op, device, rank, sets=None):
+        self.cfg = WL.CONFIGS[cfg_key]
+        self.op = op
+        self.kt = kt
+        n = self.cfg.numel
+        self.n = n
+        es = self.cfg.elem_bytes
+        self.bytes_per_step = 2 * n * es              # algorithmic: read x + write y
+        if sets is None:
+            sets = 1 if self.bytes_per_step >= 2 * L2_BYTES else \
+                max(2, math.ceil(4 * L2_BYTES / self.bytes_per_step))
+        self.sets = sets
+        x0 = WL.make_input(self.cfg, device=device, rank=rank)
+        self.xs = [x0] + [WL.make_input(self.cfg, device=device, rank=rank, seed=self.cfg.seed + 1000 * s)
+                          for s in range(1, sets)]
+        self.ys = [torch.empty_like(x0) for _ in range(sets)]
+        self.fn = self._bind()
+
+    def _bind(self):
+        kt, op = self.kt, self.op
+        if op == "lstm":
+            return lambda x, y: kt.klstm_gates_bf16(x, WL.LSTM_HIDDEN, 2, out=y)
+        return lambda x, y: getattr(kt, op)(x, out=y)
+
+    def run(self, i):
+        s = i % self.sets
+        self.fn(self.xs[s], self.ys[s])
+
+
+def barrier(world):
+    if world > 1:
+        torch.distributed.barrier()
+
+
+def max_over_ranks(v: float, world: int, device) -> float:
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_windows(step: Step, K: int, W: int, world: int, device, clocks: ClockSampler | None,
+                 min_total_s: float = 1.0, max_windows: int = 50):
+    """W warm-up steps, then windows of exactly K graph-replayed steps; returns
+    (per-window max-over-ranks ms, clock summary, launches per step)."""
+    stream = torch.cuda.Stream(device)
+    torch.cuda.synchronize(device)
+    for i in range(W):                      # untimed warm-up (eager)
+        step.run(i)
+    torch.cuda.synchronize(device)
+    c0 = step.kt.launch_count()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for i in range(K):
+            step.run(W + i)
+    launches_per_step = (step.kt.launch_count() - c0) / K
+    g.replay()                               # graph warm-up
+    torch.cuda.synchronize(device)
+    # number of windows: enough for ~min_total_s of timed work (clock sampling)
+    t0 = time.perf_counter()
+    g.replay()
+    torch.cuda.synchronize(device)
+    est = time.perf_counter() - t0
+    nwin = int(max(3, min(max_windows, math.ceil(min_total_s / max(est, 1e-6)))))
+    nwin = int(max_over_ranks(nwin, world, device))
+    mark0 = clocks.mark() if clocks else 0
+    times = []
+    for _ in range(nwin):
+        barrier(world)
+        torch.cuda.synchronize(device)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize(device)
+        barrier(world)
+        ms = e0.elapsed_time(e1)
+        times.append(max_over_ranks(ms, world, device))
+    time.sleep(0.12)
+    clk = clocks.summary(mark0, None) if clocks else None
+    del g
+    return times, clk, launches_per_step
+
+
+def time_eager(step: Step, K: int, device):
+    """K steps through the Python binding -> C ABI per step (no graph)."""
+    torch.cuda.synchronize(device)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(K):
+        step.run(i)
+    e1.record()
+    torch.cuda.synchronize(device)
+    return e0.elapsed_time(e1) / K
+
+
+def time_e2e(kt, cfg, op, K: int, W: int, world: int, device, rank):
+    """Same metric end to end through kt_apply_host: every step copies its input
+    from pinned host memory, runs the kernel, and copies the result back."""
+    x_dev = WL.make_input(cfg, device=device, rank=rank)
+    x_host = x_dev.cpu().pin_memory()
+    y_host = torch.empty_like(x_host).pin_memory()
+    del x_dev
+    work = torch.empty(64 << 20, dtype=torch.uint8, device=device)
+    for _ in range(max(1, W)):
+        kt.apply_host(op, x_host, y_host, work)
+    torch.cuda.synchronize(device)
+    barrier(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        kt.apply_host(op, x_host, y_host, work)
+    e1.record()
+    torch.cuda.synchronize(device)
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1) / K, world, device)
+    nb = x_host.numel() * x_host.element_size()
+    return ms, nb, nb
+
+
+def cpu_baseline(cfg, op, device, budget_s=12.0, max_elems=1 << 24):
+    """The oracle as it stands, single-threaded on this host, on a bounded
+    prefix of the same workload bytes; repeated until ~budget_s of CPU work."""
+    import oracle as O
+    x = WL.make_input(cfg, device=device)
+    m = min(x.numel(), max_elems)
+    if cfg.dtype == torch.bfloat16:
+        xb = x.reshape(-1)[:m].view(torch.int16).cpu().numpy().view(np.uint16)
+        f = (lambda: O.lstm_gates_bf16(xb, WL.LSTM_HIDDEN, 2)) if op == "lstm" else \
+            (lambda: O.map_bf16(op, xb))
+    else:
+        xb = x.reshape(-1)[:m].view(torch.int32).cpu().numpy().view(np.uint32)
+        f = lambda: O.map_f32(op, xb)
+    del x
+    f()  # load / build the library outside the timing
+    reps, t = 0, 0.0
+    while t < budget_s and reps < 1000:
+        t0 = time.perf_counter()
+        f()
+        t += time.perf_counter() - t0
+        reps += 1
+    return {"value": round(m * reps / t / 1e9, 6), "unit": "Gelem/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {m} elements of the {cfg.key} input, {reps} passes, {t:.1f} s, "
+                      f"single-threaded scalar C oracle (oracle/ktanh_oracle.c)",
+            "host_cpu": _cpu_model(), "host_threads": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def load_traffic(workload_op):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) \
+            if os.path.isdir(os.path.join(ROOT, "profiles")) else []:
+        if name.startswith("ncu_full_") and name.endswith(".json"):
+            try:
+                d = json.load(open(os.path.join(ROOT, "profiles", name)))
+                t = d.get("kernels", {}).get(workload_op)
+                if t and t.get("dram_bytes_per_launch"):
+                    return float(t["dram_bytes_per_launch"]), name
+            except Exception:
+                continue
+    return None, None
+
+
+KERNEL_NAME = {"ktanh_bf16": "k_map<0, 0, true>", "ktanh_f32": "k_map<0, 1, true>",
+               "kgelu_bf16": "k_map<3, 0, true>", "kswish_bf16": "k_map<2, 0, true>",
+               "lstm": "k_lstm<true>"}
+
+EXTRA = [("c3_f32_2p28", "ktanh_f32"), ("c4_lstm_gates", "lstm"),
+         ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16")]
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    cfg = WL.CONFIGS["c2_bf16_2p24"]
+    import oracle as O
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    x = WL.make_input(cfg, device=dev)
+    m = 1 << 22                                   # bounded sample per step
+    xb = x.reshape(-1)[:m].view(torch.int16).cpu().numpy().view(np.uint16)
+    del x
+    for _ in range(args.warmup):
+        O.map_bf16("tanh", xb)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.map_bf16("tanh", xb)
+        ts.append(time.perf_counter() - t0)
+    sec = sum(ts) / len(ts)
+    val = m / sec / 1e9
+    out = {
+        "impl": "reference",
+        "metric": "K-TanH Gelem/s and achieved HBM GB/s vs ~8 TB/s peak at 1/2/4/8 B200",
+        "value": round(val, 6), "unit": "Gelem/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": {"workload": cfg.key, "desc": cfg.desc, "elements_per_step": m,
+                   "note": "each step = a bounded sample (first 2^22 elements) of the workload"},
+        "cpu_baseline": {"value": round(val, 6), "unit": "Gelem/s", "cores": 1, "kind": "oracle",
+                         "sample": f"first {m} elements of {cfg.key}, {args.steps} timed steps",
+                         "host_cpu": _cpu_model()},
+        "e2e": {"value": round(val, 6), "unit": "Gelem/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ktanh", choices=["ktanh", "reference"])
+    ap.add_argument("--no-extra", action="store_true", help="skip configs 3-5 side measurements")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    rank, local_rank, world = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU path)")
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=device)
+
+    import paper_1909_07729_b200 as kt
+
+    peak, peak_src = measured_peaks()
+    clocks = ClockSampler(local_rank) if rank == 0 or world > 1 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+
+    K, W = args.steps, args.warmup
+    head_key, head_op = "c2_bf16_2p24", "ktanh_bf16"
+    step = Step(kt, head_key, head_op, device, rank)
+    windows, clk, lps = time_windows(step, K, W, world, device, clocks)
+    ms_win = statistics.median(windows)
+    ms = ms_win / K
+    n_total = step.n * world
+    value = n_total / (ms / 1e3) / 1e9
+    gbs_per_gpu = step.bytes_per_step / (ms / 1e3) / 1e9
+    eager_ms = time_eager(step, K, device)
+    sets = step.sets
+    del step
+    torch.cuda.empty_cache()
+
+    e2e_ms, h2d, d2h = time_e2e(kt, WL.CONFIGS[head_key], "tanh", K, W, world, device, rank)
+    e2e_val = n_total / (e2e_ms / 1e3) / 1e9
+
+    extra = {}
+    if not args.no_extra:
+        for key, op in EXTRA:
+            st = Step(kt, key, op, device, rank)
+            wts, _, _ = time_windows(st, K, W, world, device, None, min_total_s=0.3, max_windows=10)
+            m_ = statistics.median(wts) / K
+            extra[f"{key}:{op}"] = {
+                "elements_per_gpu": st.n, "ms_per_step": round(m_, 5),
+                "gelem_s": round(st.n * world / (m_ / 1e3) / 1e9, 3),
+                "hbm_gbs_per_gpu": round(st.bytes_per_step / (m_ / 1e3) / 1e9, 1),
+                "frac_of_measured": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / peak, 4),
+                "frac_of_8tbs": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / NOMINAL_HBM_GBS, 4),
+                "l2": "inputs larger than L2" if st.sets == 1 else f"{st.sets} rotating sets"}
+            del st
+            torch.cuda.empty_cache()
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(WL.CONFIGS[head_key], "tanh", device)
+
+    if clocks:
+        clocks.stop()
+    traffic, traffic_src = load_traffic(head_op)
+    if rank == 0:
+        out = {
+            "metric": "K-TanH Gelem/s and achieved HBM GB/s vs ~8 TB/s peak at 1/2/4/8 B200",
+            "value": round(value, 3), "unit": "Gelem/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": round(ms, 6), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+            "config": {"workload": head_key, "desc": WL.CONFIGS[head_key].desc,
+                       "elements_per_gpu": WL.CONFIGS[head_key].numel, "call": head_op,
+                       "parallelism": f"{world} independent shards (seed+rank), no collective",
+                       "l2": f"{sets} rotating input/output sets ({sets * 4 * WL.CONFIGS[head_key].numel >> 20} MiB > 4x L2)",
+                       "launch": "CUDA graph of K library calls per timed window",
+                       "windows": len(windows), "window_ms_median": round(ms_win, 5)},
+            "hbm_gbs_per_gpu": round(gbs_per_gpu, 1),
+            "roofline": {"bound": "hbm", "achieved": round(gbs_per_gpu, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(gbs_per_gpu / peak, 4),
+                         "traffic": traffic, "peak_source": peak_src,
+                         "frac_of_8tbs": round(gbs_per_gpu / NOMINAL_HBM_GBS, 4),
+                         "kernel": KERNEL_NAME[head_op],
+                         "algorithmic_bytes_per_launch": 4 * WL.CONFIGS[head_key].numel,
+                         "traffic_source": traffic_src},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_val, 4), "unit": "Gelem/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4),
+                    "path": "kt_apply_host (pinned host buffers, 3-stream chunked pipeline)"},
+            "gpu_launches": int(round(lps * K)),
+            "eager_ms_per_step": round(eager_ms, 6),
+            "clocks": clk,
+            "extra": extra,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

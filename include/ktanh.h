@@ -1,0 +1,189 @@
+/*
+ * ktanh.h -- C ABI of libktanh.so, the B200 (sm_100a) hot path of K-TanH
+ * (Kundu et al., "K-TanH: Efficient TanH for Deep Learning", arXiv 1909.07729).
+ *
+ * Problem statement (Sec. 2.3): replace TanH with a parametric
+ * integer map f(x; theta) ~= TanH(x), theta_t = (E_t, r_t, b_t) fetched from
+ * small parameter tables by a 5-bit index t.  Algorithm 1:
+ *   |x| <  T1 = 0.25 -> y = x                       (line 3, bypass)
+ *   |x| >  T2 = 3.75 -> y = (s, E_bias, 0) = +-1    (line 4, saturate)
+ *   else   t = (2 LSBs of E) : (3 MSBs of M)        (line 6)
+ *          y = (s, E_t, (M >> r_t) + b_t)           (lines 7-8)
+ * Derived activations (Sec. 1):
+ *   Sigmoid(x) = (1 + TanH(x/2))/2,  Swish(x) = x Sigmoid(x),
+ *   GELU(x) ~= x/2 (1 + TanH(sqrt(2/pi)(x + 0.044715 x^3))).
+ *
+ * Plain C: no C++ or torch types cross this boundary.  Every entry point
+ * returns a kt_status; values never cause errors (the maps are total over
+ * all bit patterns, NaN/inf/subnormal behaviour in DESIGN.md readings A2-A6,
+ * A21).  A failing call leaves a human-readable reason in kt_last_error()
+ * (thread-local).
+ *
+ * CONVENTIONS FOR ALL DEVICE ENTRY POINTS
+ *   x, y     device pointers (cudaMalloc / torch CUDA storage), caller-owned,
+ *            contiguous, element-aligned (2 B for BF16, 4 B for F32).  32-byte
+ *            alignment is NOT required (unaligned heads/tails are handled;
+ *            if x and y differ in their offset mod 32 a slower element-wise
+ *            kernel runs).  Both must live on the CURRENT CUDA device.
+ *   aliasing y == x (in place) is allowed; any other overlap -> KT_ERR_ARG.
+ *   n        element count; n == 0 -> KT_OK without a launch.
+ *   NULL     x or y NULL with n > 0 -> KT_ERR_ARG; lut NULL -> KT_ERR_ARG.
+ *   stream   a cudaStream_t passed as void* (NULL = legacy default stream).
+ *            Calls are asynchronous with respect to the host: they enqueue
+ *            one kernel and return.  The library allocates nothing and never
+ *            synchronises on these paths, so calls are CUDA-graph capturable.
+ *   BF16     data are passed as their uint16_t bit patterns.
+ *   errors   KT_ERR_CUDA if the launch fails (cudaGetLastError after launch).
+ *   threads  the LUT handle is immutable: concurrent calls from any host
+ *            thread, on any stream or device, are safe.
+ */
+#ifndef KTANH_H
+#define KTANH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define KT_API __attribute__((visibility("default")))
+#else
+#define KT_API
+#endif
+
+#define KT_ABI_VERSION 1
+
+typedef enum {
+    KT_OK = 0,
+    KT_ERR_ARG = 1,   /* bad pointer, size, overlap, device or enum value  */
+    KT_ERR_LUT = 2,   /* parameter table fails validation (kt_lut_create)   */
+    KT_ERR_CUDA = 3   /* CUDA runtime error (launch, copy, stream, event)   */
+} kt_status;
+
+typedef enum { KT_OP_TANH = 0, KT_OP_SIGMOID = 1, KT_OP_SWISH = 2, KT_OP_GELU = 3 } kt_op;
+typedef enum { KT_BF16 = 0, KT_F32 = 1 } kt_dtype;
+
+/* Opaque, immutable parameter-table handle (host memory).  It holds the
+ * validated (E_t, r_t, b_t) and the per-format packed words that kernels
+ * receive BY VALUE as a kernel parameter, so one handle serves every GPU. */
+typedef struct kt_lut_s *kt_lut;
+
+/* ---------------------------------------------------------------------- */
+/* Parameter tables T_E, T_r, T_b (Alg. 1 line 1; Sec. 2.4). */
+/* ---------------------------------------------------------------------- */
+
+/* Create a handle from three 32-entry host arrays indexed by t (t as in
+ * Alg. 1 line 6: t = ((E & 3) << 3) | (M >> 4) for BF16).  Validation
+ * (KT_ERR_LUT on failure, *out untouched):
+ *   0 <= r_t <= 7 (r_max <= p, Eq. 2), 1 <= E_t <= 127;
+ *   no mantissa overflow/underflow for every input the table path can reach
+ *   (the purpose of b_min/b_max): 0 <= (m >> r_t) + b_t <= 127
+ *   for BF16, 0 <= (M23 >> r_t) + b_t 2^16 < 2^23 for F32;
+ *   E_t == 127 only if every reachable M_o is 0 (keeps |y| <= 1).
+ * The caller keeps ownership of E, r, b; *out must be released with
+ * kt_lut_destroy. */
+KT_API kt_status kt_lut_create(const int32_t E[32], const int32_t r[32], const int32_t b[32],
+                               kt_lut *out);
+
+/* Handle for the paper's Table 1. */
+KT_API kt_status kt_lut_create_paper(kt_lut *out);
+
+/* Copy the handle's tables back out (host arrays of 32). */
+KT_API kt_status kt_lut_get(kt_lut lut, int32_t E[32], int32_t r[32], int32_t b[32]);
+
+/* Release a handle; NULL is a no-op. */
+KT_API void kt_lut_destroy(kt_lut lut);
+
+/* ---------------------------------------------------------------------- */
+/* Elementwise maps over device memory (conventions above).               */
+/* ---------------------------------------------------------------------- */
+
+/* K-TanH, Algorithm 1 on BF16 bit patterns.  Bit-exact
+ * with the paper's algorithm; NaN passes through unchanged (A6). */
+KT_API kt_status ktanh_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream);
+
+/* K-TanH on F32, native reading A8 ("compatible with multiple
+ * such data formats"): same thresholds and 5-bit index (E & 3, top 3
+ * mantissa bits), M_o = (M23 >> r_t) + b_t 2^16. */
+KT_API kt_status ktanh_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream);
+
+/* K-Sigmoid = (1 + K-TanH(x/2))/2 (reading A7).  x/2 is
+ * rounded to the format, the affine step is one fp32 fma rounded once to
+ * the format. */
+KT_API kt_status ksigmoid_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream);
+KT_API kt_status ksigmoid_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream);
+
+/* K-Swish = x K-Sigmoid(x) = hx (1 + K-TanH(RN(hx))), hx = x/2. */
+KT_API kt_status kswish_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream);
+KT_API kt_status kswish_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream);
+
+/* K-GELU = x/2 (1 + K-TanH(u)), u = x fma(C1, x^2, C0) in fp32 with
+ * C0 = f32(sqrt(2/pi)), C1 = f32(sqrt(2/pi) 0.044715) (PAPER.md:69-71,
+ * reading R-GELU-ARG); for BF16, u is rounded to BF16 before K-TanH. */
+KT_API kt_status kgelu_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream);
+KT_API kt_status kgelu_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream);
+
+/* LSTM gate block (BASELINE.json config 4; GNMT LSTM):
+ * x, y are row-major [rows, 4*hidden] BF16; quarter q of every row gets
+ * K-TanH if q == tanh_quarter (the cell candidate g; 2 in PyTorch's
+ * i,f,g,o order) and K-Sigmoid otherwise, in one pass.
+ * KT_ERR_ARG if hidden == 0 or tanh_quarter is not in 0..3. */
+KT_API kt_status klstm_gates_bf16(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,
+                                  int tanh_quarter, kt_lut lut, void *stream);
+
+/* Generic dispatcher over (op, dtype); same contract as the calls above. */
+KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size_t n,
+                          kt_lut lut, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Host-buffer path (the end-to-end call a user with host data makes).    */
+/* ---------------------------------------------------------------------- */
+
+/* y_host = op(x_host) for n elements resident in HOST memory.  The call
+ * splits the data into chunks, and for each chunk enqueues host->device
+ * copy, kernel and device->host copy on one of three internal streams so
+ * that both copy directions and the kernel overlap; the internal streams
+ * are forked from and joined back into `stream`, so the whole operation is
+ * ordered on `stream` and the call returns without waiting: synchronise
+ * `stream` before reading y_host.  x_host / y_host should be pinned
+ * (cudaHostAlloc / torch pin_memory) for asynchronous, full-bandwidth
+ * copies; pageable memory works but the copies become synchronous.
+ * d_work: caller-owned device scratch of work_bytes; at least
+ * 3 * 2 * 4096 * elem_size bytes (KT_ERR_ARG otherwise); larger scratch
+ * gives larger chunks (chunk = work_bytes / (6 * elem_size), rounded down
+ * to a multiple of 256 elements). */
+KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, void *y_host,
+                               size_t n, kt_lut lut, void *d_work, size_t work_bytes,
+                               void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Multi-GPU sharding (host logic; BASELINE.json north_star item (c)).     */
+/* ---------------------------------------------------------------------- */
+
+/* Contiguous flat shard of rank `rank` out of `world`: shard size is
+ * ceil(n / world) rounded up to a multiple of `align` elements (align >= 1;
+ * 16 keeps BF16 shards on 32-byte boundaries); the last shards take the
+ * remainder and may be empty.  No data moves: every rank owns its range
+ * and the path has no reduction, so there is no collective.
+ * KT_ERR_ARG if world < 1, rank outside [0, world), align == 0 or an
+ * output pointer is NULL. */
+KT_API kt_status kt_shard_range(size_t n, int world, int rank, size_t align,
+                                size_t *begin, size_t *count);
+
+/* ---------------------------------------------------------------------- */
+/* Diagnostics                                                            */
+/* ---------------------------------------------------------------------- */
+KT_API const char *kt_status_string(kt_status s);
+KT_API const char *kt_last_error(void);      /* thread-local; "" if none */
+KT_API int kt_abi_version(void);             /* == KT_ABI_VERSION */
+
+/* Number of kernel launches this process has issued through the library
+ * (all devices, all threads); used by bench.py's gpu_launches count. */
+KT_API uint64_t kt_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KTANH_H */

@@ -1,0 +1,245 @@
+"""paper_1909_07729_b200 -- K-TanH (arXiv 1909.07729) on B200 (sm_100a).
+
+Thin ctypes binding over ``libktanh.so`` (C ABI in ``include/ktanh.h``).
+This module only marshals arguments: every step of the K-TanH path runs in
+the library's CUDA kernels.  PyTorch is used for device memory and streams
+only.  There is no CPU fallback: if the library is missing, importing this
+package raises ImportError (build it with ``python -m
+paper_1909_07729_b200.build`` or ``__graft_entry__.build()``).
+
+Names follow the C ABI: ktanh_bf16, ktanh_f32, ksigmoid_bf16, ksigmoid_f32,
+kswish_bf16, kswish_f32, kgelu_bf16, kgelu_f32, klstm_gates_bf16,
+apply_host (kt_apply_host) and shard_range (kt_shard_range).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libktanh.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not found: the K-TanH CUDA library is not built "
+        "(python -m paper_1909_07729_b200.build). There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_c_i32p = ctypes.POINTER(ctypes.c_int32)
+_vp = ctypes.c_void_p
+_sz = ctypes.c_size_t
+
+KT_OK, KT_ERR_ARG, KT_ERR_LUT, KT_ERR_CUDA = 0, 1, 2, 3
+OPS = {"tanh": 0, "sigmoid": 1, "swish": 2, "gelu": 3}
+DTYPES = {"bf16": 0, "f32": 1}
+
+MAP_CALLS = ("ktanh_bf16", "ktanh_f32", "ksigmoid_bf16", "ksigmoid_f32",
+             "kswish_bf16", "kswish_f32", "kgelu_bf16", "kgelu_f32")
+EXPORTS = MAP_CALLS + ("kt_lut_create", "kt_lut_create_paper", "kt_lut_get", "kt_lut_destroy",
+                       "klstm_gates_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
+                       "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count")
+
+for _name in MAP_CALLS:
+    _f = getattr(_lib, _name)
+    _f.argtypes = [_vp, _vp, _sz, _vp, _vp]
+    _f.restype = ctypes.c_int
+_lib.kt_lut_create.argtypes = [_c_i32p, _c_i32p, _c_i32p, ctypes.POINTER(_vp)]
+_lib.kt_lut_create.restype = ctypes.c_int
+_lib.kt_lut_create_paper.argtypes = [ctypes.POINTER(_vp)]
+_lib.kt_lut_create_paper.restype = ctypes.c_int
+_lib.kt_lut_get.argtypes = [_vp, _c_i32p, _c_i32p, _c_i32p]
+_lib.kt_lut_get.restype = ctypes.c_int
+_lib.kt_lut_destroy.argtypes = [_vp]
+_lib.kt_lut_destroy.restype = None
+_lib.klstm_gates_bf16.argtypes = [_vp, _vp, _sz, _sz, ctypes.c_int, _vp, _vp]
+_lib.klstm_gates_bf16.restype = ctypes.c_int
+_lib.kt_apply.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp, _vp]
+_lib.kt_apply.restype = ctypes.c_int
+_lib.kt_apply_host.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp, _vp, _sz, _vp]
+_lib.kt_apply_host.restype = ctypes.c_int
+_lib.kt_shard_range.argtypes = [_sz, ctypes.c_int, ctypes.c_int, _sz, ctypes.POINTER(_sz),
+                                ctypes.POINTER(_sz)]
+_lib.kt_shard_range.restype = ctypes.c_int
+_lib.kt_status_string.argtypes = [ctypes.c_int]
+_lib.kt_status_string.restype = ctypes.c_char_p
+_lib.kt_last_error.argtypes = []
+_lib.kt_last_error.restype = ctypes.c_char_p
+_lib.kt_abi_version.argtypes = []
+_lib.kt_abi_version.restype = ctypes.c_int
+_lib.kt_launch_count.argtypes = []
+_lib.kt_launch_count.restype = ctypes.c_uint64
+
+
+class KTanhError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib.kt_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {_lib.kt_status_string(status).decode()}: {msg}")
+
+
+def _check(status: int, where: str):
+    if status != KT_OK:
+        raise KTanhError(status, where)
+
+
+def abi_version() -> int:
+    return _lib.kt_abi_version()
+
+
+def launch_count() -> int:
+    """Kernel launches issued by the library in this process."""
+    return int(_lib.kt_launch_count())
+
+
+class Lut:
+    """Immutable parameter-table handle (T_E, T_r, T_b), Alg. 1 line 1."""
+
+    def __init__(self, handle: int):
+        self._h = _vp(handle)
+
+    @classmethod
+    def paper(cls) -> "Lut":
+        """Table 1 of the paper."""
+        h = _vp()
+        _check(_lib.kt_lut_create_paper(ctypes.byref(h)), "kt_lut_create_paper")
+        return cls(h.value)
+
+    @classmethod
+    def from_tables(cls, E, r, b) -> "Lut":
+        arr = [(ctypes.c_int32 * 32)(*[int(v) for v in a]) for a in (E, r, b)]
+        if any(len(a) != 32 for a in (E, r, b)):
+            raise ValueError("tables must have 32 entries")
+        h = _vp()
+        _check(_lib.kt_lut_create(arr[0], arr[1], arr[2], ctypes.byref(h)), "kt_lut_create")
+        return cls(h.value)
+
+    def tables(self):
+        E, r, b = ((ctypes.c_int32 * 32)() for _ in range(3))
+        _check(_lib.kt_lut_get(self._h, E, r, b), "kt_lut_get")
+        return list(E), list(r), list(b)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.kt_lut_destroy(h)
+            self._h = _vp()
+
+
+_default_lut = None
+
+
+def paper_lut() -> Lut:
+    global _default_lut
+    if _default_lut is None:
+        _default_lut = Lut.paper()
+    return _default_lut
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _prep(x, out, dtype):
+    import torch
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError("x must be a CUDA tensor (no CPU path)")
+    if x.dtype != dtype:
+        raise TypeError(f"expected {dtype}, got {x.dtype}")
+    if not x.is_contiguous():
+        raise ValueError("x must be contiguous")
+    if out is None:
+        out = torch.empty_like(x)
+    elif (out.dtype != dtype or not out.is_cuda or not out.is_contiguous()
+          or out.numel() != x.numel() or out.device != x.device):
+        raise ValueError("out must be a contiguous CUDA tensor like x")
+    return out
+
+
+def _make_call(name, dtype_name):
+    fn = getattr(_lib, name)
+
+    def call(x, out=None, lut: Lut | None = None, stream=None):
+        import torch
+        dt = torch.bfloat16 if dtype_name == "bf16" else torch.float32
+        out = _prep(x, out, dt)
+        lut = lut or paper_lut()
+        with torch.cuda.device(x.device):
+            _check(fn(x.data_ptr(), out.data_ptr(), x.numel(), lut.handle, _stream_ptr(stream)), name)
+        return out
+
+    call.__name__ = name
+    call.__doc__ = f"{name}(x, out=None, lut=None, stream=None) -> out   (C ABI: include/ktanh.h)"
+    return call
+
+
+ktanh_bf16 = _make_call("ktanh_bf16", "bf16")
+ktanh_f32 = _make_call("ktanh_f32", "f32")
+ksigmoid_bf16 = _make_call("ksigmoid_bf16", "bf16")
+ksigmoid_f32 = _make_call("ksigmoid_f32", "f32")
+kswish_bf16 = _make_call("kswish_bf16", "bf16")
+kswish_f32 = _make_call("kswish_f32", "f32")
+kgelu_bf16 = _make_call("kgelu_bf16", "bf16")
+kgelu_f32 = _make_call("kgelu_f32", "f32")
+
+
+def klstm_gates_bf16(x, hidden: int, tanh_quarter: int = 2, out=None, lut: Lut | None = None,
+                     stream=None):
+    """[..., 4*hidden] BF16 gate block: K-TanH on quarter `tanh_quarter`, K-Sigmoid elsewhere."""
+    import torch
+    out = _prep(x, out, torch.bfloat16)
+    if x.numel() % (4 * hidden):
+        raise ValueError("numel must be a multiple of 4*hidden")
+    lut = lut or paper_lut()
+    with torch.cuda.device(x.device):
+        _check(_lib.klstm_gates_bf16(x.data_ptr(), out.data_ptr(), x.numel() // (4 * hidden),
+                                     hidden, tanh_quarter, lut.handle, _stream_ptr(stream)),
+               "klstm_gates_bf16")
+    return out
+
+
+def apply(op: str, x, out=None, lut: Lut | None = None, stream=None):
+    """Generic kt_apply dispatch by op name and the tensor's dtype."""
+    import torch
+    dname = "bf16" if x.dtype == torch.bfloat16 else "f32"
+    out = _prep(x, out, x.dtype)
+    lut = lut or paper_lut()
+    with torch.cuda.device(x.device):
+        _check(_lib.kt_apply(OPS[op], DTYPES[dname], x.data_ptr(), out.data_ptr(), x.numel(),
+                             lut.handle, _stream_ptr(stream)), "kt_apply")
+    return out
+
+
+def apply_host(op: str, x_host, y_host, work, lut: Lut | None = None, stream=None):
+    """kt_apply_host: x_host/y_host are (pinned) CPU tensors, `work` a CUDA uint8
+    scratch tensor on the current device.  Asynchronous on `stream`."""
+    import torch
+    if x_host.is_cuda or y_host.is_cuda or not work.is_cuda:
+        raise TypeError("x_host / y_host must be CPU tensors, work a CUDA tensor")
+    if x_host.dtype != y_host.dtype or x_host.numel() != y_host.numel():
+        raise ValueError("x_host and y_host must match")
+    dname = "bf16" if x_host.dtype == torch.bfloat16 else "f32"
+    lut = lut or paper_lut()
+    with torch.cuda.device(work.device):
+        _check(_lib.kt_apply_host(OPS[op], DTYPES[dname], x_host.data_ptr(), y_host.data_ptr(),
+                                  x_host.numel(), lut.handle, work.data_ptr(),
+                                  work.numel() * work.element_size(), _stream_ptr(stream)),
+               "kt_apply_host")
+    return y_host
+
+
+def shard_range(n: int, world: int, rank: int, align: int = 16):
+    """kt_shard_range: (begin, count) of rank's contiguous shard."""
+    b, c = _sz(), _sz()
+    _check(_lib.kt_shard_range(n, world, rank, align, ctypes.byref(b), ctypes.byref(c)),
+           "kt_shard_range")
+    return b.value, c.value

@@ -1,0 +1,360 @@
+// kt_api.cu -- the C ABI of libktanh.so (declared in include/ktanh.h):
+// parameter-table handles, argument validation, dispatch to the kernel
+// launchers, the pipelined host-buffer path and the shard helper.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "ktanh.h"
+#include "kt_internal.h"
+
+namespace kt {
+uint64_t launch_count();
+}
+
+struct kt_lut_s {
+  int32_t E[32], r[32], b[32];
+  kt::LutWords words;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+kt_status fail(kt_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+kt_status fail(kt_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+kt_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(KT_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// Table 1 of the paper, indexed by t = (E&3):(M>>4).
+// This is the product's own transcription (the test oracle keeps another).
+constexpr int32_t kPaperE[32] = {126, 126, 126, 126, 126, 126, 126, 126,   // 00000-00111
+                                 125, 125, 125, 125, 125, 125, 125, 125,   // 01000-01111
+                                 125, 126, 126, 126, 126, 126, 126, 126,   // 10000-10111
+                                 126, 126, 126, 126, 126, 126, 126, 126};  // 11000-11111
+constexpr int32_t kPaperR[32] = {2, 4, 4, 4, 6, 6, 6, 6,
+                                 1, 0, 0, 0, 0, 0, 0, 0,
+                                 0, 1, 1, 1, 1, 1, 1, 1,
+                                 0, 1, 1, 1, 2, 2, 2, 4};
+constexpr int32_t kPaperB[32] = {119, 122, 123, 123, 126, 126, 126, 126,
+                                 1,   -4,  -6,  -7,  -10, -12, -15, -18,
+                                 112, -4,  -1,  2,   3,   4,   4,   4,
+                                 65,  72,  73,  73,  88,  89,  89,  110};
+
+// Input exponent of interval t on the table path: t >> 3 = E & 3 with
+// E in {125, 126, 127, 128} (T1 = 2^-2 .. T2 = 3.75 < 2^2).
+inline int e_in(int t) { return 125 + (((t >> 3) + 3) & 3); }
+
+// Mantissa range [lo, hi] (p = 7) that the table path can reach in interval t:
+// all 16 values of the 3 index bits' sub-range, except t = 00111 (E = 128),
+// where only M = 0x70 (x = 3.75 = T2) is <= T2.
+inline void reach(int t, int *lo, int *hi) {
+  const int v = t & 7;
+  *lo = 16 * v;
+  *hi = 16 * v + 15;
+  if (e_in(t) == 128 && v == 7) *hi = *lo;
+}
+
+kt_status validate_and_pack(const int32_t *E, const int32_t *r, const int32_t *b, kt_lut_s *L) {
+  for (int t = 0; t < 32; ++t) {
+    if (r[t] < 0 || r[t] > 7) return fail(KT_ERR_LUT, "r[%d] = %d outside [0, 7]", t, r[t]);
+    if (E[t] < 1 || E[t] > 127) return fail(KT_ERR_LUT, "E[%d] = %d outside [1, 127]", t, E[t]);
+    int lo, hi;
+    reach(t, &lo, &hi);
+    for (int m = lo; m <= hi; ++m) {
+      const int mo = (m >> r[t]) + b[t];
+      if (mo < 0 || mo > 127)
+        return fail(KT_ERR_LUT, "entry %d: (m=%d >> r=%d) + b=%d = %d leaves [0, 127]", t, m,
+                    r[t], b[t], mo);
+      if (E[t] == 127 && mo != 0)
+        return fail(KT_ERR_LUT, "entry %d: E=127 with M_o=%d != 0 gives |y| > 1", t, mo);
+    }
+    // F32 (p = 23): endpoints of the reachable M23 range (the map is monotone in M23).
+    const int64_t lo23 = (int64_t)lo << 16;
+    const int64_t hi23 = (t == 7) ? lo23 : (((int64_t)hi << 16) | 0xFFFF);
+    const int64_t mlo = (lo23 >> r[t]) + (int64_t)b[t] * 65536;
+    const int64_t mhi = (hi23 >> r[t]) + (int64_t)b[t] * 65536;
+    if (mlo < 0 || mhi > 0x7FFFFF)
+      return fail(KT_ERR_LUT, "entry %d overflows the F32 mantissa", t);
+    if (E[t] == 127 && mhi != 0)
+      return fail(KT_ERR_LUT, "entry %d: E=127 gives |y| > 1 on F32", t);
+  }
+  for (int t = 0; t < 32; ++t) {
+    L->E[t] = E[t];
+    L->r[t] = r[t];
+    L->b[t] = b[t];
+    const int ei = e_in(t);
+    const int32_t c16 = (E[t] << 7) + b[t] - (ei << (7 - r[t]));
+    L->words.bf16[t] = ((uint32_t)c16 << 16) | (uint32_t)r[t];
+    L->words.f32K[t] = 1u << (31 - r[t]);
+    const int64_t c32 = ((int64_t)E[t] << 23) + (int64_t)b[t] * 65536 - ((int64_t)ei << (23 - r[t]));
+    L->words.f32C[t] = (uint32_t)(c32 & 0xFFFFFFFFll);
+  }
+  return KT_OK;
+}
+
+// ---- device info ----------------------------------------------------------
+constexpr int kMaxDev = 64;
+int g_sm_count[kMaxDev];  // 0 = unknown
+std::mutex g_dev_mu;
+
+kt_status launch_info(kt::LaunchInfo *li) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= kMaxDev) return fail(KT_ERR_ARG, "device %d out of range", dev);
+  int sm = __atomic_load_n(&g_sm_count[dev], __ATOMIC_ACQUIRE);
+  if (sm == 0) {
+    e = cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    __atomic_store_n(&g_sm_count[dev], sm, __ATOMIC_RELEASE);
+  }
+  li->device = dev;
+  li->sm_count = sm;
+  return KT_OK;
+}
+
+// x, y must be device (or managed) memory of the current device.
+kt_status check_device_ptr(const void *p, int dev, const char *name) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(KT_ERR_ARG, "%s: not a CUDA pointer (%s)", name, cudaGetErrorName(e));
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+    return fail(KT_ERR_ARG, "%s: not device memory", name);
+  if (a.type == cudaMemoryTypeDevice && a.device != dev)
+    return fail(KT_ERR_ARG, "%s lives on device %d, current device is %d", name, a.device, dev);
+  return KT_OK;
+}
+
+kt_status check_buffers(const void *x, const void *y, size_t n, size_t es, kt::LaunchInfo *li) {
+  if (!x || !y) return fail(KT_ERR_ARG, "NULL pointer with n = %zu", n);
+  const uintptr_t xa = (uintptr_t)x, ya = (uintptr_t)y;
+  if (xa % es || ya % es) return fail(KT_ERR_ARG, "pointers must be %zu-byte aligned", es);
+  if (n > (SIZE_MAX / es)) return fail(KT_ERR_ARG, "n too large");
+  const size_t bytes = n * es;
+  if (x != y && xa < ya + bytes && ya < xa + bytes)
+    return fail(KT_ERR_ARG, "x and y overlap without being equal");
+  kt_status s = launch_info(li);
+  if (s != KT_OK) return s;
+  if ((s = check_device_ptr(x, li->device, "x")) != KT_OK) return s;
+  if ((s = check_device_ptr(y, li->device, "y")) != KT_OK) return s;
+  return KT_OK;
+}
+
+kt_status run_map(int op, int fmt, const void *x, void *y, size_t n, kt_lut lut, void *stream) {
+  if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (op < 0 || op > 3 || fmt < 0 || fmt > 1) return fail(KT_ERR_ARG, "bad op/dtype");
+  if (n == 0) return KT_OK;
+  const size_t es = fmt == kt::FMT_BF16 ? 2 : 4;
+  kt::LaunchInfo li;
+  kt_status s = check_buffers(x, y, n, es, &li);
+  if (s != KT_OK) return s;
+  cudaError_t e = kt::launch_map(op, fmt, x, y, n, lut->words, (cudaStream_t)stream, li);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return KT_OK;
+}
+
+// ---- host-buffer path -------------------------------------------------------
+constexpr int kStages = 3;
+struct HostPipe {
+  bool init = false;
+  cudaStream_t st[kStages];
+  cudaEvent_t fork, join[kStages];
+  std::mutex mu;
+};
+HostPipe g_pipe[kMaxDev];
+
+kt_status pipe_for(int dev, HostPipe **out) {
+  HostPipe &p = g_pipe[dev];
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  if (!p.init) {
+    cudaError_t e;
+    for (int i = 0; i < kStages; ++i)
+      if ((e = cudaStreamCreateWithFlags(&p.st[i], cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(e, "cudaStreamCreate");
+    if ((e = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "cudaEventCreate");
+    for (int i = 0; i < kStages; ++i)
+      if ((e = cudaEventCreateWithFlags(&p.join[i], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "cudaEventCreate");
+    p.init = true;
+  }
+  *out = &p;
+  return KT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+KT_API kt_status kt_lut_create(const int32_t E[32], const int32_t r[32], const int32_t b[32],
+                               kt_lut *out) {
+  if (!E || !r || !b || !out) return fail(KT_ERR_ARG, "NULL argument");
+  kt_lut_s tmp;
+  kt_status s = validate_and_pack(E, r, b, &tmp);
+  if (s != KT_OK) return s;
+  kt_lut_s *L = new (std::nothrow) kt_lut_s(tmp);
+  if (!L) return fail(KT_ERR_ARG, "out of host memory");
+  *out = L;
+  return KT_OK;
+}
+
+KT_API kt_status kt_lut_create_paper(kt_lut *out) {
+  return kt_lut_create(kPaperE, kPaperR, kPaperB, out);
+}
+
+KT_API kt_status kt_lut_get(kt_lut lut, int32_t E[32], int32_t r[32], int32_t b[32]) {
+  if (!lut || !E || !r || !b) return fail(KT_ERR_ARG, "NULL argument");
+  memcpy(E, lut->E, sizeof(lut->E));
+  memcpy(r, lut->r, sizeof(lut->r));
+  memcpy(b, lut->b, sizeof(lut->b));
+  return KT_OK;
+}
+
+KT_API void kt_lut_destroy(kt_lut lut) { delete lut; }
+
+KT_API kt_status ktanh_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream) {
+  return run_map(kt::OP_TANH, kt::FMT_BF16, x, y, n, lut, stream);
+}
+KT_API kt_status ktanh_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream) {
+  return run_map(kt::OP_TANH, kt::FMT_F32, x, y, n, lut, stream);
+}
+KT_API kt_status ksigmoid_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream) {
+  return run_map(kt::OP_SIGMOID, kt::FMT_BF16, x, y, n, lut, stream);
+}
+KT_API kt_status ksigmoid_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream) {
+  return run_map(kt::OP_SIGMOID, kt::FMT_F32, x, y, n, lut, stream);
+}
+KT_API kt_status kswish_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream) {
+  return run_map(kt::OP_SWISH, kt::FMT_BF16, x, y, n, lut, stream);
+}
+KT_API kt_status kswish_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream) {
+  return run_map(kt::OP_SWISH, kt::FMT_F32, x, y, n, lut, stream);
+}
+KT_API kt_status kgelu_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream) {
+  return run_map(kt::OP_GELU, kt::FMT_BF16, x, y, n, lut, stream);
+}
+KT_API kt_status kgelu_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream) {
+  return run_map(kt::OP_GELU, kt::FMT_F32, x, y, n, lut, stream);
+}
+
+KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size_t n, kt_lut lut,
+                          void *stream) {
+  return run_map((int)op, (int)dtype, x, y, n, lut, stream);
+}
+
+KT_API kt_status klstm_gates_bf16(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,
+                                  int tanh_quarter, kt_lut lut, void *stream) {
+  if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (hidden == 0) return fail(KT_ERR_ARG, "hidden == 0");
+  if (tanh_quarter < 0 || tanh_quarter > 3) return fail(KT_ERR_ARG, "tanh_quarter not in 0..3");
+  if (rows > SIZE_MAX / 4 / hidden) return fail(KT_ERR_ARG, "size overflow");
+  const size_t n = rows * 4 * hidden;
+  if (n == 0) return KT_OK;
+  kt::LaunchInfo li;
+  kt_status s = check_buffers(x, y, n, 2, &li);
+  if (s != KT_OK) return s;
+  cudaError_t e =
+      kt::launch_lstm(x, y, rows, hidden, tanh_quarter, lut->words, (cudaStream_t)stream, li);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return KT_OK;
+}
+
+KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, void *y_host, size_t n,
+                               kt_lut lut, void *d_work, size_t work_bytes, void *stream) {
+  if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if ((int)op < 0 || (int)op > 3 || (int)dtype < 0 || (int)dtype > 1)
+    return fail(KT_ERR_ARG, "bad op/dtype");
+  if (n == 0) return KT_OK;
+  if (!x_host || !y_host || !d_work) return fail(KT_ERR_ARG, "NULL pointer");
+  const size_t es = dtype == KT_BF16 ? 2 : 4;
+  size_t chunk = work_bytes / (2 * kStages * es);
+  chunk -= chunk % 256;
+  if (chunk < 4096) return fail(KT_ERR_ARG, "work_bytes too small (need >= %zu)", 2 * kStages * es * 4096);
+  kt::LaunchInfo li;
+  kt_status s = launch_info(&li);
+  if (s != KT_OK) return s;
+  if ((s = check_device_ptr(d_work, li.device, "d_work")) != KT_OK) return s;
+  HostPipe *p;
+  if ((s = pipe_for(li.device, &p)) != KT_OK) return s;
+  std::lock_guard<std::mutex> g(p->mu);
+  cudaStream_t caller = (cudaStream_t)stream;
+  cudaError_t e;
+  if ((e = cudaEventRecord(p->fork, caller)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  for (int i = 0; i < kStages; ++i)
+    if ((e = cudaStreamWaitEvent(p->st[i], p->fork, 0)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamWaitEvent");
+  const char *xh = static_cast<const char *>(x_host);
+  char *yh = static_cast<char *>(y_host);
+  char *work = static_cast<char *>(d_work);
+  size_t k = 0;
+  for (size_t off = 0; off < n; off += chunk, ++k) {
+    const size_t cnt = (n - off < chunk) ? n - off : chunk;
+    const int st = (int)(k % kStages);
+    cudaStream_t ss = p->st[st];
+    char *dx = work + (size_t)st * 2 * chunk * es;
+    char *dy = dx + chunk * es;
+    if ((e = cudaMemcpyAsync(dx, xh + off * es, cnt * es, cudaMemcpyHostToDevice, ss)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync H2D");
+    if ((e = kt::launch_map((int)op, (int)dtype, dx, dy, cnt, lut->words, ss, li)) != cudaSuccess)
+      return cuda_fail(e, "kernel launch");
+    if ((e = cudaMemcpyAsync(yh + off * es, dy, cnt * es, cudaMemcpyDeviceToHost, ss)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync D2H");
+  }
+  for (int i = 0; i < kStages; ++i) {
+    if ((e = cudaEventRecord(p->join[i], p->st[i])) != cudaSuccess)
+      return cuda_fail(e, "cudaEventRecord");
+    if ((e = cudaStreamWaitEvent(caller, p->join[i], 0)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamWaitEvent");
+  }
+  return KT_OK;
+}
+
+KT_API kt_status kt_shard_range(size_t n, int world, int rank, size_t align, size_t *begin,
+                                size_t *count) {
+  if (world < 1 || rank < 0 || rank >= world || align == 0 || !begin || !count)
+    return fail(KT_ERR_ARG, "bad shard arguments");
+  size_t per = n / (size_t)world + (n % (size_t)world != 0);
+  per = (per + align - 1) / align * align;
+  size_t b = per * (size_t)rank;
+  if (b > n) b = n;
+  size_t c = n - b;
+  if (c > per) c = per;
+  *begin = b;
+  *count = c;
+  return KT_OK;
+}
+
+KT_API const char *kt_status_string(kt_status s) {
+  switch (s) {
+    case KT_OK: return "KT_OK";
+    case KT_ERR_ARG: return "KT_ERR_ARG";
+    case KT_ERR_LUT: return "KT_ERR_LUT";
+    case KT_ERR_CUDA: return "KT_ERR_CUDA";
+  }
+  return "KT_UNKNOWN";
+}
+
+KT_API const char *kt_last_error(void) { return g_err.c_str(); }
+KT_API int kt_abi_version(void) { return KT_ABI_VERSION; }
+KT_API uint64_t kt_launch_count(void) { return kt::launch_count(); }
+
+}  // extern "C"

@@ -1,0 +1,239 @@
+// kt_device.cuh -- sm_100a device code for the K-TanH element maps.
+//
+// Everything here works on the input's BITS (Sec. 2.3):
+// the BF16 core handles two elements packed in one 32-bit register, the F32
+// core one element.  All selects are branch-free; the only memory touched
+// per element is the streaming load/store in kt_kernels.cu, the parameter
+// table lives in one register per lane and is read with a warp shuffle.
+#pragma once
+
+#include <cstdint>
+
+#include "kt_internal.h"
+
+namespace kt {
+
+// ---------------------------------------------------------------- helpers --
+
+// theta_t fetch (Alg. 1 line 7): lane t of the warp holds entry t.  The
+// shuffle lane index is taken from bits [4:0] of `src_lane` (c = 0x1f, no
+// segment mask), so callers pass `x >> 4` / `x >> 20` without masking.
+__device__ __forceinline__ uint32_t shfl_lut(uint32_t lane_word, uint32_t src_lane) {
+  uint32_t d;
+  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;"
+               : "=r"(d) : "r"(lane_word), "r"(src_lane));
+  return d;
+}
+
+// a >> (n mod 32)   (one SHF.R.W; the LUT word keeps r_t in its low bits)
+__device__ __forceinline__ uint32_t shr_wrap(uint32_t a, uint32_t n) {
+  uint32_t d;
+  asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(0u), "r"(n));
+  return d;
+}
+
+// Per-half BF16 compares producing 0xFFFF / 0x0000 masks (HSET2.BF16_V2).
+// ltu: less-than OR unordered -> NaN lands in the bypass mask (reading A6).
+__device__ __forceinline__ uint32_t hset2_ltu(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("set.ltu.u32.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t hset2_gt(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("set.gt.u32.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+// m ? a : b, bitwise (one LOP3)
+__device__ __forceinline__ uint32_t bsel(uint32_t m, uint32_t a, uint32_t b) {
+  return (m & a) | (~m & b);
+}
+
+// two fp32 -> packed bf16x2, round-to-nearest-even (F2FP.BF16.F32.PACK_AB)
+__device__ __forceinline__ uint32_t pack_bf16x2(float hi, float lo) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+__device__ __forceinline__ float lo_f32(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float hi_f32(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// Thresholds: T1 = 0.25 = 0x3E80, T2 = 3.75 = 0x4070 (BF16);
+// 0x3E800000 / 0x40700000 (F32).  +-1 = (s, E_bias = 127, 0).
+constexpr uint32_t kT1x2 = 0x3E803E80u;
+constexpr uint32_t kT2x2 = 0x40704070u;
+constexpr uint32_t kOnex2 = 0x3F803F80u;
+constexpr uint32_t kSignx2 = 0x80008000u;
+constexpr uint32_t kMagx2 = 0x7FFF7FFFu;
+constexpr uint32_t kT1f = 0x3E800000u;
+constexpr uint32_t kT2f = 0x40700000u;
+constexpr uint32_t kInff = 0x7F800000u;
+
+// GELU argument constants (a = 0.044715):
+// C0 = RN32(sqrt(2/pi)), C1 = RN32(sqrt(2/pi) * a)
+constexpr uint32_t kGeluC0Bits = 0x3F4C422Au;
+constexpr uint32_t kGeluC1Bits = 0x3D122279u;
+
+// ------------------------------------------------------------- K-TanH core --
+
+// Algorithm 1 on two BF16 values packed in x.
+//   lw = this lane's word LutWords::bf16[lane] = (C_t << 16) | r_t.
+__device__ __forceinline__ uint32_t ktanh_bf16x2(uint32_t x, uint32_t lw) {
+  const uint32_t mag = x & kMagx2;                 // |x| bits of both halves
+  // line 6: t = bits [8:4] of each half = (E & 3) : (M >> 4)
+  // line 7: theta_t by shuffle from lane t
+  const uint32_t Ll = shfl_lut(lw, x >> 4);
+  const uint32_t Lh = shfl_lut(lw, x >> 20);
+  // line 8: E_o, M_o = E_t, (M >> r_t) + b_t  ==  C_t + (|x| >> r_t)
+  const uint32_t Kl = shr_wrap(0x10000u, Ll);      // 2^(16 - r_t)
+  const uint32_t Kh = shr_wrap(0x10000u, Lh);
+  const uint32_t dl = (mag & 0xffffu) * Kl + Ll;   // hi16 = C_t + (|x_lo| >> r_t)
+  const uint32_t dh = (mag >> 16) * Kh + Lh;       // hi16 = C_t + (|x_hi| >> r_t)
+  const uint32_t ymag = __byte_perm(dl, dh, 0x7632);
+  // lines 3-4: region masks per half
+  const uint32_t byp = hset2_ltu(mag, kT1x2);      // |x| < T1, or NaN
+  const uint32_t sat = hset2_gt(mag, kT2x2);       // |x| > T2, incl. inf
+  const uint32_t m2 = bsel(sat, kOnex2, ymag);     // line 4: (s, E_bias, 0)
+  const uint32_t m3 = bsel(byp, mag, m2);          // line 3: y = x
+  return (x & kSignx2) | m3;                       // s_o = s_i
+}
+
+// Algorithm 1 on one F32 (native reading A8).  lk = f32K[lane], lc = f32C[lane].
+__device__ __forceinline__ uint32_t ktanh_f32(uint32_t u, uint32_t lk, uint32_t lc) {
+  const uint32_t mag = u & 0x7fffffffu;
+  const uint32_t s = u & 0x80000000u;
+  const uint32_t K = shfl_lut(lk, u >> 20);        // line 6-7, t = bits [24:20]
+  const uint32_t C = shfl_lut(lc, u >> 20);
+  const uint32_t ym = __umulhi(u << 1, K) + C;     // line 8: C_t + (|x| >> r_t)
+  uint32_t y = s | ym;
+  y = (mag > kT2f) ? (s | 0x3F800000u) : y;        // line 4 (NaN overridden below)
+  y = (mag < kT1f || mag > kInff) ? u : y;         // line 3, NaN passthrough (A6)
+  return y;
+}
+
+// ------------------------------------------------------- derived (Sec. 1) --
+// PAPER.md:60-71.  Sigmoid(x) = (1 + TanH(x/2))/2, Swish = x Sigmoid(x),
+// GELU ~= x/2 (1 + TanH(sqrt(2/pi)(x + a x^3))).  fp32 scaffolding with
+// explicit _rn intrinsics (no contraction), one rounding to the format.
+
+__device__ __forceinline__ uint32_t ksigmoid_bf16x2(uint32_t x, uint32_t lw) {
+  const float xl = lo_f32(x), xh = hi_f32(x);
+  const uint32_t h = pack_bf16x2(__fmul_rn(xh, 0.5f), __fmul_rn(xl, 0.5f));   // RN_bf16(x/2)
+  const uint32_t t = ktanh_bf16x2(h, lw);
+  return pack_bf16x2(__fmaf_rn(0.5f, hi_f32(t), 0.5f), __fmaf_rn(0.5f, lo_f32(t), 0.5f));
+}
+
+__device__ __forceinline__ uint32_t kswish_bf16x2(uint32_t x, uint32_t lw) {
+  const float hl = __fmul_rn(lo_f32(x), 0.5f), hh = __fmul_rn(hi_f32(x), 0.5f);  // exact
+  const uint32_t t = ktanh_bf16x2(pack_bf16x2(hh, hl), lw);
+  return pack_bf16x2(__fmaf_rn(hh, hi_f32(t), hh), __fmaf_rn(hl, lo_f32(t), hl));
+}
+
+__device__ __forceinline__ float gelu_arg(float x) {
+  const float x2 = __fmul_rn(x, x);
+  const float p = __fmaf_rn(__uint_as_float(kGeluC1Bits), x2, __uint_as_float(kGeluC0Bits));
+  return __fmul_rn(x, p);
+}
+
+__device__ __forceinline__ uint32_t kgelu_bf16x2(uint32_t x, uint32_t lw) {
+  const float xl = lo_f32(x), xh = hi_f32(x);
+  const uint32_t u = pack_bf16x2(gelu_arg(xh), gelu_arg(xl));                 // RN_bf16(u)
+  const uint32_t t = ktanh_bf16x2(u, lw);
+  const float hl = __fmul_rn(xl, 0.5f), hh = __fmul_rn(xh, 0.5f);
+  return pack_bf16x2(__fmaf_rn(hh, hi_f32(t), hh), __fmaf_rn(hl, lo_f32(t), hl));
+}
+
+__device__ __forceinline__ uint32_t ksigmoid_f32(uint32_t u, uint32_t lk, uint32_t lc) {
+  const float h = __fmul_rn(__uint_as_float(u), 0.5f);
+  const float t = __uint_as_float(ktanh_f32(__float_as_uint(h), lk, lc));
+  return __float_as_uint(__fmaf_rn(0.5f, t, 0.5f));
+}
+
+__device__ __forceinline__ uint32_t kswish_f32(uint32_t u, uint32_t lk, uint32_t lc) {
+  const float hx = __fmul_rn(__uint_as_float(u), 0.5f);
+  const float t = __uint_as_float(ktanh_f32(__float_as_uint(hx), lk, lc));
+  return __float_as_uint(__fmaf_rn(hx, t, hx));
+}
+
+__device__ __forceinline__ uint32_t kgelu_f32(uint32_t u, uint32_t lk, uint32_t lc) {
+  const float x = __uint_as_float(u);
+  const float t = __uint_as_float(ktanh_f32(__float_as_uint(gelu_arg(x)), lk, lc));
+  const float hx = __fmul_rn(x, 0.5f);
+  return __float_as_uint(__fmaf_rn(hx, t, hx));
+}
+
+// ------------------------------------------------------------- dispatch ----
+
+struct LaneLut {
+  uint32_t w16, k32, c32;
+};
+
+template <int OP>
+__device__ __forceinline__ uint32_t apply_bf16x2(uint32_t x, const LaneLut &L) {
+  if (OP == OP_TANH) return ktanh_bf16x2(x, L.w16);
+  if (OP == OP_SIGMOID) return ksigmoid_bf16x2(x, L.w16);
+  if (OP == OP_SWISH) return kswish_bf16x2(x, L.w16);
+  return kgelu_bf16x2(x, L.w16);
+}
+
+template <int OP>
+__device__ __forceinline__ uint32_t apply_f32(uint32_t u, const LaneLut &L) {
+  if (OP == OP_TANH) return ktanh_f32(u, L.k32, L.c32);
+  if (OP == OP_SIGMOID) return ksigmoid_f32(u, L.k32, L.c32);
+  if (OP == OP_SWISH) return kswish_f32(u, L.k32, L.c32);
+  return kgelu_f32(u, L.k32, L.c32);
+}
+
+// One 32-bit word: two BF16 or one F32.
+template <int OP, int FMT>
+__device__ __forceinline__ uint32_t apply_word(uint32_t w, const LaneLut &L) {
+  if (FMT == FMT_BF16) return apply_bf16x2<OP>(w, L);
+  return apply_f32<OP>(w, L);
+}
+
+// LSTM gate pair: K-TanH (is_tanh) or K-Sigmoid, same core, per-lane choice.
+__device__ __forceinline__ uint32_t lstm_bf16x2(uint32_t x, uint32_t lw, bool is_tanh) {
+  uint32_t h = x;
+  if (!is_tanh) {
+    h = pack_bf16x2(__fmul_rn(hi_f32(x), 0.5f), __fmul_rn(lo_f32(x), 0.5f));
+  }
+  const uint32_t t = ktanh_bf16x2(h, lw);
+  if (is_tanh) return t;
+  return pack_bf16x2(__fmaf_rn(0.5f, hi_f32(t), 0.5f), __fmaf_rn(0.5f, lo_f32(t), 0.5f));
+}
+
+// ------------------------------------------------------ streaming memory --
+
+// 32-byte (256-bit) predicated global load / store (LDG.E.256 / STG.E.256).
+// NC: read-only non-coherent path, used only when y does not alias x.
+template <bool NC>
+__device__ __forceinline__ void ld256(const void *p, uint32_t (&r)[8], bool pred) {
+  if (NC) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t"
+        "@p ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "l"(p), "r"((int)pred));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t"
+        "@p ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "l"(p), "r"((int)pred)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void st256(void *p, const uint32_t (&r)[8], bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t"
+      "@p st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n\t}" ::"l"(p),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"((int)pred)
+      : "memory");
+}
+
+}  // namespace kt

@@ -1,0 +1,272 @@
+// kt_kernels.cu -- sm_100a streaming kernels for the K-TanH element maps and
+// their launchers.
+//
+// Layout: x, y are flat contiguous arrays in HBM.  The body of the array
+// (from the first 32-byte boundary) is processed as 32-byte vectors
+// (16 BF16 or 8 F32) with 256-bit LDG/STG; every warp owns "chunks" of
+// 32 lanes x kUnroll vectors and walks them grid-stride, so the loop bound
+// is warp-uniform and the shuffle-held LUT never sees a diverged warp.  The
+// unaligned head (< 32 B before the first boundary) and the tail (< 32 B)
+// are done element-wise by warp 0 of block 0 inside the same launch.  The
+// grid is sized from the occupancy of the kernel on this device's SM count
+// so that every warp does the same number of chunks (+-1).
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+
+#include "kt_device.cuh"
+#include "kt_internal.h"
+
+namespace kt {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kUnroll = 2;                    // 32-B vectors per lane per chunk
+constexpr int kVecBytes = 32;
+constexpr int kChunkVecs = 32 * kUnroll;      // vectors per warp-chunk
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+__device__ __forceinline__ LaneLut load_lane_lut(const LutWords &lut) {
+  const uint32_t lane = threadIdx.x & 31;
+  return LaneLut{lut.bf16[lane], lut.f32K[lane], lut.f32C[lane]};
+}
+
+// Element-wise head/tail helper: lane i handles element i (i < cnt) of the
+// range starting at p.  All 32 lanes execute apply_word (shuffle-safe).
+template <int OP, int FMT>
+__device__ __forceinline__ void scalar_span(const uint8_t *xp, uint8_t *yp, uint32_t cnt,
+                                            const LaneLut &L) {
+  const uint32_t lane = threadIdx.x & 31;
+  const bool on = lane < cnt;
+  uint32_t w = 0;
+  if (FMT == FMT_BF16) {
+    if (on) w = reinterpret_cast<const uint16_t *>(xp)[lane];
+  } else {
+    if (on) w = reinterpret_cast<const uint32_t *>(xp)[lane];
+  }
+  const uint32_t r = apply_word<OP, FMT>(w, L);
+  if (FMT == FMT_BF16) {
+    if (on) reinterpret_cast<uint16_t *>(yp)[lane] = (uint16_t)r;
+  } else {
+    if (on) reinterpret_cast<uint32_t *>(yp)[lane] = r;
+  }
+}
+
+// Main streaming kernel.  x/y: original (element-aligned) pointers; `head`
+// elements precede the first 32-B boundary of x (and of y: same offset mod
+// 32, checked on the host); nvec vectors follow; then `tail` elements.
+template <int OP, int FMT, bool NC>
+__global__ void __launch_bounds__(kThreads)
+k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec,
+      uint32_t tail, uint64_t nchunks, const __grid_constant__ LutWords lut) {
+  constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
+  const LaneLut L = load_lane_lut(lut);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint8_t *xb = x + (size_t)head * es;
+  uint8_t *yb = y + (size_t)head * es;
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t c = warp0; c < nchunks; c += nwarps) {     // warp-uniform trip count
+    const uint64_t base = c * kChunkVecs + lane;
+    uint32_t v[kUnroll][8];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t i = base + (uint64_t)u * 32;
+      ld256<NC>(xb + i * kVecBytes, v[u], i < nvec);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[u][j] = apply_word<OP, FMT>(v[u][j], L);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t i = base + (uint64_t)u * 32;
+      st256(yb + i * kVecBytes, v[u], i < nvec);
+    }
+  }
+  if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
+    scalar_span<OP, FMT>(x, y, head, L);
+    const size_t toff = ((size_t)head + (size_t)nvec * (kVecBytes / es)) * es;
+    scalar_span<OP, FMT>(x + toff, y + toff, tail, L);
+  }
+}
+
+// Fallback when x and y have different offsets mod 32 B: one element per
+// lane per step, warp-uniform loop.
+template <int OP, int FMT>
+__global__ void __launch_bounds__(kThreads)
+k_map_elem(const uint8_t *__restrict__ x, uint8_t *__restrict__ y, uint64_t n,
+           const __grid_constant__ LutWords lut) {
+  constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
+  const LaneLut L = load_lane_lut(lut);
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  const uint64_t nch = (n + 31) / 32;
+  for (uint64_t c = warp0; c < nch; c += nwarps) {
+    const uint64_t off = c * 32;
+    const uint64_t rem = n - off;
+    scalar_span<OP, FMT>(x + off * es, y + off * es, (uint32_t)(rem < 32 ? rem : 32), L);
+  }
+}
+
+// LSTM gates, vector path: x, y 32-B aligned, hidden % 16 == 0, so each
+// 16-element vector lies in one quarter of its row.  vpr = vectors per row
+// (= hidden / 4), vpq = vectors per quarter (= hidden / 16).
+template <bool NC>
+__global__ void __launch_bounds__(kThreads)
+k_lstm(const uint8_t *x, uint8_t *y, uint32_t nvec, uint32_t nchunks,
+       uint32_t vpr, uint32_t vpq, int tanh_quarter, const __grid_constant__ LutWords lut) {
+  const LaneLut L = load_lane_lut(lut);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t nwarps = gridDim.x * kWarps;
+  for (uint32_t c = warp0; c < nchunks; c += nwarps) {
+    const uint32_t base = c * kChunkVecs + lane;
+    uint32_t v[kUnroll][8];
+    bool tq[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t i = base + u * 32;
+      ld256<NC>(x + (size_t)i * kVecBytes, v[u], i < nvec);
+      tq[u] = ((i % vpr) / vpq) == (uint32_t)tanh_quarter;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[u][j] = lstm_bf16x2(v[u][j], L.w16, tq[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t i = base + u * 32;
+      st256(y + (size_t)i * kVecBytes, v[u], i < nvec);
+    }
+  }
+}
+
+// LSTM gates, element fallback (any alignment / hidden).
+__global__ void __launch_bounds__(kThreads)
+k_lstm_elem(const uint16_t *__restrict__ x, uint16_t *__restrict__ y, uint64_t n, uint64_t width,
+            uint64_t hidden, int tanh_quarter, const __grid_constant__ LutWords lut) {
+  const LaneLut L = load_lane_lut(lut);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t c = warp0; c * 32 < n; c += nwarps) {
+    const uint64_t i = c * 32 + lane;
+    const bool on = i < n;
+    const uint32_t w = on ? x[i] : 0u;
+    const bool is_tanh = on && ((i % width) / hidden) == (uint64_t)tanh_quarter;
+    const uint32_t r = lstm_bf16x2(w, L.w16, is_tanh);
+    if (on) y[i] = (uint16_t)r;
+  }
+}
+
+// ---------------------------------------------------------------- host ----
+
+template <class K>
+static int resident_blocks(K kernel) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1)
+    b = 1;
+  return b;
+}
+
+// Balanced grid: every warp does `iters` or `iters - 1` chunks.
+static unsigned grid_for(uint64_t nchunks, int sm_count, int blocks_per_sm) {
+  const uint64_t max_warps = (uint64_t)sm_count * blocks_per_sm * kWarps;
+  if (nchunks == 0) return 1;
+  const uint64_t iters = (nchunks + max_warps - 1) / max_warps;
+  const uint64_t warps = (nchunks + iters - 1) / iters;
+  return (unsigned)std::max<uint64_t>(1, (warps + kWarps - 1) / kWarps);
+}
+
+template <int OP, int FMT>
+static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &lut, cudaStream_t s,
+                             const LaunchInfo &li) {
+  constexpr size_t es = (FMT == FMT_BF16) ? 2 : 4;
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+  const uint8_t *xp = static_cast<const uint8_t *>(x);
+  uint8_t *yp = static_cast<uint8_t *>(y);
+  if ((xa % kVecBytes) != (ya % kVecBytes)) {
+    static const int bps = resident_blocks(k_map_elem<OP, FMT>);
+    const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
+    k_map_elem<OP, FMT><<<grid, kThreads, 0, s>>>(xp, yp, (uint64_t)n, lut);
+    count_launch();
+    return cudaGetLastError();
+  }
+  const size_t mis = xa % kVecBytes;
+  size_t head = mis ? (kVecBytes - mis) / es : 0;
+  if (head > n) head = n;
+  const size_t body = n - head;
+  const uint64_t nvec = body / (kVecBytes / es);
+  const uint32_t tail = (uint32_t)(body - nvec * (kVecBytes / es));
+  const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+  if (x != y) {
+    static const int bps = resident_blocks(k_map<OP, FMT, true>);
+    const unsigned grid = grid_for(nchunks, li.sm_count, bps);
+    k_map<OP, FMT, true><<<grid, kThreads, 0, s>>>(xp, yp, (uint32_t)head, nvec, tail, nchunks, lut);
+  } else {
+    static const int bps = resident_blocks(k_map<OP, FMT, false>);
+    const unsigned grid = grid_for(nchunks, li.sm_count, bps);
+    k_map<OP, FMT, false><<<grid, kThreads, 0, s>>>(xp, yp, (uint32_t)head, nvec, tail, nchunks, lut);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const LutWords &lut,
+                       cudaStream_t s, const LaunchInfo &li) {
+#define KT_CASE(O, F) \
+  if (op == O && fmt == F) return launch_op<O, F>(x, y, n, lut, s, li);
+  KT_CASE(OP_TANH, FMT_BF16)
+  KT_CASE(OP_SIGMOID, FMT_BF16)
+  KT_CASE(OP_SWISH, FMT_BF16)
+  KT_CASE(OP_GELU, FMT_BF16)
+  KT_CASE(OP_TANH, FMT_F32)
+  KT_CASE(OP_SIGMOID, FMT_F32)
+  KT_CASE(OP_SWISH, FMT_F32)
+  KT_CASE(OP_GELU, FMT_F32)
+#undef KT_CASE
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_lstm(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,
+                        int tanh_quarter, const LutWords &lut, cudaStream_t s,
+                        const LaunchInfo &li) {
+  const size_t n = rows * 4 * hidden;
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+  const uint64_t nvec = n / 16;
+  const bool vec_ok = (xa % kVecBytes) == 0 && (ya % kVecBytes) == 0 && hidden % 16 == 0 &&
+                      nvec < (1ull << 31);
+  if (vec_ok) {
+    const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+    const uint8_t *xp = reinterpret_cast<const uint8_t *>(x);
+    uint8_t *yp = reinterpret_cast<uint8_t *>(y);
+    if (static_cast<const void *>(x) != static_cast<const void *>(y)) {
+      static const int bps = resident_blocks(k_lstm<true>);
+      const unsigned grid = grid_for(nchunks, li.sm_count, bps);
+      k_lstm<true><<<grid, kThreads, 0, s>>>(xp, yp, (uint32_t)nvec, (uint32_t)nchunks,
+                                             (uint32_t)(hidden / 4), (uint32_t)(hidden / 16),
+                                             tanh_quarter, lut);
+    } else {
+      static const int bps = resident_blocks(k_lstm<false>);
+      const unsigned grid = grid_for(nchunks, li.sm_count, bps);
+      k_lstm<false><<<grid, kThreads, 0, s>>>(xp, yp, (uint32_t)nvec, (uint32_t)nchunks,
+                                              (uint32_t)(hidden / 4), (uint32_t)(hidden / 16),
+                                              tanh_quarter, lut);
+    }
+  } else {
+    static const int bps = resident_blocks(k_lstm_elem);
+    const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
+    k_lstm_elem<<<grid, kThreads, 0, s>>>(x, y, (uint64_t)n, (uint64_t)(4 * hidden),
+                                          (uint64_t)hidden, tanh_quarter, lut);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace kt

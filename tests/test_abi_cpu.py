@@ -1,0 +1,139 @@
+"""C-ABI library checks that need no GPU: the library loads, exports every
+symbol include/ktanh.h declares, validates parameter tables, rejects bad
+arguments before touching the device, and computes shard ranges."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+import oracle as O
+
+HEADER = os.path.join(ROOT, "include", "ktanh.h")
+
+
+@pytest.fixture(scope="module")
+def kt():
+    from paper_1909_07729_b200 import build
+    build.build()
+    import paper_1909_07729_b200 as kt
+    return kt
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"KT_API\s+[\w\s\*]+?\b(\w+)\s*\(", txt)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_symbols()
+    for n in ("ktanh_bf16", "ktanh_f32", "ksigmoid_bf16", "ksigmoid_f32", "kswish_bf16",
+              "kswish_f32", "kgelu_bf16", "kgelu_f32", "kt_lut_create", "kt_lut_destroy",
+              "klstm_gates_bf16", "kt_apply_host", "kt_shard_range"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(kt):
+    lib = ctypes.CDLL(kt.LIB_PATH)
+    for n in declared_symbols():
+        assert hasattr(lib, n), n
+    assert set(declared_symbols()) == set(kt.EXPORTS)
+    assert kt.abi_version() == 1
+
+
+def test_paper_lut_roundtrip(kt):
+    E, r, b = kt.Lut.paper().tables()
+    T = O.table1()
+    assert (E, r, b) == (list(T.E), list(T.r), list(T.b))
+
+
+def test_lut_validation_accepts_optimizer_tables(kt):
+    for bz in (False, True):
+        L, _ = O.build_lut(bz)
+        h = kt.Lut.from_tables(L.E, L.r, L.b)
+        assert h.tables() == (list(L.E), list(L.r), list(L.b))
+
+
+def test_lut_validation_bounds(kt):
+    """Every b within the Sec. 2.4 bounds is accepted; b_max + 1
+    and r outside [0, 7] are rejected with KT_ERR_LUT."""
+    T = O.table1()
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        E, r, b = T.E.copy(), T.r.copy(), T.b.copy()
+        t = int(rng.integers(0, 32))
+        if t == 7:
+            continue
+        r[t] = int(rng.integers(0, 8))
+        lo, hi = O.bounds(int(r[t]), t & 7)
+        b[t] = int(rng.integers(lo, hi + 1))
+        kt.Lut.from_tables(E, r, b)
+        b[t] = hi + 1
+        with pytest.raises(kt.KTanhError) as ei:
+            kt.Lut.from_tables(E, r, b)
+        assert ei.value.status == kt.KT_ERR_LUT
+    E, r, b = T.E.copy(), T.r.copy(), T.b.copy()
+    r[3] = 8
+    with pytest.raises(kt.KTanhError):
+        kt.Lut.from_tables(E, r, b)
+    E[3], r[3] = 128, 4
+    with pytest.raises(kt.KTanhError):
+        kt.Lut.from_tables(E, r, b)
+
+
+def test_bad_arguments_rejected_before_device(kt):
+    lut = kt.Lut.paper()
+    lib = kt._lib
+    for name in kt.MAP_CALLS:
+        f = getattr(lib, name)
+        assert f(None, None, 0, lut.handle, None) == kt.KT_OK          # n == 0: no launch
+        assert f(None, None, 16, lut.handle, None) == kt.KT_ERR_ARG    # NULL with n > 0
+        assert f(None, None, 16, None, None) == kt.KT_ERR_ARG          # NULL lut
+    # misaligned element pointers and partial overlap are argument errors
+    assert lib.ktanh_f32(ctypes.c_void_p(0x1002), ctypes.c_void_p(0x10002), 4, lut.handle, None) == kt.KT_ERR_ARG
+    assert lib.ktanh_bf16(ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1002), 64, lut.handle, None) == kt.KT_ERR_ARG
+    assert lib.klstm_gates_bf16(None, None, 1, 0, 2, lut.handle, None) == kt.KT_ERR_ARG
+    assert lib.klstm_gates_bf16(None, None, 1, 16, 4, lut.handle, None) == kt.KT_ERR_ARG
+    assert lib.kt_apply(7, 0, None, None, 16, lut.handle, None) == kt.KT_ERR_ARG
+    assert "overlap" in lib.kt_last_error().decode() or lib.kt_last_error()
+
+
+@pytest.mark.parametrize("n", [0, 1, 15, 16, 17, 1000, 65537, 1 << 30, (1 << 33) + 5])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_range_partition(kt, n, world):
+    """Shards tile [0, n) exactly, in rank order, each starting on a multiple of 16."""
+    pos = 0
+    for rank in range(world):
+        b, c = kt.shard_range(n, world, rank, 16)
+        assert b == pos and b % 16 == 0 or c == 0
+        pos = b + c
+    assert pos == n
+    sizes = [kt.shard_range(n, world, r, 16)[1] for r in range(world)]
+    assert max(sizes) - min(sizes) <= max(16, -(-n // world) + 16)
+
+
+def test_shard_range_errors(kt):
+    with pytest.raises(kt.KTanhError):
+        kt.shard_range(10, 0, 0)
+    with pytest.raises(kt.KTanhError):
+        kt.shard_range(10, 2, 2)
+    with pytest.raises(kt.KTanhError):
+        kt.shard_range(10, 2, 0, 0)
+
+
+def test_product_and_oracle_do_not_import_each_other():
+    """The CUDA path and the oracle share no code and never import each other."""
+    imp = re.compile(r"^\s*(import|from)\s+(\S+)|#include\s+[<\"]([^>\"]+)", re.M)
+    pkg = os.path.join(ROOT, "paper_1909_07729_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                for m in imp.finditer(open(os.path.join(dp, f)).read()):
+                    assert "oracle" not in "".join(g or "" for g in m.groups()), (f, m.group(0))
+    for f in ("ktanh_oracle.c", "__init__.py"):
+        for m in imp.finditer(open(os.path.join(ROOT, "oracle", f)).read()):
+            tgt = "".join(g or "" for g in m.groups())
+            assert "paper_1909_07729_b200" not in tgt and "ktanh.h" not in tgt and "kt_" not in tgt

@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): K-TanH bit-exact on every BF16 pattern and on
+all configs; K-Sigmoid bit-exact too (NaN compared by class, GPU arithmetic
+canonicalises NaN payloads); K-GELU / K-Swish within 1 BF16 ulp and 2 FP32
+ulp (NaN by class).  Inputs come from workloads/ (seeded, on the device) and
+are copied to the host for the oracle, so both sides see the same bytes.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads as WL
+from _cmp import assert_bitexact, assert_ulp
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"bf16": {"tanh": 0, "sigmoid": 0, "swish": 1, "gelu": 1},
+       "f32": {"tanh": 0, "sigmoid": 0, "swish": 2, "gelu": 2}}
+
+
+@pytest.fixture(scope="module")
+def kt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1909_07729_b200 as kt
+    return kt
+
+
+def u16(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def u32(t):
+    return t.contiguous().view(torch.int32).cpu().numpy().view(np.uint32)
+
+
+def call(kt, op, fmt, x, **kw):
+    return getattr(kt, f"k{op}_{fmt}")(x, **kw)
+
+
+def check(op, fmt, got_bits, want_bits, ctx):
+    bits = 16 if fmt == "bf16" else 32
+    tol = TOL[fmt][op]
+    if tol == 0:
+        assert_bitexact(got_bits, want_bits, bits, nan_by_class=(op != "tanh"), ctx=ctx)
+    else:
+        assert_ulp(got_bits, want_bits, bits, tol, ctx=ctx)
+
+
+def oracle_bf16(op, x_bits, lut=None):
+    return O.map_bf16(op, x_bits, lut)
+
+
+# --------------------------------------------------------------- config 1 --
+@pytest.mark.parametrize("op", ["tanh", "sigmoid", "swish", "gelu"])
+def test_exhaustive_bf16(kt, op):
+    """Config 1: all 65,536 BF16 patterns as one tensor."""
+    x = WL.make_input("c1_exhaustive_bf16", device="cuda")
+    y = call(kt, op, "bf16", x)
+    torch.cuda.synchronize()
+    check(op, "bf16", u16(y), oracle_bf16(op, u16(x)), f"{op} bf16 exhaustive")
+
+
+def test_exhaustive_bf16_ktanh_nan_passthrough(kt):
+    x = WL.make_input("c1_exhaustive_bf16", device="cuda")
+    y = u16(kt.ktanh_bf16(x))
+    xb = u16(x)
+    nan = (xb & 0x7FFF) > 0x7F80
+    assert np.array_equal(y[nan], xb[nan])
+
+
+@pytest.mark.parametrize("which", ["rstar", "ablation", "fuzz0", "fuzz1", "fuzz2", "fuzz3"])
+def test_lut_generic(kt, which):
+    """The kernel is LUT-generic: optimizer tables and random valid tables
+    (r in 0..7, b within the Sec. 2.4 bounds) give oracle-identical maps."""
+    if which == "rstar":
+        L = O.build_lut(False)[0]
+    elif which == "ablation":
+        L = O.build_lut(True)[0]
+    else:
+        rng = np.random.default_rng(int(which[-1]))
+        T = O.table1()
+        E, r, b = T.E.copy(), T.r.copy(), T.b.copy()
+        for t in range(32):
+            r[t] = rng.integers(0, 8)
+            lo, hi = O.bounds(int(r[t]), t & 7)
+            if t == 7:
+                hi = 127 - (112 >> int(r[t]))
+            b[t] = rng.integers(lo, hi + 1)
+            E[t] = rng.integers(100, 127)
+        L = O.Lut(E, r, b)
+    h = kt.Lut.from_tables(L.E, L.r, L.b)
+    x = WL.make_input("c1_exhaustive_bf16", device="cuda")
+    for op in ("tanh", "sigmoid", "swish", "gelu"):
+        y = call(kt, op, "bf16", x, lut=h)
+        check(op, "bf16", u16(y), oracle_bf16(op, u16(x), L), f"{op} lut={which}")
+    # F32 with the same table on BF16-exact and random inputs
+    rng = np.random.default_rng(7)
+    xf = torch.from_numpy(np.concatenate([
+        (np.arange(65536, dtype=np.uint32) << 16),
+        rng.integers(0, 2**32, 200000, dtype=np.uint64).astype(np.uint32)]).view(np.int32)).cuda().view(torch.float32)
+    for op in ("tanh", "sigmoid", "swish", "gelu"):
+        y = call(kt, op, "f32", xf, lut=h)
+        check(op, "f32", u32(y), O.map_f32(op, u32(xf), L), f"{op} f32 lut={which}")
+
+
+# ------------------------------------------------------------------ F32 -----
+@pytest.mark.parametrize("op", ["tanh", "sigmoid", "swish", "gelu"])
+def test_f32_patterns(kt, op):
+    """F32: every (exp, top-12-mantissa) pattern class + random bits + specials."""
+    rng = np.random.default_rng(11)
+    bits = np.concatenate([
+        (np.arange(1 << 20, dtype=np.uint64) << 12).astype(np.uint32),
+        ((np.arange(1 << 20, dtype=np.uint64) << 12) | 0xFFF).astype(np.uint32),
+        rng.integers(0, 2**32, 1 << 20, dtype=np.uint64).astype(np.uint32),
+        np.array(WL.special_values_f32(), np.uint32)])
+    x = torch.from_numpy(bits.view(np.int32)).cuda().view(torch.float32)
+    y = call(kt, op, "f32", x)
+    check(op, "f32", u32(y), O.map_f32(op, bits), f"{op} f32 patterns")
+
+
+# ------------------------------------------------------------ configs 2-5 ---
+def _bf16_table(op, lut=None):
+    """Oracle output for every BF16 pattern (the BF16 map is a function of the
+    16 input bits, so full-size tensors are checked by table lookup)."""
+    return torch.from_numpy(oracle_bf16(op, O.all_bf16(), lut).view(np.int16).copy())
+
+
+def _lookup_check(op, x, y, chunk=1 << 26):
+    """Full-size check on the GPU: want[i] = oracle_table[x[i]] for every element."""
+    table = _bf16_table(op).cuda()
+    xi = x.view(-1).view(torch.int16)
+    yi = y.view(-1).view(torch.int16)
+    for s in range(0, xi.numel(), chunk):
+        idx = xi[s:s + chunk].to(torch.int32) & 0xFFFF
+        want = table[idx]
+        got = yi[s:s + chunk]
+        if TOL["bf16"][op] == 0:
+            bad = got != want
+            if op != "tanh":
+                nan_g = (got.to(torch.int32) & 0x7FFF) > 0x7F80
+                nan_w = (want.to(torch.int32) & 0x7FFF) > 0x7F80
+                bad &= ~(nan_g & nan_w)
+            assert not bool(bad.any()), f"{op}: {int(bad.sum())} mismatches in chunk {s}"
+        else:
+            g = got.to(torch.int32); w = want.to(torch.int32)
+            og = torch.where(g < 0, -(g & 0x7FFF), g)
+            ow = torch.where(w < 0, -(w & 0x7FFF), w)
+            d = (og - ow).abs()
+            nan_g = (g & 0x7FFF) > 0x7F80
+            nan_w = (w & 0x7FFF) > 0x7F80
+            d = torch.where(nan_g & nan_w, torch.zeros_like(d), d)
+            d = torch.where(nan_g ^ nan_w, torch.full_like(d, 1 << 20), d)
+            assert int(d.max()) <= TOL["bf16"][op], f"{op}: max ulp {int(d.max())} in chunk {s}"
+    del table
+
+
+def _sampled_oracle_check(op, x, y, m=1 << 16, seed=0):
+    """Sampled outputs computed one by one by the oracle (no table)."""
+    n = x.numel()
+    idx = np.random.default_rng(seed).integers(0, n, m, dtype=np.int64)
+    idx = np.concatenate([idx, [0, n - 1]])
+    it = torch.from_numpy(idx).cuda()
+    xs = u16(x.view(-1)[it])
+    ys = u16(y.view(-1)[it])
+    want = O.map_bf16(op, xs)
+    check(op, "bf16", ys, want, f"{op} sampled")
+
+
+def test_config2_bf16_full(kt):
+    x = WL.make_input("c2_bf16_2p24", device="cuda")
+    y = kt.ktanh_bf16(x)
+    _lookup_check("tanh", x, y)
+    _sampled_oracle_check("tanh", x, y)
+    # and the whole tensor through the oracle directly (2^24 elements, ~0.1 s)
+    assert_bitexact(u16(y), O.map_bf16("tanh", u16(x)), 16, ctx="c2 direct")
+
+
+def test_config3_f32_full(kt):
+    x = WL.make_input("c3_f32_2p28", device="cuda")
+    y = kt.ktanh_f32(x)
+    torch.cuda.synchronize()
+    xb, yb = u32(x), u32(y)
+    del y
+    # 2^28 elements through the scalar oracle in slices (a few seconds)
+    step = 1 << 25
+    for s in range(0, xb.size, step):
+        assert_bitexact(yb[s:s + step], O.map_f32("tanh", xb[s:s + step]), 32, ctx=f"c3 slice {s}")
+
+
+def test_config4_lstm_gates_full(kt):
+    x = WL.make_input("c4_lstm_gates", device="cuda")
+    y = kt.klstm_gates_bf16(x, WL.LSTM_HIDDEN, 2)
+    want = O.lstm_gates_bf16(u16(x), WL.LSTM_HIDDEN, 2)
+    assert_bitexact(u16(y), want, 16, nan_by_class=True, ctx="c4 lstm")
+
+
+@pytest.mark.parametrize("op", ["gelu", "swish"])
+def test_config5_ffn_full(kt, op):
+    """Config 5 at full per-GPU size (2^30 BF16): every element via the oracle
+    table, plus oracle samples computed one by one."""
+    x = WL.make_input("c5_ffn_2p30", device="cuda")
+    y = call(kt, op, "bf16", x)
+    _lookup_check(op, x, y)
+    _sampled_oracle_check(op, x, y, seed=5)
+    del x, y
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------- edge cases ---
+@pytest.mark.parametrize("fmt", ["bf16", "f32"])
+@pytest.mark.parametrize("n", [1, 7, 8, 15, 16, 17, 31, 33, 511, 512, 513, 65537, 1048593])
+@pytest.mark.parametrize("offset", [0, 1, 3])
+def test_sizes_and_offsets(kt, fmt, n, offset):
+    """Ragged sizes and element offsets (heads/tails around 32-B boundaries)."""
+    dt = torch.bfloat16 if fmt == "bf16" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(n * 7 + offset)
+    base = (torch.randn(n + 8, generator=g, device="cuda") * 3).to(dt)
+    x = base[offset:offset + n]
+    ybase = torch.full_like(base, 7.0)
+    y = ybase[offset:offset + n]
+    for op in ("tanh", "gelu"):
+        call(kt, op, fmt, x, out=y)
+        torch.cuda.synchronize()
+        if fmt == "bf16":
+            check(op, fmt, u16(y), O.map_bf16(op, u16(x)), f"{op} n={n} off={offset}")
+        else:
+            check(op, fmt, u32(y), O.map_f32(op, u32(x)), f"{op} n={n} off={offset}")
+    # the guard elements around the output are untouched
+    assert torch.all(ybase[:offset].float() == 7.0) and torch.all(ybase[offset + n:].float() == 7.0)
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "f32"])
+def test_mismatched_alignment(kt, fmt):
+    """x and y with different offsets mod 32 B take the element-wise kernel."""
+    dt = torch.bfloat16 if fmt == "bf16" else torch.float32
+    n = 100003
+    base = (torch.randn(n + 16, device="cuda") * 3).to(dt)
+    out = torch.empty(n + 16, device="cuda", dtype=dt)
+    x, y = base[1:1 + n], out[4:4 + n]
+    for op in ("tanh", "sigmoid", "swish", "gelu"):
+        call(kt, op, fmt, x, out=y)
+        want = O.map_bf16(op, u16(x)) if fmt == "bf16" else O.map_f32(op, u32(x))
+        check(op, fmt, u16(y) if fmt == "bf16" else u32(y), want, f"{op} misaligned")
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "f32"])
+def test_in_place(kt, fmt):
+    dt = torch.bfloat16 if fmt == "bf16" else torch.float32
+    x = (torch.randn(1 << 20, device="cuda") * 3).to(dt)
+    xb = u16(x) if fmt == "bf16" else u32(x)
+    for op in ("tanh", "sigmoid"):
+        z = x.clone()
+        call(kt, op, fmt, z, out=z)
+        want = O.map_bf16(op, xb) if fmt == "bf16" else O.map_f32(op, xb)
+        check(op, fmt, u16(z) if fmt == "bf16" else u32(z), want, f"{op} in place")
+
+
+def test_empty_and_errors(kt):
+    x = torch.empty(0, device="cuda", dtype=torch.bfloat16)
+    assert kt.ktanh_bf16(x).numel() == 0
+    # host memory is rejected (KT_ERR_ARG), not dereferenced
+    lut = kt.paper_lut()
+    h = torch.zeros(64, dtype=torch.bfloat16)
+    d = torch.zeros(64, dtype=torch.bfloat16, device="cuda")
+    assert kt._lib.ktanh_bf16(h.data_ptr(), d.data_ptr(), 64, lut.handle, None) == kt.KT_ERR_ARG
+    with pytest.raises(TypeError):
+        kt.ktanh_bf16(h)
+    with pytest.raises(TypeError):
+        kt.ktanh_bf16(d.float())
+    # partial overlap
+    assert kt._lib.ktanh_bf16(d.data_ptr(), d.data_ptr() + 2, 32, lut.handle, None) == kt.KT_ERR_ARG
+
+
+def test_stream_and_graph_capture(kt):
+    """Async on a side stream, and capturable into a CUDA graph."""
+    x = (torch.randn(1 << 22, device="cuda") * 2).to(torch.bfloat16)
+    want = O.map_bf16("tanh", u16(x))
+    s = torch.cuda.Stream()
+    y = torch.empty_like(x)
+    with torch.cuda.stream(s):
+        kt.ktanh_bf16(x, out=y, stream=s)
+    s.synchronize()
+    assert_bitexact(u16(y), want, 16, ctx="side stream")
+    y2 = torch.zeros_like(x)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        kt.ktanh_bf16(x, out=y2)
+    g.replay()
+    torch.cuda.synchronize()
+    assert_bitexact(u16(y2), want, 16, ctx="graph replay")
+
+
+@pytest.mark.parametrize("hidden,rows,tq", [(1024, 33, 2), (16, 5, 0), (24, 7, 3), (10, 3, 1)])
+def test_lstm_shapes(kt, hidden, rows, tq):
+    x = (torch.randn(rows, 4 * hidden, device="cuda") * 1.5).to(torch.bfloat16)
+    y = kt.klstm_gates_bf16(x, hidden, tq)
+    assert_bitexact(u16(y), O.lstm_gates_bf16(u16(x), hidden, tq), 16, nan_by_class=True,
+                    ctx=f"lstm H={hidden}")
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "f32"])
+def test_apply_host_pipeline(kt, fmt):
+    """kt_apply_host: host buffers -> chunked H2D / kernel / D2H over 3 streams."""
+    dt = torch.bfloat16 if fmt == "bf16" else torch.float32
+    n = 3 * 1000003
+    x = (torch.randn(n) * 3).to(dt).pin_memory()
+    y = torch.empty_like(x).pin_memory()
+    work = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+    for op in ("tanh", "gelu"):
+        kt.apply_host(op, x, y, work)
+        torch.cuda.current_stream().synchronize()
+        xb = x.view(torch.int16).numpy().view(np.uint16) if fmt == "bf16" else x.view(torch.int32).numpy().view(np.uint32)
+        yb = y.view(torch.int16).numpy().view(np.uint16) if fmt == "bf16" else y.view(torch.int32).numpy().view(np.uint32)
+        want = O.map_bf16(op, xb) if fmt == "bf16" else O.map_f32(op, xb)
+        check(op, fmt, yb, want, f"apply_host {op}")
+
+
+def test_launch_counter(kt):
+    c0 = kt.launch_count()
+    x = torch.randn(4096, device="cuda").to(torch.bfloat16)
+    kt.ktanh_bf16(x)
+    kt.kgelu_bf16(x)
+    assert kt.launch_count() - c0 == 2
