@@ -164,7 +164,7 @@ def max_over_ranks(v: float, world: int, device) -> float:
 
 
 def time_windows(step: Step, K: int, W: int, world: int, device, clocks: ClockSampler | None,
-                 min_total_s: float = 1.0, max_windows: int = 50):
+                 min_total_s: float = 1.0, max_windows: int = 4000):
     """W warm-up steps, then windows of exactly K graph-replayed steps; returns
     (per-window max-over-ranks ms, clock summary, launches per step)."""
     stream = torch.cuda.Stream(device)
