@@ -45,6 +45,35 @@ __device__ __forceinline__ uint32_t hset2_gt(uint32_t a, uint32_t b) {
   return d;
 }
 
+// hi32(a*b) and hi32(a*b) + c (IMAD.HI, FMA pipe)
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// packed fp32x2 arithmetic (FMUL2 / FFMA2), round-to-nearest-even, no FTZ
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
 // m ? a : b, bitwise (one LOP3)
 __device__ __forceinline__ uint32_t bsel(uint32_t m, uint32_t a, uint32_t b) {
   return (m & a) | (~m & b);
@@ -58,6 +87,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float hi, float lo) {
 }
 __device__ __forceinline__ float lo_f32(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float hi_f32(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+// the two BF16 of w widened exactly to fp32: .x = low half, .y = high half
+__device__ __forceinline__ float2 widen2(uint32_t w) { return make_float2(lo_f32(w), hi_f32(w)); }
+__device__ __forceinline__ uint32_t pack2(float2 v) { return pack_bf16x2(v.y, v.x); }
+__device__ __forceinline__ float2 splat2(float a) { return make_float2(a, a); }
 
 // Thresholds: T1 = 0.25 = 0x3E80, T2 = 3.75 = 0x4070 (BF16);
 // 0x3E800000 / 0x40700000 (F32).  +-1 = (s, E_bias = 127, 0).
@@ -78,25 +111,32 @@ constexpr uint32_t kGeluC1Bits = 0x3D122279u;
 // ------------------------------------------------------------- K-TanH core --
 
 // Algorithm 1 on two BF16 values packed in x.
-//   lw = this lane's word LutWords::bf16[lane] = (C_t << 16) | r_t.
+//   lw = this lane's word LutWords::bf16[lane] = (2^(15 - r_t) << 16) | (C_t mod 2^16).
+// Shifts by constants and the per-entry shift are done as integer multiplies
+// (IMAD.SHL / IMAD.HI on the FMA pipe) so the ALU pipe only carries the
+// mask, the pack and the three selects:
+//   lo: hi32((x << 17) * 2^(15-r)) = |x_lo| >> r        (x << 17 = |x_lo| << 17)
+//   hi: hi32((x << 1)  * 2^(15-r)) = |x_hi| >> r        (the x_lo bits below
+//       contribute < 2^(32-r) - 2^(16-r) to the low word: no carry)
+// and adding the whole LUT word puts C_t + (|x| >> r_t) in the low 16 bits.
 __device__ __forceinline__ uint32_t ktanh_bf16x2(uint32_t x, uint32_t lw) {
-  const uint32_t mag = x & kMagx2;                 // |x| bits of both halves
   // line 6: t = bits [8:4] of each half = (E & 3) : (M >> 4)
   // line 7: theta_t by shuffle from lane t
-  const uint32_t Ll = shfl_lut(lw, x >> 4);
-  const uint32_t Lh = shfl_lut(lw, x >> 20);
+  const uint32_t Ll = shfl_lut(lw, mulhi(x, 1u << 28));    // lane = x >> 4
+  const uint32_t Lh = shfl_lut(lw, mulhi(x, 1u << 12));    // lane = x >> 20
   // line 8: E_o, M_o = E_t, (M >> r_t) + b_t  ==  C_t + (|x| >> r_t)
-  const uint32_t Kl = shr_wrap(0x10000u, Ll);      // 2^(16 - r_t)
-  const uint32_t Kh = shr_wrap(0x10000u, Lh);
-  const uint32_t dl = (mag & 0xffffu) * Kl + Ll;   // hi16 = C_t + (|x_lo| >> r_t)
-  const uint32_t dh = (mag >> 16) * Kh + Lh;       // hi16 = C_t + (|x_hi| >> r_t)
-  const uint32_t ymag = __byte_perm(dl, dh, 0x7632);
+  const uint32_t Kl = mulhi(Ll, 1u << 16);                 // 2^(15 - r_t)
+  const uint32_t Kh = mulhi(Lh, 1u << 16);
+  const uint32_t dl = madhi(x << 17, Kl, Ll);              // lo16 = C_t + (|x_lo| >> r_t)
+  const uint32_t dh = madhi(x << 1, Kh, Lh);               // lo16 = C_t + (|x_hi| >> r_t)
+  const uint32_t ymag = __byte_perm(dl, dh, 0x5410);
   // lines 3-4: region masks per half
+  const uint32_t mag = x & kMagx2;
   const uint32_t byp = hset2_ltu(mag, kT1x2);      // |x| < T1, or NaN
   const uint32_t sat = hset2_gt(mag, kT2x2);       // |x| > T2, incl. inf
-  const uint32_t m2 = bsel(sat, kOnex2, ymag);     // line 4: (s, E_bias, 0)
-  const uint32_t m3 = bsel(byp, mag, m2);          // line 3: y = x
-  return (x & kSignx2) | m3;                       // s_o = s_i
+  const uint32_t m = bsel(sat, kOnex2, ymag);      // line 4: (s, E_bias, 0)
+  const uint32_t o = bsel(byp, x, m);              // line 3: y = x
+  return o | (x & kSignx2);                        // s_o = s_i
 }
 
 // Algorithm 1 on one F32 (native reading A8).  lk = f32K[lane], lc = f32C[lane].
@@ -118,16 +158,15 @@ __device__ __forceinline__ uint32_t ktanh_f32(uint32_t u, uint32_t lk, uint32_t 
 // explicit _rn intrinsics (no contraction), one rounding to the format.
 
 __device__ __forceinline__ uint32_t ksigmoid_bf16x2(uint32_t x, uint32_t lw) {
-  const float xl = lo_f32(x), xh = hi_f32(x);
-  const uint32_t h = pack_bf16x2(__fmul_rn(xh, 0.5f), __fmul_rn(xl, 0.5f));   // RN_bf16(x/2)
+  const uint32_t h = pack2(mul2(widen2(x), splat2(0.5f)));                 // RN_bf16(x/2)
   const uint32_t t = ktanh_bf16x2(h, lw);
-  return pack_bf16x2(__fmaf_rn(0.5f, hi_f32(t), 0.5f), __fmaf_rn(0.5f, lo_f32(t), 0.5f));
+  return pack2(fma2(splat2(0.5f), widen2(t), splat2(0.5f)));               // RN((1+t)/2)
 }
 
 __device__ __forceinline__ uint32_t kswish_bf16x2(uint32_t x, uint32_t lw) {
-  const float hl = __fmul_rn(lo_f32(x), 0.5f), hh = __fmul_rn(hi_f32(x), 0.5f);  // exact
-  const uint32_t t = ktanh_bf16x2(pack_bf16x2(hh, hl), lw);
-  return pack_bf16x2(__fmaf_rn(hh, hi_f32(t), hh), __fmaf_rn(hl, lo_f32(t), hl));
+  const float2 hx = mul2(widen2(x), splat2(0.5f));                         // exact x/2
+  const uint32_t t = ktanh_bf16x2(pack2(hx), lw);
+  return pack2(fma2(hx, widen2(t), hx));                                   // RN(hx (1+t))
 }
 
 __device__ __forceinline__ float gelu_arg(float x) {
@@ -137,11 +176,12 @@ __device__ __forceinline__ float gelu_arg(float x) {
 }
 
 __device__ __forceinline__ uint32_t kgelu_bf16x2(uint32_t x, uint32_t lw) {
-  const float xl = lo_f32(x), xh = hi_f32(x);
-  const uint32_t u = pack_bf16x2(gelu_arg(xh), gelu_arg(xl));                 // RN_bf16(u)
-  const uint32_t t = ktanh_bf16x2(u, lw);
-  const float hl = __fmul_rn(xl, 0.5f), hh = __fmul_rn(xh, 0.5f);
-  return pack_bf16x2(__fmaf_rn(hh, hi_f32(t), hh), __fmaf_rn(hl, lo_f32(t), hl));
+  const float2 xv = widen2(x);
+  const float2 x2 = mul2(xv, xv);
+  const float2 p = fma2(splat2(__uint_as_float(kGeluC1Bits)), x2, splat2(__uint_as_float(kGeluC0Bits)));
+  const uint32_t t = ktanh_bf16x2(pack2(mul2(xv, p)), lw);                 // RN_bf16(u)
+  const float2 hx = mul2(xv, splat2(0.5f));
+  return pack2(fma2(hx, widen2(t), hx));
 }
 
 __device__ __forceinline__ uint32_t ksigmoid_f32(uint32_t u, uint32_t lk, uint32_t lc) {
@@ -194,13 +234,9 @@ __device__ __forceinline__ uint32_t apply_word(uint32_t w, const LaneLut &L) {
 
 // LSTM gate pair: K-TanH (is_tanh) or K-Sigmoid, same core, per-lane choice.
 __device__ __forceinline__ uint32_t lstm_bf16x2(uint32_t x, uint32_t lw, bool is_tanh) {
-  uint32_t h = x;
-  if (!is_tanh) {
-    h = pack_bf16x2(__fmul_rn(hi_f32(x), 0.5f), __fmul_rn(lo_f32(x), 0.5f));
-  }
+  const uint32_t h = is_tanh ? x : pack2(mul2(widen2(x), splat2(0.5f)));
   const uint32_t t = ktanh_bf16x2(h, lw);
-  if (is_tanh) return t;
-  return pack_bf16x2(__fmaf_rn(0.5f, hi_f32(t), 0.5f), __fmaf_rn(0.5f, lo_f32(t), 0.5f));
+  return is_tanh ? t : pack2(fma2(splat2(0.5f), widen2(t), splat2(0.5f)));
 }
 
 // ------------------------------------------------------ streaming memory --
