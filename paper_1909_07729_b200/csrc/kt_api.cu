@@ -100,7 +100,11 @@ kt_status validate_and_pack(const int32_t *E, const int32_t *r, const int32_t *b
     L->b[t] = b[t];
     const int ei = e_in(t);
     const int32_t c16 = (E[t] << 7) + b[t] - (ei << (7 - r[t]));
-    L->words.bf16[t] = ((uint32_t)(1u << (15 - r[t])) << 16) | ((uint32_t)c16 & 0xFFFFu);
+    // fp32 word with exponent E_in + 16 + r and mantissa D = C + E_in 2^(7-r) - 2^(7-r)
+    // (mod 2^16): see ktanh_bf16x2 in kt_device.cuh
+    const int32_t d16 = (E[t] << 7) + b[t] - (1 << (7 - r[t]));
+    L->words.bf16[t] = ((uint32_t)(ei + 16 + r[t]) << 23) | ((uint32_t)d16 & 0xFFFFu);
+    (void)c16;
     L->words.f32K[t] = 1u << (31 - r[t]);
     const int64_t c32 = ((int64_t)E[t] << 23) + (int64_t)b[t] * 65536 - ((int64_t)ei << (23 - r[t]));
     L->words.f32C[t] = (uint32_t)(c32 & 0xFFFFFFFFll);

@@ -111,25 +111,28 @@ constexpr uint32_t kGeluC1Bits = 0x3D122279u;
 // ------------------------------------------------------------- K-TanH core --
 
 // Algorithm 1 on two BF16 values packed in x.
-//   lw = this lane's word LutWords::bf16[lane] = (2^(15 - r_t) << 16) | (C_t mod 2^16).
-// Shifts by constants and the per-entry shift are done as integer multiplies
-// (IMAD.SHL / IMAD.HI on the FMA pipe) so the ALU pipe only carries the
-// mask, the pack and the three selects:
-//   lo: hi32((x << 17) * 2^(15-r)) = |x_lo| >> r        (x << 17 = |x_lo| << 17)
-//   hi: hi32((x << 1)  * 2^(15-r)) = |x_hi| >> r        (the x_lo bits below
-//       contribute < 2^(32-r) - 2^(16-r) to the low word: no carry)
-// and adding the whole LUT word puts C_t + (|x| >> r_t) in the low 16 bits.
+//
+// Line 8, M_o = (M >> r_t) + b_t with E_o = E_t, is computed by ONE fp32 add in
+// round-toward-zero per element.  For a table-path input of exponent E_in the
+// LUT word L_t = bits((2^(E_in + 16 + r_t - 127)) (1 + D_t / 2^23)), with
+// D_t = ((E_t << 7) + b_t - 2^(7 - r_t)) mod 2^16, has ulp(L_t) = 2^r_t input
+// mantissa ulps, so RZ(|x| + L_t) = L_t + floor(|x| / ulp) ulp and
+//   low16(bits(RZ(|x| + L_t))) = D_t + 2^(7-r_t) + (M >> r_t) = (E_t << 7) + M_o.
+// Bits of |x| below the BF16 mantissa add < 1 to the floored numerator
+// (128 + M), so the high element can use the packed word as its fp32 operand
+// directly.  The FADD runs on the FMA pipe; the ALU pipe only carries the two
+// lane shifts, the pack and the masks/selects.  Exhaustively checked against
+// the oracle (tests/test_gpu_parity.py).
+//   lw = this lane's word LutWords::bf16[lane] = L_lane.
 __device__ __forceinline__ uint32_t ktanh_bf16x2(uint32_t x, uint32_t lw) {
   // line 6: t = bits [8:4] of each half = (E & 3) : (M >> 4)
   // line 7: theta_t by shuffle from lane t
-  const uint32_t Ll = shfl_lut(lw, mulhi(x, 1u << 28));    // lane = x >> 4
-  const uint32_t Lh = shfl_lut(lw, mulhi(x, 1u << 12));    // lane = x >> 20
-  // line 8: E_o, M_o = E_t, (M >> r_t) + b_t  ==  C_t + (|x| >> r_t)
-  const uint32_t Kl = mulhi(Ll, 1u << 16);                 // 2^(15 - r_t)
-  const uint32_t Kh = mulhi(Lh, 1u << 16);
-  const uint32_t dl = madhi(x << 17, Kl, Ll);              // lo16 = C_t + (|x_lo| >> r_t)
-  const uint32_t dh = madhi(x << 1, Kh, Lh);               // lo16 = C_t + (|x_hi| >> r_t)
-  const uint32_t ymag = __byte_perm(dl, dh, 0x5410);
+  const uint32_t Ll = shfl_lut(lw, x >> 4);
+  const uint32_t Lh = shfl_lut(lw, x >> 20);
+  // line 8: (E_t, (M >> r_t) + b_t) in the low 16 bits of the RZ sums
+  const float ql = __fadd_rz(fabsf(__uint_as_float(x << 16)), __uint_as_float(Ll));
+  const float qh = __fadd_rz(fabsf(__uint_as_float(x)), __uint_as_float(Lh));
+  const uint32_t ymag = __byte_perm(__float_as_uint(ql), __float_as_uint(qh), 0x5410);
   // lines 3-4: region masks per half
   const uint32_t mag = x & kMagx2;
   const uint32_t byp = hset2_ltu(mag, kT1x2);      // |x| < T1, or NaN

@@ -21,9 +21,10 @@ namespace kt {
 // so Alg. 1 line 8, (E_t, (M >> r_t) + b_t), equals
 //     (|x| >> r_t) + C_t,   C_t = (E_t << p) + b_t 2^(p-7) - (E_in << (p - r_t)).
 //
-//   bf16[t] = (2^(15 - r_t) << 16) | (C_t mod 2^16)
-//             kernel: lo16(hi32(|x| << 17 * (bf16[t] >> 16)) + bf16[t])
-//                     = C_t + (|x| >> r_t)   (see ktanh_bf16x2)
+//   bf16[t] = fp32 bits: exponent E_in + 16 + r_t, mantissa
+//             ((E_t << 7) + b_t - 2^(7 - r_t)) mod 2^16
+//             kernel: low16(bits(RZ(|x| + bf16[t]))) = (E_t << 7) + M_o
+//             (see ktanh_bf16x2 in kt_device.cuh)
 //   f32K[t] = 2^(31 - r_t),  f32C[t] = C_t (mod 2^32)
 //             kernel: umulhi(|x| << 1, f32K[t]) + f32C[t] = (|x| >> r_t) + C_t
 struct LutWords {
