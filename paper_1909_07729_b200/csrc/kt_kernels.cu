@@ -3,16 +3,27 @@
 //
 // Layout: x, y are flat contiguous arrays in HBM.  The body of the array
 // (from the first 32-byte boundary) is processed as 32-byte vectors
-// (16 BF16 or 8 F32) with 256-bit LDG/STG; every warp owns "chunks" of
-// 32 lanes x kUnroll vectors and walks them grid-stride, so the loop bound
-// is warp-uniform and the shuffle-held LUT never sees a diverged warp.  The
-// unaligned head (< 32 B before the first boundary) and the tail (< 32 B)
-// are done element-wise by warp 0 of block 0 inside the same launch.  The
-// grid is sized from the occupancy of the kernel on this device's SM count
-// so that every warp does the same number of chunks (+-1).
+// (16 BF16 or 8 F32) with 256-bit LDG/STG.  Each warp owns ONE "chunk" of
+// 32 lanes x kUnroll vectors (2 KiB) and the grid has one warp per chunk
+// ("flat" launch): the hardware block scheduler streams CTAs over the array
+// in address order.  Measured on B200 (profiles/),
+// this beats persistent grid-stride loops for a read-once/write-once stream:
+// a plain copy reaches 6.93 TB/s flat vs 6.05-6.70 TB/s persistent (torch
+// copy_: 6.56).  All lanes of a warp execute the shuffle-held LUT path
+// (loads/stores are predicated, never branched around), so the shuffles
+// never see a diverged warp.  The unaligned head (< 32 B before the first
+// boundary) and the tail (< 32 B) are done element-wise by warp 0 of block 0
+// inside the same launch.
+//
+// Launches use programmatic dependent launch (PDL): the kernel starts with
+// griddepcontrol.wait (it does not touch memory before the preceding grid in
+// the stream has completed and flushed), then immediately allows the next
+// PDL launch to be scheduled, so back-to-back calls overlap launch latency
+// and ramp-up with the previous call's tail.  Set KT_PDL=0 to disable.
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kt_device.cuh"
 #include "kt_internal.h"
@@ -21,13 +32,20 @@ namespace kt {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 2;                    // 32-B vectors per lane per chunk
+constexpr int kUnroll = 2;                    // 32-B vectors per lane per chunk (flat: 1 chunk/warp)
 constexpr int kVecBytes = 32;
 constexpr int kChunkVecs = 32 * kUnroll;      // vectors per warp-chunk
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+// PDL: wait for the preceding grid (no-op without a programmatic dependency),
+// then let the next grid in the stream begin launching.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ LaneLut load_lane_lut(const LutWords &lut) {
   const uint32_t lane = threadIdx.x & 31;
@@ -60,33 +78,31 @@ __device__ __forceinline__ void scalar_span(const uint8_t *xp, uint8_t *yp, uint
 // 32, checked on the host); nvec vectors follow; then `tail` elements.
 template <int OP, int FMT, bool NC>
 __global__ void __launch_bounds__(kThreads)
-k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec,
-      uint32_t tail, uint64_t nchunks, const __grid_constant__ LutWords lut) {
+k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
+      const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
   const LaneLut L = load_lane_lut(lut);
+  pdl_enter();
   const uint32_t lane = threadIdx.x & 31;
   const uint8_t *xb = x + (size_t)head * es;
   uint8_t *yb = y + (size_t)head * es;
-  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t c = warp0; c < nchunks; c += nwarps) {     // warp-uniform trip count
-    const uint64_t base = c * kChunkVecs + lane;
-    uint32_t v[kUnroll][8];
+  const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);   // this warp's chunk
+  const uint64_t base = c * kChunkVecs + lane;
+  uint32_t v[kUnroll][8];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t i = base + (uint64_t)u * 32;
-      ld256<NC>(xb + i * kVecBytes, v[u], i < nvec);
-    }
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t i = base + (uint64_t)u * 32;
+    ld256<NC>(xb + i * kVecBytes, v[u], i < nvec);
+  }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < kUnroll; ++u) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[u][j] = apply_word<OP, FMT>(v[u][j], L);
-    }
+    for (int j = 0; j < 8; ++j) v[u][j] = apply_word<OP, FMT>(v[u][j], L);
+  }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t i = base + (uint64_t)u * 32;
-      st256(yb + i * kVecBytes, v[u], i < nvec);
-    }
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t i = base + (uint64_t)u * 32;
+    st256(yb + i * kVecBytes, v[u], i < nvec);
   }
   if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
     scalar_span<OP, FMT>(x, y, head, L);
@@ -103,6 +119,7 @@ k_map_elem(const uint8_t *__restrict__ x, uint8_t *__restrict__ y, uint64_t n,
            const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
   const LaneLut L = load_lane_lut(lut);
+  pdl_enter();
   const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const uint64_t nch = (n + 31) / 32;
@@ -118,32 +135,30 @@ k_map_elem(const uint8_t *__restrict__ x, uint8_t *__restrict__ y, uint64_t n,
 // (= hidden / 4), vpq = vectors per quarter (= hidden / 16).
 template <bool NC>
 __global__ void __launch_bounds__(kThreads)
-k_lstm(const uint8_t *x, uint8_t *y, uint32_t nvec, uint32_t nchunks,
-       uint32_t vpr, uint32_t vpq, int tanh_quarter, const __grid_constant__ LutWords lut) {
+k_lstm(const uint8_t *x, uint8_t *y, uint32_t nvec, uint32_t vpr, uint32_t vpq, int tanh_quarter,
+       const __grid_constant__ LutWords lut) {
   const LaneLut L = load_lane_lut(lut);
+  pdl_enter();
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint32_t nwarps = gridDim.x * kWarps;
-  for (uint32_t c = warp0; c < nchunks; c += nwarps) {
-    const uint32_t base = c * kChunkVecs + lane;
-    uint32_t v[kUnroll][8];
-    bool tq[kUnroll];
+  const uint32_t c = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t base = c * kChunkVecs + lane;
+  uint32_t v[kUnroll][8];
+  bool tq[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint32_t i = base + u * 32;
-      ld256<NC>(x + (size_t)i * kVecBytes, v[u], i < nvec);
-      tq[u] = ((i % vpr) / vpq) == (uint32_t)tanh_quarter;
-    }
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint32_t i = base + u * 32;
+    ld256<NC>(x + (size_t)i * kVecBytes, v[u], i < nvec);
+    tq[u] = ((i % vpr) / vpq) == (uint32_t)tanh_quarter;
+  }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < kUnroll; ++u) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[u][j] = lstm_bf16x2(v[u][j], L.w16, tq[u]);
-    }
+    for (int j = 0; j < 8; ++j) v[u][j] = lstm_bf16x2(v[u][j], L.w16, tq[u]);
+  }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint32_t i = base + u * 32;
-      st256(y + (size_t)i * kVecBytes, v[u], i < nvec);
-    }
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint32_t i = base + u * 32;
+    st256(y + (size_t)i * kVecBytes, v[u], i < nvec);
   }
 }
 
@@ -152,6 +167,7 @@ __global__ void __launch_bounds__(kThreads)
 k_lstm_elem(const uint16_t *__restrict__ x, uint16_t *__restrict__ y, uint64_t n, uint64_t width,
             uint64_t hidden, int tanh_quarter, const __grid_constant__ LutWords lut) {
   const LaneLut L = load_lane_lut(lut);
+  pdl_enter();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
@@ -167,6 +183,32 @@ k_lstm_elem(const uint16_t *__restrict__ x, uint16_t *__restrict__ y, uint64_t n
 
 // ---------------------------------------------------------------- host ----
 
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("KT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  count_launch();
+  return e;
+}
+
 template <class K>
 static int resident_blocks(K kernel) {
   int b = 0;
@@ -175,13 +217,16 @@ static int resident_blocks(K kernel) {
   return b;
 }
 
-// Balanced grid: every warp does `iters` or `iters - 1` chunks.
+// Grid for the grid-stride fallback kernels: about 4 waves' worth of warps.
 static unsigned grid_for(uint64_t nchunks, int sm_count, int blocks_per_sm) {
-  const uint64_t max_warps = (uint64_t)sm_count * blocks_per_sm * kWarps;
-  if (nchunks == 0) return 1;
-  const uint64_t iters = (nchunks + max_warps - 1) / max_warps;
-  const uint64_t warps = (nchunks + iters - 1) / iters;
+  const uint64_t max_warps = (uint64_t)sm_count * blocks_per_sm * kWarps * 4;
+  const uint64_t warps = nchunks < max_warps ? nchunks : max_warps;
   return (unsigned)std::max<uint64_t>(1, (warps + kWarps - 1) / kWarps);
+}
+
+// Flat grid: one warp per chunk (at least one block for head/tail work).
+static unsigned flat_grid(uint64_t nchunks) {
+  return (unsigned)std::max<uint64_t>(1, (nchunks + kWarps - 1) / kWarps);
 }
 
 template <int OP, int FMT>
@@ -194,9 +239,7 @@ static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &l
   if ((xa % kVecBytes) != (ya % kVecBytes)) {
     static const int bps = resident_blocks(k_map_elem<OP, FMT>);
     const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
-    k_map_elem<OP, FMT><<<grid, kThreads, 0, s>>>(xp, yp, (uint64_t)n, lut);
-    count_launch();
-    return cudaGetLastError();
+    return launch(k_map_elem<OP, FMT>, grid, s, xp, yp, (uint64_t)n, lut);
   }
   const size_t mis = xa % kVecBytes;
   size_t head = mis ? (kVecBytes - mis) / es : 0;
@@ -205,17 +248,11 @@ static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &l
   const uint64_t nvec = body / (kVecBytes / es);
   const uint32_t tail = (uint32_t)(body - nvec * (kVecBytes / es));
   const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
-  if (x != y) {
-    static const int bps = resident_blocks(k_map<OP, FMT, true>);
-    const unsigned grid = grid_for(nchunks, li.sm_count, bps);
-    k_map<OP, FMT, true><<<grid, kThreads, 0, s>>>(xp, yp, (uint32_t)head, nvec, tail, nchunks, lut);
-  } else {
-    static const int bps = resident_blocks(k_map<OP, FMT, false>);
-    const unsigned grid = grid_for(nchunks, li.sm_count, bps);
-    k_map<OP, FMT, false><<<grid, kThreads, 0, s>>>(xp, yp, (uint32_t)head, nvec, tail, nchunks, lut);
-  }
-  count_launch();
-  return cudaGetLastError();
+  if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  const unsigned grid = flat_grid(nchunks);
+  if (x != y)
+    return launch(k_map<OP, FMT, true>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
+  return launch(k_map<OP, FMT, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
 }
 
 cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const LutWords &lut,
@@ -244,29 +281,18 @@ cudaError_t launch_lstm(const uint16_t *x, uint16_t *y, size_t rows, size_t hidd
                       nvec < (1ull << 31);
   if (vec_ok) {
     const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+    const unsigned grid = flat_grid(nchunks);
     const uint8_t *xp = reinterpret_cast<const uint8_t *>(x);
     uint8_t *yp = reinterpret_cast<uint8_t *>(y);
-    if (static_cast<const void *>(x) != static_cast<const void *>(y)) {
-      static const int bps = resident_blocks(k_lstm<true>);
-      const unsigned grid = grid_for(nchunks, li.sm_count, bps);
-      k_lstm<true><<<grid, kThreads, 0, s>>>(xp, yp, (uint32_t)nvec, (uint32_t)nchunks,
-                                             (uint32_t)(hidden / 4), (uint32_t)(hidden / 16),
-                                             tanh_quarter, lut);
-    } else {
-      static const int bps = resident_blocks(k_lstm<false>);
-      const unsigned grid = grid_for(nchunks, li.sm_count, bps);
-      k_lstm<false><<<grid, kThreads, 0, s>>>(xp, yp, (uint32_t)nvec, (uint32_t)nchunks,
-                                              (uint32_t)(hidden / 4), (uint32_t)(hidden / 16),
-                                              tanh_quarter, lut);
-    }
-  } else {
-    static const int bps = resident_blocks(k_lstm_elem);
-    const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
-    k_lstm_elem<<<grid, kThreads, 0, s>>>(x, y, (uint64_t)n, (uint64_t)(4 * hidden),
-                                          (uint64_t)hidden, tanh_quarter, lut);
+    const uint32_t vpr = (uint32_t)(hidden / 4), vpq = (uint32_t)(hidden / 16);
+    if (static_cast<const void *>(x) != static_cast<const void *>(y))
+      return launch(k_lstm<true>, grid, s, xp, yp, (uint32_t)nvec, vpr, vpq, tanh_quarter, lut);
+    return launch(k_lstm<false>, grid, s, xp, yp, (uint32_t)nvec, vpr, vpq, tanh_quarter, lut);
   }
-  count_launch();
-  return cudaGetLastError();
+  static const int bps = resident_blocks(k_lstm_elem);
+  const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
+  return launch(k_lstm_elem, grid, s, x, y, (uint64_t)n, (uint64_t)(4 * hidden), (uint64_t)hidden,
+                tanh_quarter, lut);
 }
 
 }  // namespace kt

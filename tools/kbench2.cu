@@ -169,6 +169,36 @@ kreg(const uint8_t *x, uint8_t *y, uint64_t nvec, uint64_t nchunks, const __grid
   }
 }
 
+// ---- flat (non-persistent) kernel: each warp does CPW consecutive chunks ----
+template <int OP, int U, int T, int CPW>
+__global__ void __launch_bounds__(T)
+kflat(const uint8_t *x, uint8_t *y, uint64_t nvec, uint64_t nchunks, const __grid_constant__ LutWords lut) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lw = lut.bf16[lane];
+  const uint64_t w = (uint64_t)blockIdx.x * (T / 32) + (threadIdx.x >> 5);
+#pragma unroll 1
+  for (int k = 0; k < CPW; ++k) {
+    const uint64_t c = w * CPW + k;
+    if (c >= nchunks) break;
+    const uint64_t base = c * (32 * U) + lane;
+    uint32_t v[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = base + (uint64_t)u * 32;
+      ld256<true>(x + i * 32, v[u], i < nvec);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[u][j] = opw<OP>(v[u][j], lw);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = base + (uint64_t)u * 32;
+      st256(y + i * 32, v[u], i < nvec);
+    }
+  }
+}
+
 // ---- TMA bulk kernel ------------------------------------------------------
 __device__ __forceinline__ uint32_t saddr(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -270,26 +300,25 @@ ktma(const uint8_t *x, uint8_t *y, uint64_t ntiles, const __grid_constant__ LutW
 struct Variant {
   const char *name;
   const void *fn;
-  int threads, unroll, tma, tile, smem;
+  int threads, unroll, tma, tile, smem, cpw;
 };
 
 #define VR(OP, U, T, MINB, PF) \
-  Variant{"reg op" #OP " U" #U " T" #T " minb" #MINB " pf" #PF, (const void *)kreg<OP, U, T, MINB, PF>, T, U, 0, 0, 0}
+  Variant{"reg op" #OP " U" #U " T" #T " minb" #MINB " pf" #PF, (const void *)kreg<OP, U, T, MINB, PF>, T, U, 0, 0, 0, 0}
 #define VT(OP, TILE, ST, T, MINB)                                                                   \
   Variant{"tma op" #OP " tile" #TILE " st" #ST " T" #T " minb" #MINB, (const void *)ktma<OP, TILE, ST, T, MINB>, \
-          T, 0, 1, TILE, TILE * ST}
+          T, 0, 1, TILE, TILE * ST, 0}
+#define VF(OP, U, T, CPW) \
+  Variant{"flat op" #OP " U" #U " T" #T " cpw" #CPW, (const void *)kflat<OP, U, T, CPW>, T, U, 0, 0, 0, CPW}
 
 static Variant variants[] = {
-    VR(-1, 2, 256, 1, 0), VR(10, 2, 128, 1, 0),
-    VR(0, 2, 128, 1, 0), VR(0, 1, 128, 1, 0), VR(0, 2, 256, 1, 0), VR(0, 1, 256, 1, 0),
-    VR(0, 2, 64, 1, 0), VR(0, 4, 128, 1, 0), VR(0, 1, 128, 1, 1), VR(0, 2, 128, 1, 1),
-    VR(0, 1, 256, 8, 0), VR(0, 2, 256, 4, 0), VR(0, 2, 128, 8, 0), VR(0, 1, 512, 1, 0),
-    VR(3, 1, 128, 1, 0), VR(3, 2, 128, 1, 0), VR(3, 1, 256, 1, 0), VR(3, 1, 128, 1, 1),
-    VR(2, 1, 128, 1, 0), VR(2, 2, 128, 1, 0), VR(1, 1, 128, 1, 0), VR(1, 2, 128, 1, 0),
-    VT(-1, 16384, 4, 256, 1),
-    VT(0, 16384, 4, 256, 1), VT(0, 8192, 4, 256, 2), VT(0, 4096, 4, 128, 4), VT(0, 4096, 6, 128, 3),
-    VT(0, 8192, 6, 256, 1), VT(0, 2048, 8, 64, 6),
-    VT(3, 8192, 4, 256, 2), VT(3, 4096, 4, 128, 4),
+    VF(-1, 1, 256, 1), VF(-1, 2, 256, 1), VF(-1, 1, 128, 1), VF(-1, 1, 256, 4),
+    VR(0, 2, 64, 1, 0),
+    VF(0, 1, 256, 1), VF(0, 2, 256, 1), VF(0, 1, 128, 1), VF(0, 2, 128, 1), VF(0, 1, 64, 1),
+    VF(0, 1, 512, 1), VF(0, 1, 256, 2), VF(0, 1, 256, 4), VF(0, 2, 128, 2), VF(0, 4, 128, 1),
+    VF(10, 1, 256, 1), VF(10, 2, 128, 1),
+    VF(3, 1, 256, 1), VF(3, 1, 128, 1), VF(3, 2, 128, 1), VF(3, 1, 256, 2),
+    VF(2, 1, 256, 1), VF(2, 1, 128, 1), VF(1, 1, 256, 1), VF(1, 1, 128, 1),
 };
 
 int main() {
@@ -342,6 +371,13 @@ int main() {
         a1 = n * 2 / v.tile;
         a2 = 0;
         grid = (unsigned)std::min<uint64_t>((uint64_t)sms * bps, a1);
+      } else if (v.cpw) {
+        uint64_t nvec = n / 16;
+        uint64_t nchunks = (nvec + 32 * v.unroll - 1) / (32 * v.unroll);
+        uint64_t warps = (nchunks + v.cpw - 1) / v.cpw;
+        grid = (unsigned)((warps + v.threads / 32 - 1) / (v.threads / 32));
+        a1 = nvec;
+        a2 = nchunks;
       } else {
         uint64_t nvec = n / 16;
         uint64_t nchunks = (nvec + 32 * v.unroll - 1) / (32 * v.unroll);
