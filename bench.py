@@ -53,6 +53,11 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
+def _kd():
+    from paper_1909_07729_b200 import dist as kd
+    return kd
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -152,15 +157,14 @@ class Step:
 
 def barrier(world):
     if world > 1:
-        torch.distributed.barrier()
+        _kd().barrier()
 
 
 def max_over_ranks(v: float, world: int, device) -> float:
+    """Timing plumbing only (paper_1909_07729_b200.dist, tested with gloo)."""
     if world == 1:
         return v
-    t = torch.tensor([v], dtype=torch.float64, device=device)
-    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    return float(t.item())
+    return _kd().max_over_ranks(v, device)
 
 
 def time_windows(step: Step, K: int, W: int, world: int, device, clocks: ClockSampler | None,
@@ -283,18 +287,22 @@ def _cpu_model():
     return "unknown"
 
 
-def load_traffic(workload_op):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
-    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) \
-            if os.path.isdir(os.path.join(ROOT, "profiles")) else []:
-        if name.startswith("ncu_full_") and name.endswith(".json"):
-            try:
-                d = json.load(open(os.path.join(ROOT, "profiles", name)))
-                t = d.get("kernels", {}).get(workload_op)
-                if t and t.get("dram_bytes_per_launch"):
-                    return float(t["dram_bytes_per_launch"]), name
-            except Exception:
-                continue
+def load_traffic(tag_substr):
+    """dram bytes per launch of the dominant kernel from the newest committed
+    ncu --set full summary (profiles/ncu_full_rNN.json), if any."""
+    pdir = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(pdir):
+        return None, None
+    for name in sorted(os.listdir(pdir), reverse=True):
+        if not (name.startswith("ncu_full_") and name.endswith(".json")):
+            continue
+        try:
+            d = json.load(open(os.path.join(pdir, name)))
+        except Exception:
+            continue
+        for tag, ks in d.items():
+            if tag_substr in tag and ks and ks[0].get("dram_bytes_per_launch"):
+                return float(ks[0]["dram_bytes_per_launch"]), f"profiles/{name}:{tag}"
     return None, None
 
 
@@ -363,7 +371,7 @@ def main():
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=device)
+        _kd().init("nccl", device)
 
     import paper_1909_07729_b200 as kt
 
@@ -412,7 +420,7 @@ def main():
 
     if clocks:
         clocks.stop()
-    traffic, traffic_src = load_traffic(head_op)
+    traffic, traffic_src = load_traffic("tanh_bf16")
     if rank == 0:
         out = {
             "metric": "K-TanH Gelem/s and achieved HBM GB/s vs ~8 TB/s peak at 1/2/4/8 B200",
