@@ -40,6 +40,15 @@ static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+// L2 prefetch of [p, p + bytes) by one thread (TMA bulk prefetch, no data
+// returned to the SM).  A prefetch has no architectural effect on the values
+// later loads observe (L2 is the point of coherence for global memory), so it
+// is issued BEFORE griddepcontrol.wait: under PDL this warms L2 with the
+// chunk while the preceding grid drains.
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // PDL: wait for the preceding grid (no-op without a programmatic dependency),
 // then let the next grid in the stream begin launching.
 __device__ __forceinline__ void pdl_enter() {
@@ -76,17 +85,22 @@ __device__ __forceinline__ void scalar_span(const uint8_t *xp, uint8_t *yp, uint
 // Main streaming kernel.  x/y: original (element-aligned) pointers; `head`
 // elements precede the first 32-B boundary of x (and of y: same offset mod
 // 32, checked on the host); nvec vectors follow; then `tail` elements.
-template <int OP, int FMT, bool NC>
+template <int OP, int FMT, bool NC, bool PF>
 __global__ void __launch_bounds__(kThreads)
 k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
       const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
   const LaneLut L = load_lane_lut(lut);
-  pdl_enter();
   const uint32_t lane = threadIdx.x & 31;
   const uint8_t *xb = x + (size_t)head * es;
   uint8_t *yb = y + (size_t)head * es;
   const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);   // this warp's chunk
+  if (PF && lane == 0 && c * kChunkVecs < nvec) {
+    const uint64_t left = nvec - c * kChunkVecs;
+    prefetch_l2(xb + c * kChunkVecs * kVecBytes,
+                (uint32_t)((left < kChunkVecs ? left : kChunkVecs) * kVecBytes));
+  }
+  pdl_enter();
   const uint64_t base = c * kChunkVecs + lane;
   uint32_t v[kUnroll][8];
 #pragma unroll
@@ -192,6 +206,16 @@ static bool pdl_enabled() {
 }
 
 // cudaLaunchKernelEx with the programmatic-stream-serialization attribute.
+// Early L2 prefetch of each warp's input chunk (before the PDL wait);
+// KT_PREFETCH=0 disables.
+static bool prefetch_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("KT_PREFETCH");
+    return !(e && e[0] == '0');
+  }();
+  return on && pdl_enabled();
+}
+
 template <typename... KArgs, typename... Args>
 static cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -250,9 +274,12 @@ static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &l
   const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
   if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const unsigned grid = flat_grid(nchunks);
-  if (x != y)
-    return launch(k_map<OP, FMT, true>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
-  return launch(k_map<OP, FMT, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
+  if (x != y) {
+    if (prefetch_enabled())
+      return launch(k_map<OP, FMT, true, true>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
+    return launch(k_map<OP, FMT, true, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
+  }
+  return launch(k_map<OP, FMT, false, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
 }
 
 cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const LutWords &lut,

@@ -63,6 +63,18 @@ def test_exhaustive_bf16(kt, op):
     check(op, "bf16", u16(y), oracle_bf16(op, u16(x)), f"{op} bf16 exhaustive")
 
 
+def test_exhaustive_bf16_derived_ulp_report(kt):
+    """DESIGN.md R-DERIVED: the derived ops are expected to be bit-identical to the
+    oracle on every BF16 pattern (NaN by class) even though 1 ulp is allowed."""
+    from _cmp import ulp_dist
+    x = WL.make_input("c1_exhaustive_bf16", device="cuda")
+    worst = {}
+    for op in ("sigmoid", "swish", "gelu"):
+        worst[op] = int(ulp_dist(u16(call(kt, op, "bf16", x)), oracle_bf16(op, u16(x)), 16).max())
+    print("max ulp vs oracle over all BF16 patterns:", worst)
+    assert max(worst.values()) <= 1
+
+
 def test_exhaustive_bf16_ktanh_nan_passthrough(kt):
     x = WL.make_input("c1_exhaustive_bf16", device="cuda")
     y = u16(kt.ktanh_bf16(x))
