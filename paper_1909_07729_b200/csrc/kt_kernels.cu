@@ -88,14 +88,15 @@ __device__ __forceinline__ void scalar_span(const uint8_t *xp, uint8_t *yp, uint
 template <int OP, int FMT, bool NC, bool PF>
 __global__ void __launch_bounds__(kThreads)
 k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
-      const __grid_constant__ LutWords lut) {
+      uint32_t pf_blocks, const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
   const LaneLut L = load_lane_lut(lut);
   const uint32_t lane = threadIdx.x & 31;
   const uint8_t *xb = x + (size_t)head * es;
   uint8_t *yb = y + (size_t)head * es;
   const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);   // this warp's chunk
-  if (PF && lane == 0 && c * kChunkVecs < nvec) {
+  // only the first resident wave can be waiting behind a predecessor's tail
+  if (PF && blockIdx.x < pf_blocks && lane == 0 && c * kChunkVecs < nvec) {
     const uint64_t left = nvec - c * kChunkVecs;
     prefetch_l2(xb + c * kChunkVecs * kVecBytes,
                 (uint32_t)((left < kChunkVecs ? left : kChunkVecs) * kVecBytes));
@@ -150,11 +151,16 @@ k_map_elem(const uint8_t *__restrict__ x, uint8_t *__restrict__ y, uint64_t n,
 template <bool NC>
 __global__ void __launch_bounds__(kThreads)
 k_lstm(const uint8_t *x, uint8_t *y, uint32_t nvec, uint32_t vpr, uint32_t vpq, int tanh_quarter,
-       const __grid_constant__ LutWords lut) {
+       uint32_t pf_blocks, const __grid_constant__ LutWords lut) {
   const LaneLut L = load_lane_lut(lut);
-  pdl_enter();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t c = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (NC && blockIdx.x < pf_blocks && lane == 0 && c * kChunkVecs < nvec) {
+    const uint32_t left = nvec - c * kChunkVecs;
+    prefetch_l2(x + (size_t)c * kChunkVecs * kVecBytes,
+                (left < (uint32_t)kChunkVecs ? left : (uint32_t)kChunkVecs) * kVecBytes);
+  }
+  pdl_enter();
   const uint32_t base = c * kChunkVecs + lane;
   uint32_t v[kUnroll][8];
   bool tq[kUnroll];
@@ -275,11 +281,15 @@ static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &l
   if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const unsigned grid = flat_grid(nchunks);
   if (x != y) {
-    if (prefetch_enabled())
-      return launch(k_map<OP, FMT, true, true>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
-    return launch(k_map<OP, FMT, true, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
+    if (prefetch_enabled()) {
+      static const int bps = resident_blocks(k_map<OP, FMT, true, true>);
+      const uint32_t pf_blocks = (uint32_t)(li.sm_count * bps);
+      return launch(k_map<OP, FMT, true, true>, grid, s, xp, yp, (uint32_t)head, nvec, tail,
+                    pf_blocks, lut);
+    }
+    return launch(k_map<OP, FMT, true, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, lut);
   }
-  return launch(k_map<OP, FMT, false, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, lut);
+  return launch(k_map<OP, FMT, false, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, lut);
 }
 
 cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const LutWords &lut,
@@ -312,9 +322,13 @@ cudaError_t launch_lstm(const uint16_t *x, uint16_t *y, size_t rows, size_t hidd
     const uint8_t *xp = reinterpret_cast<const uint8_t *>(x);
     uint8_t *yp = reinterpret_cast<uint8_t *>(y);
     const uint32_t vpr = (uint32_t)(hidden / 4), vpq = (uint32_t)(hidden / 16);
-    if (static_cast<const void *>(x) != static_cast<const void *>(y))
-      return launch(k_lstm<true>, grid, s, xp, yp, (uint32_t)nvec, vpr, vpq, tanh_quarter, lut);
-    return launch(k_lstm<false>, grid, s, xp, yp, (uint32_t)nvec, vpr, vpq, tanh_quarter, lut);
+    if (static_cast<const void *>(x) != static_cast<const void *>(y)) {
+      static const int bps = resident_blocks(k_lstm<true>);
+      const uint32_t pf_blocks = prefetch_enabled() ? (uint32_t)(li.sm_count * bps) : 0u;
+      return launch(k_lstm<true>, grid, s, xp, yp, (uint32_t)nvec, vpr, vpq, tanh_quarter,
+                    pf_blocks, lut);
+    }
+    return launch(k_lstm<false>, grid, s, xp, yp, (uint32_t)nvec, vpr, vpq, tanh_quarter, 0u, lut);
   }
   static const int bps = resident_blocks(k_lstm_elem);
   const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
