@@ -151,9 +151,9 @@ KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size
  * (cudaHostAlloc / torch pin_memory) for asynchronous, full-bandwidth
  * copies; pageable memory works but the copies become synchronous.
  * d_work: caller-owned device scratch of work_bytes; at least
- * 3 * 2 * 4096 * elem_size bytes (KT_ERR_ARG otherwise); larger scratch
- * gives larger chunks (chunk = work_bytes / (6 * elem_size), rounded down
- * to a multiple of 256 elements). */
+ * 3 * 2 * 4096 * elem_size bytes (KT_ERR_ARG otherwise).  The chunk is
+ * about n/16 elements (at least 1 MiB, at most work_bytes / (6 * elem_size)),
+ * a multiple of 256 elements. */
 KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, void *y_host,
                                size_t n, kt_lut lut, void *d_work, size_t work_bytes,
                                void *stream);

@@ -293,6 +293,12 @@ KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, voi
   size_t chunk = work_bytes / (2 * kStages * es);
   chunk -= chunk % 256;
   if (chunk < 4096) return fail(KT_ERR_ARG, "work_bytes too small (need >= %zu)", 2 * kStages * es * 4096);
+  // ~16 chunks per call (at least 1 MiB each) keeps both copy directions busy
+  // and the pipeline fill/drain (one chunk's H2D + D2H) short.
+  size_t want = (n / 16 + 255) / 256 * 256;
+  const size_t min_chunk = ((size_t)1 << 20) / es;
+  if (want < min_chunk) want = min_chunk;
+  if (want < chunk) chunk = want;
   kt::LaunchInfo li;
   kt_status s = launch_info(&li);
   if (s != KT_OK) return s;
