@@ -142,9 +142,10 @@ KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size
 /* ---------------------------------------------------------------------- */
 
 /* y_host = op(x_host) for n elements resident in HOST memory.  The call
- * splits the data into chunks, and for each chunk enqueues host->device
- * copy, kernel and device->host copy on one of three internal streams so
- * that both copy directions and the kernel overlap; the internal streams
+ * splits the data into chunks and pipelines them over three internal
+ * streams, one per engine (host->device copies, kernels, device->host
+ * copies), with three rotating device buffers, so that both copy directions
+ * and the kernel overlap; the internal streams
  * are forked from and joined back into `stream`, so the whole operation is
  * ordered on `stream` and the call returns without waiting: synchronise
  * `stream` before reading y_host.  x_host / y_host should be pinned
@@ -152,7 +153,7 @@ KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size
  * copies; pageable memory works but the copies become synchronous.
  * d_work: caller-owned device scratch of work_bytes; at least
  * 3 * 2 * 4096 * elem_size bytes (KT_ERR_ARG otherwise).  The chunk is
- * about n/16 elements (at least 1 MiB, at most work_bytes / (6 * elem_size)),
+ * about n/8 elements (at least 1 MiB, at most work_bytes / (6 * elem_size)),
  * a multiple of 256 elements. */
 KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, void *y_host,
                                size_t n, kt_lut lut, void *d_work, size_t work_bytes,

@@ -125,8 +125,9 @@ class Lut:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            _lib.kt_lut_destroy(h)
+        lib = globals().get("_lib")
+        if h is not None and h.value and lib is not None:
+            lib.kt_lut_destroy(h)
             self._h = _vp()
 
 

@@ -5,6 +5,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -177,11 +178,17 @@ kt_status run_map(int op, int fmt, const void *x, void *y, size_t n, kt_lut lut,
 }
 
 // ---- host-buffer path -------------------------------------------------------
+// Role streams: [0] host->device copies, [1] kernels, [2] device->host copies,
+// so each copy engine streams chunks back to back.  kBufs buffer pairs
+// (dx, dy) rotate; per buffer b: ev_in (H2D done), ev_comp (kernel done, dx
+// free), ev_out (D2H done, dy free).
 constexpr int kStages = 3;
+constexpr int kBufs = 3;
 struct HostPipe {
   bool init = false;
   cudaStream_t st[kStages];
   cudaEvent_t fork, join[kStages];
+  cudaEvent_t ev_in[kBufs], ev_comp[kBufs], ev_out[kBufs];
   std::mutex mu;
 };
 HostPipe g_pipe[kMaxDev];
@@ -194,11 +201,16 @@ kt_status pipe_for(int dev, HostPipe **out) {
     for (int i = 0; i < kStages; ++i)
       if ((e = cudaStreamCreateWithFlags(&p.st[i], cudaStreamNonBlocking)) != cudaSuccess)
         return cuda_fail(e, "cudaStreamCreate");
-    if ((e = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming)) != cudaSuccess)
-      return cuda_fail(e, "cudaEventCreate");
-    for (int i = 0; i < kStages; ++i)
-      if ((e = cudaEventCreateWithFlags(&p.join[i], cudaEventDisableTiming)) != cudaSuccess)
+    cudaEvent_t *evs[] = {&p.fork, &p.join[0], &p.join[1], &p.join[2]};
+    for (cudaEvent_t *ev : evs)
+      if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
         return cuda_fail(e, "cudaEventCreate");
+    for (int i = 0; i < kBufs; ++i) {
+      if ((e = cudaEventCreateWithFlags(&p.ev_in[i], cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&p.ev_comp[i], cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&p.ev_out[i], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "cudaEventCreate");
+    }
     p.init = true;
   }
   *out = &p;
@@ -290,14 +302,19 @@ KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, voi
   if (n == 0) return KT_OK;
   if (!x_host || !y_host || !d_work) return fail(KT_ERR_ARG, "NULL pointer");
   const size_t es = dtype == KT_BF16 ? 2 : 4;
-  size_t chunk = work_bytes / (2 * kStages * es);
+  size_t chunk = work_bytes / (2 * kBufs * es);
   chunk -= chunk % 256;
-  if (chunk < 4096) return fail(KT_ERR_ARG, "work_bytes too small (need >= %zu)", 2 * kStages * es * 4096);
-  // ~16 chunks per call (at least 1 MiB each) keeps both copy directions busy
-  // and the pipeline fill/drain (one chunk's H2D + D2H) short.
-  size_t want = (n / 16 + 255) / 256 * 256;
+  if (chunk < 4096)
+    return fail(KT_ERR_ARG, "work_bytes too small (need >= %zu)", 2 * kBufs * es * 4096);
+  // ~8 chunks per call (at least 1 MiB each): both copy directions stay busy
+  // and the pipeline fill/drain (one chunk's H2D + D2H) stays short.
+  size_t want = (n / 8 + 255) / 256 * 256;
   const size_t min_chunk = ((size_t)1 << 20) / es;
   if (want < min_chunk) want = min_chunk;
+  if (const char *ev = getenv("KT_HOST_CHUNK")) {   // tuning override (elements)
+    const size_t c = (size_t)strtoull(ev, nullptr, 10);
+    if (c >= 4096) want = c - c % 256;
+  }
   if (want < chunk) chunk = want;
   kt::LaunchInfo li;
   kt_status s = launch_info(&li);
@@ -307,34 +324,37 @@ KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, voi
   if ((s = pipe_for(li.device, &p)) != KT_OK) return s;
   std::lock_guard<std::mutex> g(p->mu);
   cudaStream_t caller = (cudaStream_t)stream;
+  cudaStream_t h2d = p->st[0], comp = p->st[1], d2h = p->st[2];
   cudaError_t e;
-  if ((e = cudaEventRecord(p->fork, caller)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
-  for (int i = 0; i < kStages; ++i)
-    if ((e = cudaStreamWaitEvent(p->st[i], p->fork, 0)) != cudaSuccess)
-      return cuda_fail(e, "cudaStreamWaitEvent");
+#define KT_CK(call, what) \
+  if ((e = (call)) != cudaSuccess) return cuda_fail(e, what);
+  KT_CK(cudaEventRecord(p->fork, caller), "cudaEventRecord");
+  for (int i = 0; i < kStages; ++i) KT_CK(cudaStreamWaitEvent(p->st[i], p->fork, 0), "cudaStreamWaitEvent");
   const char *xh = static_cast<const char *>(x_host);
   char *yh = static_cast<char *>(y_host);
   char *work = static_cast<char *>(d_work);
   size_t k = 0;
   for (size_t off = 0; off < n; off += chunk, ++k) {
     const size_t cnt = (n - off < chunk) ? n - off : chunk;
-    const int st = (int)(k % kStages);
-    cudaStream_t ss = p->st[st];
-    char *dx = work + (size_t)st * 2 * chunk * es;
+    const int b = (int)(k % kBufs);
+    char *dx = work + (size_t)b * 2 * chunk * es;
     char *dy = dx + chunk * es;
-    if ((e = cudaMemcpyAsync(dx, xh + off * es, cnt * es, cudaMemcpyHostToDevice, ss)) != cudaSuccess)
-      return cuda_fail(e, "cudaMemcpyAsync H2D");
-    if ((e = kt::launch_map((int)op, (int)dtype, dx, dy, cnt, lut->words, ss, li)) != cudaSuccess)
-      return cuda_fail(e, "kernel launch");
-    if ((e = cudaMemcpyAsync(yh + off * es, dy, cnt * es, cudaMemcpyDeviceToHost, ss)) != cudaSuccess)
-      return cuda_fail(e, "cudaMemcpyAsync D2H");
+    if (k >= (size_t)kBufs) KT_CK(cudaStreamWaitEvent(h2d, p->ev_comp[b], 0), "wait");  // dx free
+    KT_CK(cudaMemcpyAsync(dx, xh + off * es, cnt * es, cudaMemcpyHostToDevice, h2d), "H2D");
+    KT_CK(cudaEventRecord(p->ev_in[b], h2d), "record");
+    KT_CK(cudaStreamWaitEvent(comp, p->ev_in[b], 0), "wait");
+    if (k >= (size_t)kBufs) KT_CK(cudaStreamWaitEvent(comp, p->ev_out[b], 0), "wait");  // dy free
+    KT_CK(kt::launch_map((int)op, (int)dtype, dx, dy, cnt, lut->words, comp, li), "kernel launch");
+    KT_CK(cudaEventRecord(p->ev_comp[b], comp), "record");
+    KT_CK(cudaStreamWaitEvent(d2h, p->ev_comp[b], 0), "wait");
+    KT_CK(cudaMemcpyAsync(yh + off * es, dy, cnt * es, cudaMemcpyDeviceToHost, d2h), "D2H");
+    KT_CK(cudaEventRecord(p->ev_out[b], d2h), "record");
   }
   for (int i = 0; i < kStages; ++i) {
-    if ((e = cudaEventRecord(p->join[i], p->st[i])) != cudaSuccess)
-      return cuda_fail(e, "cudaEventRecord");
-    if ((e = cudaStreamWaitEvent(caller, p->join[i], 0)) != cudaSuccess)
-      return cuda_fail(e, "cudaStreamWaitEvent");
+    KT_CK(cudaEventRecord(p->join[i], p->st[i]), "record");
+    KT_CK(cudaStreamWaitEvent(caller, p->join[i], 0), "wait");
   }
+#undef KT_CK
   return KT_OK;
 }
 
