@@ -141,13 +141,37 @@ def paper_lut() -> Lut:
     return _default_lut
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device_index=None):
     import torch
     if stream is None:
-        return torch.cuda.current_stream().cuda_stream
+        if device_index is None:
+            device_index = torch.cuda.current_device()
+        return torch._C._cuda_getCurrentRawStream(device_index)
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
+
+
+class _on_device:
+    """Make x's device current for the call only if it is not already."""
+    __slots__ = ("idx", "prev")
+
+    def __init__(self, idx):
+        self.idx = idx
+        self.prev = None
+
+    def __enter__(self):
+        import torch
+        cur = torch.cuda.current_device()
+        if cur != self.idx:
+            self.prev = cur
+            torch.cuda.set_device(self.idx)
+        return self
+
+    def __exit__(self, *a):
+        if self.prev is not None:
+            import torch
+            torch.cuda.set_device(self.prev)
 
 
 def _prep(x, out, dtype):
@@ -174,8 +198,10 @@ def _make_call(name, dtype_name):
         dt = torch.bfloat16 if dtype_name == "bf16" else torch.float32
         out = _prep(x, out, dt)
         lut = lut or paper_lut()
-        with torch.cuda.device(x.device):
-            _check(fn(x.data_ptr(), out.data_ptr(), x.numel(), lut.handle, _stream_ptr(stream)), name)
+        idx = x.device.index
+        with _on_device(idx):
+            _check(fn(x.data_ptr(), out.data_ptr(), x.numel(), lut.handle, _stream_ptr(stream, idx)),
+                   name)
         return out
 
     call.__name__ = name
