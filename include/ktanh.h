@@ -138,6 +138,41 @@ KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size
                           kt_lut lut, void *stream);
 
 /* ---------------------------------------------------------------------- */
+/* Backward passes (the paper trains GNMT with K-TanH,   */
+/* PAPER.md:308, but never states the gradient).  Reading R-BWD            */
+/* (DESIGN.md): the derivative of the approximated function taken through  */
+/* the K-TanH value, dx = dy * g, fp32 arithmetic with a fixed op order and */
+/* one rounding to the format:                                              */
+/*   tanh:    g = 1 - y^2        (y = saved K-TanH output)                  */
+/*   sigmoid: g = s (1 - s)      (s = saved K-Sigmoid output)               */
+/*   swish:   g = (1+t)/2 + x (1-t^2)/4,  t = K-TanH(RN(x/2))               */
+/*   gelu:    g = (1+t)/2 + x/2 (1-t^2) sqrt(2/pi)(1 + 3*0.044715 x^2),     */
+/*            t = K-TanH(u), u as in kgelu_*                                */
+/* Same conventions as the forward maps; dx may equal dy or the first       */
+/* input (in place), any other overlap -> KT_ERR_ARG.  tanh/sigmoid need no */
+/* table; swish/gelu recompute K-TanH and need lut (NULL -> KT_ERR_ARG).    */
+/* 6 bytes of HBM traffic per BF16 element (12 per F32).                    */
+/* ---------------------------------------------------------------------- */
+KT_API kt_status ktanh_bwd_bf16(const uint16_t *y, const uint16_t *dy, uint16_t *dx, size_t n,
+                                void *stream);
+KT_API kt_status ktanh_bwd_f32(const float *y, const float *dy, float *dx, size_t n, void *stream);
+KT_API kt_status ksigmoid_bwd_bf16(const uint16_t *s, const uint16_t *dy, uint16_t *dx, size_t n,
+                                   void *stream);
+KT_API kt_status ksigmoid_bwd_f32(const float *s, const float *dy, float *dx, size_t n,
+                                  void *stream);
+KT_API kt_status kswish_bwd_bf16(const uint16_t *x, const uint16_t *dy, uint16_t *dx, size_t n,
+                                 kt_lut lut, void *stream);
+KT_API kt_status kswish_bwd_f32(const float *x, const float *dy, float *dx, size_t n, kt_lut lut,
+                                void *stream);
+KT_API kt_status kgelu_bwd_bf16(const uint16_t *x, const uint16_t *dy, uint16_t *dx, size_t n,
+                                kt_lut lut, void *stream);
+KT_API kt_status kgelu_bwd_f32(const float *x, const float *dy, float *dx, size_t n, kt_lut lut,
+                               void *stream);
+/* Generic dispatcher; a = y (tanh), s (sigmoid) or x (swish, gelu). */
+KT_API kt_status kt_apply_bwd(kt_op op, kt_dtype dtype, const void *a, const void *dy, void *dx,
+                              size_t n, kt_lut lut, void *stream);
+
+/* ---------------------------------------------------------------------- */
 /* Host-buffer path (the end-to-end call a user with host data makes).    */
 /* ---------------------------------------------------------------------- */
 

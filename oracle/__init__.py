@@ -75,6 +75,10 @@ def lib():
             L.kto_interval_sse.restype = ctypes.c_double
             L.kto_overflow_flag.argtypes = []
             L.kto_overflow_flag.restype = ctypes.c_int
+            L.kto_bwd_map_bf16.argtypes = [ctypes.c_int, u16p, u16p, u16p, ctypes.c_size_t, ip, ip, ip]
+            L.kto_bwd_map_bf16.restype = None
+            L.kto_bwd_map_f32.argtypes = [ctypes.c_int, u32p, u32p, u32p, ctypes.c_size_t, ip, ip, ip]
+            L.kto_bwd_map_f32.restype = None
             L.kto_gelu_consts.argtypes = [ctypes.c_int]
             L.kto_gelu_consts.restype = ctypes.c_uint32
             _lib = L
@@ -163,6 +167,31 @@ def map_f32(op: str, x_u32: np.ndarray, lut: Lut | None = None) -> np.ndarray:
     y = np.empty_like(x)
     u32p = ctypes.POINTER(ctypes.c_uint32)
     lib().kto_map_f32(OPS[op], x.ctypes.data_as(u32p), y.ctypes.data_as(u32p), x.size, *lut.ptrs())
+    return y
+
+
+def bwd_bf16(op: str, a_u16: np.ndarray, dy_u16: np.ndarray, lut: Lut | None = None) -> np.ndarray:
+    """Backward pass (reading R-BWD): a = saved output (tanh, sigmoid) or input x (swish, gelu)."""
+    lut = _lut(lut)
+    a = np.ascontiguousarray(a_u16, dtype=np.uint16)
+    d = np.ascontiguousarray(dy_u16, dtype=np.uint16)
+    assert a.shape == d.shape
+    y = np.empty_like(a)
+    u16p = ctypes.POINTER(ctypes.c_uint16)
+    lib().kto_bwd_map_bf16(OPS[op], a.ctypes.data_as(u16p), d.ctypes.data_as(u16p),
+                           y.ctypes.data_as(u16p), a.size, *lut.ptrs())
+    return y
+
+
+def bwd_f32(op: str, a_u32: np.ndarray, dy_u32: np.ndarray, lut: Lut | None = None) -> np.ndarray:
+    lut = _lut(lut)
+    a = np.ascontiguousarray(a_u32, dtype=np.uint32)
+    d = np.ascontiguousarray(dy_u32, dtype=np.uint32)
+    assert a.shape == d.shape
+    y = np.empty_like(a)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    lib().kto_bwd_map_f32(OPS[op], a.ctypes.data_as(u32p), d.ctypes.data_as(u32p),
+                          y.ctypes.data_as(u32p), a.size, *lut.ptrs())
     return y
 
 

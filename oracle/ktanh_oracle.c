@@ -30,6 +30,9 @@
  *                                               error bound, invariants)
  *   kto_ksigmoid_* ............................ pinned (exact rational (1+t)/2)
  *   kto_kswish_* / kto_kgelu_* ................ pinned (special cases + error bound)
+ *   kto_bwd_* (reading R-BWD) ................. pinned (closed forms at 0, in the
+ *                                               bypass/saturation regions, and
+ *                                               error bounds vs the true derivative)
  *   kto_build_lut (Sec. 2.4 optimizer) ........ pinned (Table 1 match counts,
  *                                               SSE dominance, Table 2 ablation)
  *   kto_bounds ................................ pinned (exhaustive no-overflow)
@@ -275,6 +278,67 @@ uint32_t kto_kgelu_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
     uint32_t t = kto_ktanh_f32(bits_from_f32(u), TE, Tr, Tb);
     double tv = (double)f32_from_bits(t);
     return bits_from_f32((float)((double)xf / 2.0 * (1.0 + tv)));
+}
+
+/* ------------------------------------------------------------------ */
+/* Backward passes.  The paper trains GNMT with K-TanH */
+/* but never states the gradient; reading R-BWD: the  */
+/* derivative of the function K-TanH approximates, evaluated through the  */
+/* K-TanH value, in binary64, rounded once to the format:                 */
+/*   tanh:    dx = dy (1 - y^2),          y = saved K-TanH output         */
+/*   sigmoid: dx = dy s (1 - s),          s = saved K-Sigmoid output      */
+/*   swish:   dx = dy ((1+t)/2 + x (1-t^2)/4),  t = K-TanH(RN(x/2))       */
+/*   gelu:    dx = dy ((1+t)/2 + x/2 (1-t^2) sqrt(2/pi)(1 + 3 a x^2)),   */
+/*            t = K-TanH(u) with u as in the forward (R-GELU-ARG)         */
+/* op: 0 tanh, 1 sigmoid, 2 swish, 3 gelu; a = saved output (0, 1) or the  */
+/* input x (2, 3).                                                         */
+/* ------------------------------------------------------------------ */
+static double bwd_factor(int op, double a, double tv)
+{
+    const double c = sqrt(2.0 / M_PI), ga = 0.044715;
+    switch (op) {
+    case 0: return 1.0 - a * a;
+    case 1: return a * (1.0 - a);
+    case 2: return (1.0 + tv) / 2.0 + a * (1.0 - tv * tv) / 4.0;
+    default: return (1.0 + tv) / 2.0 + a / 2.0 * (1.0 - tv * tv) * c * (1.0 + 3.0 * ga * a * a);
+    }
+}
+
+uint16_t kto_bwd_bf16(int op, uint16_t a, uint16_t dy, const int *TE, const int *Tr, const int *Tb)
+{
+    double av = kto_bf16_decode(a), dv = kto_bf16_decode(dy), tv = 0.0;
+    if (op == 2) {
+        tv = kto_bf16_decode(kto_ktanh_bf16(kto_bf16_encode_rne(av / 2.0), TE, Tr, Tb));
+    } else if (op == 3) {
+        float u = gelu_arg_f32((float)av);
+        tv = kto_bf16_decode(kto_ktanh_bf16(kto_bf16_encode_rne((double)u), TE, Tr, Tb));
+    }
+    return kto_bf16_encode_rne(dv * bwd_factor(op, av, tv));
+}
+
+uint32_t kto_bwd_f32(int op, uint32_t a, uint32_t dy, const int *TE, const int *Tr, const int *Tb)
+{
+    double av = (double)f32_from_bits(a), dv = (double)f32_from_bits(dy), tv = 0.0;
+    if (op == 2) {
+        float h = (float)(av / 2.0);
+        tv = (double)f32_from_bits(kto_ktanh_f32(bits_from_f32(h), TE, Tr, Tb));
+    } else if (op == 3) {
+        float u = gelu_arg_f32((float)av);
+        tv = (double)f32_from_bits(kto_ktanh_f32(bits_from_f32(u), TE, Tr, Tb));
+    }
+    return bits_from_f32((float)(dv * bwd_factor(op, av, tv)));
+}
+
+void kto_bwd_map_bf16(int op, const uint16_t *a, const uint16_t *dy, uint16_t *dx, size_t n,
+                      const int *TE, const int *Tr, const int *Tb)
+{
+    for (size_t i = 0; i < n; ++i) dx[i] = kto_bwd_bf16(op, a[i], dy[i], TE, Tr, Tb);
+}
+
+void kto_bwd_map_f32(int op, const uint32_t *a, const uint32_t *dy, uint32_t *dx, size_t n,
+                     const int *TE, const int *Tr, const int *Tb)
+{
+    for (size_t i = 0; i < n; ++i) dx[i] = kto_bwd_f32(op, a[i], dy[i], TE, Tr, Tb);
 }
 
 /* ------------------------------------------------------------------ */

@@ -36,7 +36,9 @@ DTYPES = {"bf16": 0, "f32": 1}
 
 MAP_CALLS = ("ktanh_bf16", "ktanh_f32", "ksigmoid_bf16", "ksigmoid_f32",
              "kswish_bf16", "kswish_f32", "kgelu_bf16", "kgelu_f32")
-EXPORTS = MAP_CALLS + ("kt_lut_create", "kt_lut_create_paper", "kt_lut_get", "kt_lut_destroy",
+BWD_CALLS = ("ktanh_bwd_bf16", "ktanh_bwd_f32", "ksigmoid_bwd_bf16", "ksigmoid_bwd_f32")
+BWD_LUT_CALLS = ("kswish_bwd_bf16", "kswish_bwd_f32", "kgelu_bwd_bf16", "kgelu_bwd_f32")
+EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_create", "kt_lut_create_paper", "kt_lut_get", "kt_lut_destroy",
                        "klstm_gates_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
                        "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count")
 
@@ -44,6 +46,16 @@ for _name in MAP_CALLS:
     _f = getattr(_lib, _name)
     _f.argtypes = [_vp, _vp, _sz, _vp, _vp]
     _f.restype = ctypes.c_int
+for _name in BWD_CALLS:
+    _f = getattr(_lib, _name)
+    _f.argtypes = [_vp, _vp, _vp, _sz, _vp]
+    _f.restype = ctypes.c_int
+for _name in BWD_LUT_CALLS:
+    _f = getattr(_lib, _name)
+    _f.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
+    _f.restype = ctypes.c_int
+_lib.kt_apply_bwd.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _sz, _vp, _vp]
+_lib.kt_apply_bwd.restype = ctypes.c_int
 _lib.kt_lut_create.argtypes = [_c_i32p, _c_i32p, _c_i32p, ctypes.POINTER(_vp)]
 _lib.kt_lut_create.restype = ctypes.c_int
 _lib.kt_lut_create_paper.argtypes = [ctypes.POINTER(_vp)]
@@ -217,6 +229,43 @@ kswish_bf16 = _make_call("kswish_bf16", "bf16")
 kswish_f32 = _make_call("kswish_f32", "f32")
 kgelu_bf16 = _make_call("kgelu_bf16", "bf16")
 kgelu_f32 = _make_call("kgelu_f32", "f32")
+
+
+def _make_bwd(name, dtype_name, needs_lut):
+    fn = getattr(_lib, name)
+
+    def call(a, dy, out=None, lut: Lut | None = None, stream=None):
+        """dx = dy * g(a); a = saved output (tanh, sigmoid) or input x (swish, gelu)."""
+        import torch
+        dt = torch.bfloat16 if dtype_name == "bf16" else torch.float32
+        out = _prep(a, out, dt)
+        _prep(dy, out, dt)
+        if dy.numel() != a.numel():
+            raise ValueError("a and dy must have the same number of elements")
+        idx = a.device.index
+        with _on_device(idx):
+            if needs_lut:
+                lut = lut or paper_lut()
+                st = fn(a.data_ptr(), dy.data_ptr(), out.data_ptr(), a.numel(), lut.handle,
+                        _stream_ptr(stream, idx))
+            else:
+                st = fn(a.data_ptr(), dy.data_ptr(), out.data_ptr(), a.numel(),
+                        _stream_ptr(stream, idx))
+            _check(st, name)
+        return out
+
+    call.__name__ = name
+    return call
+
+
+ktanh_bwd_bf16 = _make_bwd("ktanh_bwd_bf16", "bf16", False)
+ktanh_bwd_f32 = _make_bwd("ktanh_bwd_f32", "f32", False)
+ksigmoid_bwd_bf16 = _make_bwd("ksigmoid_bwd_bf16", "bf16", False)
+ksigmoid_bwd_f32 = _make_bwd("ksigmoid_bwd_f32", "f32", False)
+kswish_bwd_bf16 = _make_bwd("kswish_bwd_bf16", "bf16", True)
+kswish_bwd_f32 = _make_bwd("kswish_bwd_f32", "f32", True)
+kgelu_bwd_bf16 = _make_bwd("kgelu_bwd_bf16", "bf16", True)
+kgelu_bwd_f32 = _make_bwd("kgelu_bwd_f32", "f32", True)
 
 
 def klstm_gates_bf16(x, hidden: int, tanh_quarter: int = 2, out=None, lut: Lut | None = None,

@@ -177,6 +177,38 @@ kt_status run_map(int op, int fmt, const void *x, void *y, size_t n, kt_lut lut,
   return KT_OK;
 }
 
+bool overlaps(const void *p, const void *q, size_t bytes) {
+  const uintptr_t a = (uintptr_t)p, b = (uintptr_t)q;
+  return p != q && a < b + bytes && b < a + bytes;
+}
+
+kt_status run_bwd(int op, int fmt, const void *a, const void *dy, void *dx, size_t n, kt_lut lut,
+                  void *stream) {
+  if (op < 0 || op > 3 || fmt < 0 || fmt > 1) return fail(KT_ERR_ARG, "bad op/dtype");
+  if ((op == kt::OP_SWISH || op == kt::OP_GELU) && !lut)
+    return fail(KT_ERR_ARG, "lut is NULL (needed to recompute K-TanH)");
+  if (n == 0) return KT_OK;
+  const size_t es = fmt == kt::FMT_BF16 ? 2 : 4;
+  if (!a || !dy || !dx) return fail(KT_ERR_ARG, "NULL pointer with n = %zu", n);
+  if ((uintptr_t)a % es || (uintptr_t)dy % es || (uintptr_t)dx % es)
+    return fail(KT_ERR_ARG, "pointers must be %zu-byte aligned", es);
+  if (n > SIZE_MAX / es) return fail(KT_ERR_ARG, "n too large");
+  const size_t bytes = n * es;
+  if (overlaps(dx, a, bytes) || overlaps(dx, dy, bytes))
+    return fail(KT_ERR_ARG, "dx overlaps an input without being equal to it");
+  kt::LaunchInfo li;
+  kt_status s = launch_info(&li);
+  if (s != KT_OK) return s;
+  if ((s = check_device_ptr(a, li.device, "a")) != KT_OK) return s;
+  if ((s = check_device_ptr(dy, li.device, "dy")) != KT_OK) return s;
+  if ((s = check_device_ptr(dx, li.device, "dx")) != KT_OK) return s;
+  static const kt::LutWords kNoLut = {};
+  cudaError_t e = kt::launch_bwd(op, fmt, a, dy, dx, n, lut ? lut->words : kNoLut,
+                                 (cudaStream_t)stream, li);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return KT_OK;
+}
+
 // ---- host-buffer path -------------------------------------------------------
 // Role streams: [0] host->device copies, [1] kernels, [2] device->host copies,
 // so each copy engine streams chunks back to back.  kBufs buffer pairs
@@ -275,6 +307,41 @@ KT_API kt_status kgelu_f32(const float *x, float *y, size_t n, kt_lut lut, void 
 KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size_t n, kt_lut lut,
                           void *stream) {
   return run_map((int)op, (int)dtype, x, y, n, lut, stream);
+}
+
+KT_API kt_status ktanh_bwd_bf16(const uint16_t *y, const uint16_t *dy, uint16_t *dx, size_t n,
+                                void *stream) {
+  return run_bwd(kt::OP_TANH, kt::FMT_BF16, y, dy, dx, n, nullptr, stream);
+}
+KT_API kt_status ktanh_bwd_f32(const float *y, const float *dy, float *dx, size_t n, void *stream) {
+  return run_bwd(kt::OP_TANH, kt::FMT_F32, y, dy, dx, n, nullptr, stream);
+}
+KT_API kt_status ksigmoid_bwd_bf16(const uint16_t *s, const uint16_t *dy, uint16_t *dx, size_t n,
+                                   void *stream) {
+  return run_bwd(kt::OP_SIGMOID, kt::FMT_BF16, s, dy, dx, n, nullptr, stream);
+}
+KT_API kt_status ksigmoid_bwd_f32(const float *s, const float *dy, float *dx, size_t n, void *stream) {
+  return run_bwd(kt::OP_SIGMOID, kt::FMT_F32, s, dy, dx, n, nullptr, stream);
+}
+KT_API kt_status kswish_bwd_bf16(const uint16_t *x, const uint16_t *dy, uint16_t *dx, size_t n,
+                                 kt_lut lut, void *stream) {
+  return run_bwd(kt::OP_SWISH, kt::FMT_BF16, x, dy, dx, n, lut, stream);
+}
+KT_API kt_status kswish_bwd_f32(const float *x, const float *dy, float *dx, size_t n, kt_lut lut,
+                                void *stream) {
+  return run_bwd(kt::OP_SWISH, kt::FMT_F32, x, dy, dx, n, lut, stream);
+}
+KT_API kt_status kgelu_bwd_bf16(const uint16_t *x, const uint16_t *dy, uint16_t *dx, size_t n,
+                                kt_lut lut, void *stream) {
+  return run_bwd(kt::OP_GELU, kt::FMT_BF16, x, dy, dx, n, lut, stream);
+}
+KT_API kt_status kgelu_bwd_f32(const float *x, const float *dy, float *dx, size_t n, kt_lut lut,
+                               void *stream) {
+  return run_bwd(kt::OP_GELU, kt::FMT_F32, x, dy, dx, n, lut, stream);
+}
+KT_API kt_status kt_apply_bwd(kt_op op, kt_dtype dtype, const void *a, const void *dy, void *dx,
+                              size_t n, kt_lut lut, void *stream) {
+  return run_bwd((int)op, (int)dtype, a, dy, dx, n, lut, stream);
 }
 
 KT_API kt_status klstm_gates_bf16(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,

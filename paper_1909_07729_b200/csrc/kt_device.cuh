@@ -206,6 +206,66 @@ __device__ __forceinline__ uint32_t kgelu_f32(uint32_t u, uint32_t lk, uint32_t 
   return __float_as_uint(__fmaf_rn(hx, t, hx));
 }
 
+// ------------------------------------------------------- backward (NEXT-1) --
+// Reading R-BWD: derivative of the approximated function, taken
+// through the K-TanH value; fp32 with a fixed op order, one rounding to the
+// format.  a = saved output y (tanh, sigmoid) or the input x (swish, gelu).
+//   tanh:    dx = dy * fma(-y, y, 1)
+//   sigmoid: dx = dy * fma(-s, s, s)
+//   swish:   t = K(RN(x/2)),  g = fma(x/4, fma(-t, t, 1), fma(t, 1/2, 1/2))
+//   gelu:    t = K(RN(u)),    g = fma((x/2) fma(-t, t, 1), fma(C3, x^2, C0), fma(t, 1/2, 1/2))
+//            with C0 = RN32(sqrt(2/pi)), C3 = RN32(3 sqrt(2/pi) 0.044715)
+constexpr uint32_t kGeluC3Bits = 0x3DDB33B6u;
+
+__device__ __forceinline__ float2 neg2(float2 v) { return make_float2(-v.x, -v.y); }
+
+template <int OP>
+__device__ __forceinline__ float2 bwd_factor2(float2 av, uint32_t a, uint32_t lw) {
+  if (OP == OP_TANH) return fma2(neg2(av), av, splat2(1.0f));
+  if (OP == OP_SIGMOID) return fma2(neg2(av), av, av);
+  const float2 half = splat2(0.5f);
+  if (OP == OP_SWISH) {
+    const float2 hx = mul2(av, half);
+    const float2 t = widen2(ktanh_bf16x2(pack2(hx), lw));
+    return fma2(mul2(hx, half), fma2(neg2(t), t, splat2(1.0f)), fma2(t, half, half));
+  }
+  // GELU
+  const float2 x2 = mul2(av, av);
+  const float2 p = fma2(splat2(__uint_as_float(kGeluC1Bits)), x2, splat2(__uint_as_float(kGeluC0Bits)));
+  const float2 t = widen2(ktanh_bf16x2(pack2(mul2(av, p)), lw));
+  const float2 up = fma2(splat2(__uint_as_float(kGeluC3Bits)), x2, splat2(__uint_as_float(kGeluC0Bits)));
+  const float2 hx = mul2(av, half);
+  return fma2(mul2(hx, fma2(neg2(t), t, splat2(1.0f))), up, fma2(t, half, half));
+}
+
+template <int OP>
+__device__ __forceinline__ uint32_t bwd_bf16x2(uint32_t a, uint32_t dy, uint32_t lw) {
+  const float2 g = bwd_factor2<OP>(widen2(a), a, lw);
+  return pack2(mul2(widen2(dy), g));
+}
+
+template <int OP>
+__device__ __forceinline__ uint32_t bwd_f32(uint32_t a, uint32_t dy, const uint32_t lk, const uint32_t lc) {
+  const float av = __uint_as_float(a);
+  float g;
+  if (OP == OP_TANH) {
+    g = __fmaf_rn(-av, av, 1.0f);
+  } else if (OP == OP_SIGMOID) {
+    g = __fmaf_rn(-av, av, av);
+  } else if (OP == OP_SWISH) {
+    const float hx = __fmul_rn(av, 0.5f);
+    const float t = __uint_as_float(ktanh_f32(__float_as_uint(hx), lk, lc));
+    g = __fmaf_rn(__fmul_rn(hx, 0.5f), __fmaf_rn(-t, t, 1.0f), __fmaf_rn(t, 0.5f, 0.5f));
+  } else {
+    const float x2 = __fmul_rn(av, av);
+    const float t = __uint_as_float(ktanh_f32(__float_as_uint(gelu_arg(av)), lk, lc));
+    const float up = __fmaf_rn(__uint_as_float(kGeluC3Bits), x2, __uint_as_float(kGeluC0Bits));
+    const float hx = __fmul_rn(av, 0.5f);
+    g = __fmaf_rn(__fmul_rn(hx, __fmaf_rn(-t, t, 1.0f)), up, __fmaf_rn(t, 0.5f, 0.5f));
+  }
+  return __float_as_uint(__fmul_rn(__uint_as_float(dy), g));
+}
+
 // ------------------------------------------------------------- dispatch ----
 
 struct LaneLut {
@@ -233,6 +293,12 @@ template <int OP, int FMT>
 __device__ __forceinline__ uint32_t apply_word(uint32_t w, const LaneLut &L) {
   if (FMT == FMT_BF16) return apply_bf16x2<OP>(w, L);
   return apply_f32<OP>(w, L);
+}
+
+template <int OP, int FMT>
+__device__ __forceinline__ uint32_t apply_bwd_word(uint32_t a, uint32_t dy, const LaneLut &L) {
+  if (FMT == FMT_BF16) return bwd_bf16x2<OP>(a, dy, L.w16);
+  return bwd_f32<OP>(a, dy, L.k32, L.c32);
 }
 
 // LSTM gate pair: K-TanH (is_tanh) or K-Sigmoid, same core, per-lane choice.

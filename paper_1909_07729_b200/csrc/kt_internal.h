@@ -46,6 +46,11 @@ struct LaunchInfo {
 cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const LutWords &lut,
                        cudaStream_t s, const LaunchInfo &li);
 
+// Backward: dx = dy * g(a) (a = saved output for tanh/sigmoid, input x for
+// swish/gelu); reading R-BWD.
+cudaError_t launch_bwd(int op, int fmt, const void *a, const void *dy, void *dx, size_t n,
+                       const LutWords &lut, cudaStream_t s, const LaunchInfo &li);
+
 cudaError_t launch_lstm(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,
                         int tanh_quarter, const LutWords &lut, cudaStream_t s,
                         const LaunchInfo &li);

@@ -126,6 +126,80 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
   }
 }
 
+// ---- backward (NEXT-1): dx = dy * g(a), two input streams -----------------
+template <int OP, int FMT>
+__device__ __forceinline__ void scalar_span_bwd(const uint8_t *ap, const uint8_t *dp, uint8_t *xp,
+                                                uint32_t cnt, const LaneLut &L) {
+  const uint32_t lane = threadIdx.x & 31;
+  const bool on = lane < cnt;
+  uint32_t a = 0, d = 0;
+  if (FMT == FMT_BF16) {
+    if (on) {
+      a = reinterpret_cast<const uint16_t *>(ap)[lane];
+      d = reinterpret_cast<const uint16_t *>(dp)[lane];
+    }
+  } else if (on) {
+    a = reinterpret_cast<const uint32_t *>(ap)[lane];
+    d = reinterpret_cast<const uint32_t *>(dp)[lane];
+  }
+  const uint32_t r = apply_bwd_word<OP, FMT>(a, d, L);
+  if (on) {
+    if (FMT == FMT_BF16) reinterpret_cast<uint16_t *>(xp)[lane] = (uint16_t)r;
+    else reinterpret_cast<uint32_t *>(xp)[lane] = r;
+  }
+}
+
+template <int OP, int FMT, bool NC>
+__global__ void __launch_bounds__(kThreads)
+k_bwd(const uint8_t *a, const uint8_t *dy, uint8_t *dx, uint32_t head, uint64_t nvec, uint32_t tail,
+      const __grid_constant__ LutWords lut) {
+  constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
+  const LaneLut L = load_lane_lut(lut);
+  pdl_enter();
+  const uint32_t lane = threadIdx.x & 31;
+  const size_t hb = (size_t)head * es;
+  const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint64_t base = c * kChunkVecs + lane;
+  uint32_t va[kUnroll][8], vd[kUnroll][8];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t i = base + (uint64_t)u * 32;
+    ld256<NC>(a + hb + i * kVecBytes, va[u], i < nvec);
+    ld256<NC>(dy + hb + i * kVecBytes, vd[u], i < nvec);
+  }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) va[u][j] = apply_bwd_word<OP, FMT>(va[u][j], vd[u][j], L);
+  }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t i = base + (uint64_t)u * 32;
+    st256(dx + hb + i * kVecBytes, va[u], i < nvec);
+  }
+  if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
+    scalar_span_bwd<OP, FMT>(a, dy, dx, head, L);
+    const size_t toff = ((size_t)head + (size_t)nvec * (kVecBytes / es)) * es;
+    scalar_span_bwd<OP, FMT>(a + toff, dy + toff, dx + toff, tail, L);
+  }
+}
+
+template <int OP, int FMT>
+__global__ void __launch_bounds__(kThreads)
+k_bwd_elem(const uint8_t *a, const uint8_t *dy, uint8_t *dx, uint64_t n,
+           const __grid_constant__ LutWords lut) {
+  constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
+  const LaneLut L = load_lane_lut(lut);
+  pdl_enter();
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t c = warp0; c < (n + 31) / 32; c += nwarps) {
+    const uint64_t off = c * 32, rem = n - off;
+    scalar_span_bwd<OP, FMT>(a + off * es, dy + off * es, dx + off * es,
+                             (uint32_t)(rem < 32 ? rem : 32), L);
+  }
+}
+
 // Fallback when x and y have different offsets mod 32 B: one element per
 // lane per step, warp-uniform loop.
 template <int OP, int FMT>
@@ -296,6 +370,49 @@ cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const 
                        cudaStream_t s, const LaunchInfo &li) {
 #define KT_CASE(O, F) \
   if (op == O && fmt == F) return launch_op<O, F>(x, y, n, lut, s, li);
+  KT_CASE(OP_TANH, FMT_BF16)
+  KT_CASE(OP_SIGMOID, FMT_BF16)
+  KT_CASE(OP_SWISH, FMT_BF16)
+  KT_CASE(OP_GELU, FMT_BF16)
+  KT_CASE(OP_TANH, FMT_F32)
+  KT_CASE(OP_SIGMOID, FMT_F32)
+  KT_CASE(OP_SWISH, FMT_F32)
+  KT_CASE(OP_GELU, FMT_F32)
+#undef KT_CASE
+  return cudaErrorInvalidValue;
+}
+
+template <int OP, int FMT>
+static cudaError_t launch_bwd_op(const void *a, const void *dy, void *dx, size_t n,
+                                 const LutWords &lut, cudaStream_t s, const LaunchInfo &li) {
+  constexpr size_t es = (FMT == FMT_BF16) ? 2 : 4;
+  const uintptr_t aa = reinterpret_cast<uintptr_t>(a), da = reinterpret_cast<uintptr_t>(dy),
+                  xa = reinterpret_cast<uintptr_t>(dx);
+  const uint8_t *ap = static_cast<const uint8_t *>(a), *dp = static_cast<const uint8_t *>(dy);
+  uint8_t *xp = static_cast<uint8_t *>(dx);
+  if (aa % kVecBytes != xa % kVecBytes || da % kVecBytes != xa % kVecBytes) {
+    static const int bps = resident_blocks(k_bwd_elem<OP, FMT>);
+    const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
+    return launch(k_bwd_elem<OP, FMT>, grid, s, ap, dp, xp, (uint64_t)n, lut);
+  }
+  const size_t mis = xa % kVecBytes;
+  size_t head = mis ? (kVecBytes - mis) / es : 0;
+  if (head > n) head = n;
+  const size_t body = n - head;
+  const uint64_t nvec = body / (kVecBytes / es);
+  const uint32_t tail = (uint32_t)(body - nvec * (kVecBytes / es));
+  const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+  if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  const unsigned grid = flat_grid(nchunks);
+  if (dx != a && dx != dy)
+    return launch(k_bwd<OP, FMT, true>, grid, s, ap, dp, xp, (uint32_t)head, nvec, tail, lut);
+  return launch(k_bwd<OP, FMT, false>, grid, s, ap, dp, xp, (uint32_t)head, nvec, tail, lut);
+}
+
+cudaError_t launch_bwd(int op, int fmt, const void *a, const void *dy, void *dx, size_t n,
+                       const LutWords &lut, cudaStream_t s, const LaunchInfo &li) {
+#define KT_CASE(O, F) \
+  if (op == O && fmt == F) return launch_bwd_op<O, F>(a, dy, dx, n, lut, s, li);
   KT_CASE(OP_TANH, FMT_BF16)
   KT_CASE(OP_SIGMOID, FMT_BF16)
   KT_CASE(OP_SWISH, FMT_BF16)

@@ -1,0 +1,115 @@
+"""GPU parity of the backward kernels (reading R-BWD) against the oracle.
+
+Tolerance: tanh/sigmoid backward <= 1 ulp of the format (two fp32 roundings
+then one rounding to the format, against the oracle's one rounding of the
+exact value).  Swish/GELU backward additionally allow the fp32 evaluation
+error of the sum (1+t)/2 + ... when it cancels: |dx - oracle| <= 1 ulp +
+2^-20 |dy| S, with S an upper bound on the magnitude of the summed terms.
+NaN compared by class."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads as WL
+from _cmp import _isnan, ulp_dist
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1909_07729_b200 as kt
+    return kt
+
+
+def u16(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def u32(t):
+    return t.contiguous().view(torch.int32).cpu().numpy().view(np.uint32)
+
+
+def _vals(bits, nbits):
+    if nbits == 16:
+        return O.bf16_to_f64(bits)
+    return np.asarray(bits, np.uint32).view(np.float32).astype(np.float64)
+
+
+def check_bwd(op, nbits, a, dy, got, want):
+    d = ulp_dist(got, want, nbits)
+    if op in ("tanh", "sigmoid"):
+        ok = d <= 1
+    else:
+        x = _vals(a, nbits)
+        g = _vals(dy, nbits)
+        S = (1 + np.abs(x) / 4) if op == "swish" else (1 + np.abs(x) * 0.8 * (1 + 0.134 * x * x))
+        with np.errstate(invalid="ignore", over="ignore"):
+            diff = np.abs(_vals(got, nbits) - _vals(want, nbits))
+            ok = (d <= 1) | (diff <= 2.0 ** -20 * np.abs(g) * S)
+    nan = _isnan(got, nbits) & _isnan(want, nbits)
+    bad = ~(ok | nan)
+    assert not bad.any(), (op, nbits, int(bad.sum()), [hex(int(v)) for v in a[bad][:4]],
+                           [hex(int(v)) for v in got[bad][:4]], [hex(int(v)) for v in want[bad][:4]])
+    return int(d[~nan].max()) if (~nan).any() else 0
+
+
+@pytest.mark.parametrize("op", ["tanh", "sigmoid", "swish", "gelu"])
+def test_bwd_bf16_all_patterns(kt, op):
+    a = WL.make_input("c1_exhaustive_bf16", device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(17)
+    dy = torch.randn(65536, device="cuda", generator=g).to(torch.bfloat16)
+    dx = getattr(kt, f"k{op}_bwd_bf16")(a, dy)
+    want = O.bwd_bf16(op, u16(a), u16(dy))
+    worst = check_bwd(op, 16, u16(a), u16(dy), u16(dx), want)
+    print(f"{op} bwd bf16 max ulp {worst}")
+
+
+@pytest.mark.parametrize("op", ["tanh", "sigmoid", "swish", "gelu"])
+def test_bwd_f32_patterns(kt, op):
+    rng = np.random.default_rng(5)
+    a_bits = np.concatenate([
+        (np.arange(1 << 18, dtype=np.uint64) << 14).astype(np.uint32),
+        (rng.standard_normal(1 << 18).astype(np.float32) * 3).view(np.uint32),
+        np.array(WL.special_values_f32(), np.uint32)])
+    dy_bits = (rng.standard_normal(a_bits.size).astype(np.float32)).view(np.uint32)
+    a = torch.from_numpy(a_bits.view(np.int32)).cuda().view(torch.float32)
+    dy = torch.from_numpy(dy_bits.view(np.int32)).cuda().view(torch.float32)
+    dx = getattr(kt, f"k{op}_bwd_f32")(a, dy)
+    want = O.bwd_f32(op, a_bits, dy_bits)
+    check_bwd(op, 32, a_bits, dy_bits, u32(dx), want)
+
+
+@pytest.mark.parametrize("n,off", [(1, 0), (17, 1), (1000, 3), (65537, 0), (100003, 5)])
+def test_bwd_sizes_offsets_inplace(kt, n, off):
+    base = (torch.randn(n + 8, device="cuda") * 2).to(torch.bfloat16)
+    dyb = torch.randn(n + 8, device="cuda").to(torch.bfloat16)
+    a, dy = base[off:off + n], dyb[off:off + n]
+    want = O.bwd_bf16("gelu", u16(a), u16(dy))
+    out = kt.kgelu_bwd_bf16(a, dy)
+    check_bwd("gelu", 16, u16(a), u16(dy), u16(out), want)
+    z = dy.clone()
+    kt.kgelu_bwd_bf16(a, z, out=z)                       # in place over dy
+    check_bwd("gelu", 16, u16(a), u16(dy), u16(z), want)
+
+
+def test_bwd_config5_sampled(kt):
+    """Config 5 size (2^30 BF16) for the GELU backward, sampled outputs."""
+    x = WL.make_input("c5_ffn_2p30", device="cuda")
+    dy = WL.make_input("c5_ffn_2p30", device="cuda", seed=55)
+    dx = kt.kgelu_bwd_bf16(x, dy)
+    idx = torch.from_numpy(np.random.default_rng(9).integers(0, x.numel(), 1 << 16)).cuda()
+    a_s, d_s, g_s = (u16(t.view(-1)[idx]) for t in (x, dy, dx))
+    check_bwd("gelu", 16, a_s, d_s, g_s, O.bwd_bf16("gelu", a_s, d_s))
+    del x, dy, dx
+    torch.cuda.empty_cache()
+
+
+def test_bwd_errors(kt):
+    a = torch.zeros(64, device="cuda", dtype=torch.bfloat16)
+    assert kt._lib.kgelu_bwd_bf16(a.data_ptr(), a.data_ptr(), a.data_ptr(), 64, None, None) == kt.KT_ERR_ARG
+    assert kt._lib.ktanh_bwd_bf16(a.data_ptr(), a.data_ptr() + 2, a.data_ptr() + 2, 32, None) == kt.KT_OK
+    assert kt._lib.ktanh_bwd_bf16(a.data_ptr(), a.data_ptr(), a.data_ptr() + 2, 32, None) == kt.KT_ERR_ARG
