@@ -233,7 +233,10 @@ __device__ __forceinline__ float2 bwd_factor2(float2 av, uint32_t a, uint32_t lw
   const float2 x2 = mul2(av, av);
   const float2 p = fma2(splat2(__uint_as_float(kGeluC1Bits)), x2, splat2(__uint_as_float(kGeluC0Bits)));
   const float2 t = widen2(ktanh_bf16x2(pack2(mul2(av, p)), lw));
-  const float2 up = fma2(splat2(__uint_as_float(kGeluC3Bits)), x2, splat2(__uint_as_float(kGeluC0Bits)));
+  // x^2 clamped to FLT_MAX for u' only: where it overflows, t = +-1 and the
+  // term (x/2)(1 - t^2) u' must be exactly 0 (not 0 * inf)
+  const float2 x2c = make_float2(fminf(x2.x, 3.4028235e38f), fminf(x2.y, 3.4028235e38f));
+  const float2 up = fma2(splat2(__uint_as_float(kGeluC3Bits)), x2c, splat2(__uint_as_float(kGeluC0Bits)));
   const float2 hx = mul2(av, half);
   return fma2(mul2(hx, fma2(neg2(t), t, splat2(1.0f))), up, fma2(t, half, half));
 }
@@ -259,7 +262,8 @@ __device__ __forceinline__ uint32_t bwd_f32(uint32_t a, uint32_t dy, const uint3
   } else {
     const float x2 = __fmul_rn(av, av);
     const float t = __uint_as_float(ktanh_f32(__float_as_uint(gelu_arg(av)), lk, lc));
-    const float up = __fmaf_rn(__uint_as_float(kGeluC3Bits), x2, __uint_as_float(kGeluC0Bits));
+    const float up = __fmaf_rn(__uint_as_float(kGeluC3Bits), fminf(x2, 3.4028235e38f),
+                               __uint_as_float(kGeluC0Bits));
     const float hx = __fmul_rn(av, 0.5f);
     g = __fmaf_rn(__fmul_rn(hx, __fmaf_rn(-t, t, 1.0f)), up, __fmaf_rn(t, 0.5f, 0.5f));
   }
