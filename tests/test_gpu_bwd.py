@@ -124,5 +124,9 @@ def test_bwd_config5_sampled(kt):
 def test_bwd_errors(kt):
     a = torch.zeros(64, device="cuda", dtype=torch.bfloat16)
     assert kt._lib.kgelu_bwd_bf16(a.data_ptr(), a.data_ptr(), a.data_ptr(), 64, None, None) == kt.KT_ERR_ARG
-    assert kt._lib.ktanh_bwd_bf16(a.data_ptr(), a.data_ptr() + 2, a.data_ptr() + 2, 32, None) == kt.KT_OK
-    assert kt._lib.ktanh_bwd_bf16(a.data_ptr(), a.data_ptr(), a.data_ptr() + 2, 32, None) == kt.KT_ERR_ARG
+    b = torch.zeros(64, device="cuda", dtype=torch.bfloat16)
+    assert kt._lib.ktanh_bwd_bf16(a.data_ptr(), b.data_ptr(), b.data_ptr(), 64, None) == kt.KT_OK  # dx == dy
+    assert kt._lib.ktanh_bwd_bf16(a.data_ptr(), b.data_ptr(), a.data_ptr(), 64, None) == kt.KT_OK  # dx == a
+    # dx partially overlapping an input is rejected
+    assert kt._lib.ktanh_bwd_bf16(a.data_ptr(), b.data_ptr(), a.data_ptr() + 2, 32, None) == kt.KT_ERR_ARG
+    torch.cuda.synchronize()
