@@ -133,7 +133,9 @@ class Step:
         n = self.cfg.numel
         self.n = n
         es = self.cfg.elem_bytes
-        self.bytes_per_step = 2 * n * es              # algorithmic: read x + write y
+        self.bwd = "_bwd_" in op
+        # algorithmic bytes: read x (+ dy for a backward) + write y
+        self.bytes_per_step = (3 if self.bwd else 2) * n * es
         if sets is None:
             sets = 1 if self.bytes_per_step >= 2 * L2_BYTES else \
                 max(2, math.ceil(4 * L2_BYTES / self.bytes_per_step))
@@ -142,6 +144,8 @@ class Step:
         self.xs = [x0] + [WL.make_input(self.cfg, device=device, rank=rank, seed=self.cfg.seed + 1000 * s)
                           for s in range(1, sets)]
         self.ys = [torch.empty_like(x0) for _ in range(sets)]
+        self.ds = [WL.make_input(self.cfg, device=device, rank=rank, seed=self.cfg.seed + 77 + 1000 * s)
+                   for s in range(sets)] if self.bwd else None
         self.fn = self._bind()
 
     def _bind(self):
@@ -152,7 +156,10 @@ class Step:
 
     def run(self, i):
         s = i % self.sets
-        self.fn(self.xs[s], self.ys[s])
+        if self.bwd:
+            getattr(self.kt, self.op)(self.xs[s], self.ds[s], out=self.ys[s])
+        else:
+            self.fn(self.xs[s], self.ys[s])
 
 
 def barrier(world):
@@ -311,7 +318,8 @@ KERNEL_NAME = {"ktanh_bf16": "k_map<0, 0, true>", "ktanh_f32": "k_map<0, 1, true
                "lstm": "k_lstm<true>"}
 
 EXTRA = [("c3_f32_2p28", "ktanh_f32"), ("c4_lstm_gates", "lstm"),
-         ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16")]
+         ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16"),
+         ("c5_ffn_2p30", "kgelu_bwd_bf16")]
 
 
 def run_reference(args):

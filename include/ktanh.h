@@ -133,6 +133,20 @@ KT_API kt_status kgelu_f32(const float *x, float *y, size_t n, kt_lut lut, void 
 KT_API kt_status klstm_gates_bf16(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,
                                   int tanh_quarter, kt_lut lut, void *stream);
 
+/* Fused LSTM cell (GNMT LSTM), one pass:
+ *   gates  [rows, 4*hidden] BF16, quarters in PyTorch order i, f, g, o;
+ *   c_prev [rows, hidden] F32 -> c_next [rows, hidden] F32,
+ *   h_next [rows, hidden] BF16:
+ *   i, f, o = K-Sigmoid(gate), g = K-TanH(gate) (BF16, as klstm_gates_bf16)
+ *   c_next  = RN32(f * c_prev + i * g)
+ *   h_next  = RN_bf16(o * K-TanH_f32(c_next))   (reading R-LSTM-CELL)
+ * 18 bytes of HBM traffic per cell element.  c_next may equal c_prev (in
+ * place); any other overlap between outputs and inputs -> KT_ERR_ARG.
+ * hidden % 16 == 0 and 32-B aligned pointers take the vector path. */
+KT_API kt_status klstm_cell_bf16(const uint16_t *gates, const float *c_prev, float *c_next,
+                                 uint16_t *h_next, size_t rows, size_t hidden, kt_lut lut,
+                                 void *stream);
+
 /* Generic dispatcher over (op, dtype); same contract as the calls above. */
 KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size_t n,
                           kt_lut lut, void *stream);

@@ -79,6 +79,9 @@ def lib():
             L.kto_bwd_map_bf16.restype = None
             L.kto_bwd_map_f32.argtypes = [ctypes.c_int, u32p, u32p, u32p, ctypes.c_size_t, ip, ip, ip]
             L.kto_bwd_map_f32.restype = None
+            L.kto_lstm_cell_bf16.argtypes = [u16p, u32p, u32p, u16p, ctypes.c_size_t,
+                                             ctypes.c_size_t, ip, ip, ip]
+            L.kto_lstm_cell_bf16.restype = None
             L.kto_gelu_consts.argtypes = [ctypes.c_int]
             L.kto_gelu_consts.restype = ctypes.c_uint32
             _lib = L
@@ -220,6 +223,23 @@ def lstm_gates_bf16(x_u16: np.ndarray, hidden: int, tanh_quarter: int = 2,
     lib().kto_lstm_gates_bf16(x.ctypes.data_as(u16p), y.ctypes.data_as(u16p), rows, hidden,
                               tanh_quarter, *lut.ptrs())
     return y
+
+
+def lstm_cell_bf16(gates_u16: np.ndarray, c_prev_u32: np.ndarray, hidden: int,
+                   lut: Lut | None = None):
+    """Fused LSTM cell (reading R-LSTM-CELL): returns (c_next bits u32, h_next bits u16)."""
+    lut = _lut(lut)
+    g = np.ascontiguousarray(gates_u16, dtype=np.uint16)
+    c = np.ascontiguousarray(c_prev_u32, dtype=np.uint32)
+    rows = g.size // (4 * hidden)
+    assert g.size == rows * 4 * hidden and c.size == rows * hidden
+    cn = np.empty(rows * hidden, np.uint32)
+    hn = np.empty(rows * hidden, np.uint16)
+    u16p = ctypes.POINTER(ctypes.c_uint16)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    lib().kto_lstm_cell_bf16(g.ctypes.data_as(u16p), c.ctypes.data_as(u32p), cn.ctypes.data_as(u32p),
+                             hn.ctypes.data_as(u16p), rows, hidden, *lut.ptrs())
+    return cn, hn
 
 
 def all_bf16() -> np.ndarray:

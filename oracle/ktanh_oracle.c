@@ -395,6 +395,32 @@ void kto_lstm_gates_bf16(const uint16_t *x, uint16_t *y, size_t rows, size_t hid
     }
 }
 
+/* Fused LSTM cell (GNMT LSTM), reading   */
+/* R-LSTM-CELL: gates [rows, 4H] BF16 in i, f, g, o order; c_prev, c_next  */
+/* [rows, H] F32; h_next [rows, H] BF16.                                   */
+/*   i, f, o = K-Sigmoid_bf16(gate), g = K-TanH_bf16(gate)  (as above)     */
+/*   c'  = RN32(f c + i g)             (exact sum, one rounding)           */
+/*   h'  = RN_bf16(o K-TanH_f32(c'))   (F32 native reading A8, one rounding)*/
+void kto_lstm_cell_bf16(const uint16_t *gates, const uint32_t *c_prev, uint32_t *c_next,
+                        uint16_t *h_next, size_t rows, size_t hidden,
+                        const int *TE, const int *Tr, const int *Tb)
+{
+    for (size_t r = 0; r < rows; ++r) {
+        for (size_t j = 0; j < hidden; ++j) {
+            const uint16_t *gr = gates + r * 4 * hidden;
+            double i = kto_bf16_decode(kto_ksigmoid_bf16(gr[j], TE, Tr, Tb));
+            double f = kto_bf16_decode(kto_ksigmoid_bf16(gr[hidden + j], TE, Tr, Tb));
+            double g = kto_bf16_decode(kto_ktanh_bf16(gr[2 * hidden + j], TE, Tr, Tb));
+            double o = kto_bf16_decode(kto_ksigmoid_bf16(gr[3 * hidden + j], TE, Tr, Tb));
+            double c = (double)f32_from_bits(c_prev[r * hidden + j]);
+            float cn = (float)(f * c + i * g);
+            double t = (double)f32_from_bits(kto_ktanh_f32(bits_from_f32(cn), TE, Tr, Tb));
+            c_next[r * hidden + j] = bits_from_f32(cn);
+            h_next[r * hidden + j] = kto_bf16_encode_rne(o * t);
+        }
+    }
+}
+
 /* ------------------------------------------------------------------ */
 /* Sec. 2.4 bounds, with p = 7 mantissa bits and       */
 /* s = 3 index bits of the mantissa, v = mantissa_idx_val:                 */

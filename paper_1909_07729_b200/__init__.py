@@ -4,8 +4,8 @@ Thin ctypes binding over ``libktanh.so`` (C ABI in ``include/ktanh.h``).
 This module only marshals arguments: every step of the K-TanH path runs in
 the library's CUDA kernels.  PyTorch is used for device memory and streams
 only.  There is no CPU fallback: if the library is missing, importing this
-package raises ImportError (build it with ``python -m
-paper_1909_07729_b200.build`` or ``__graft_entry__.build()``).
+package raises ImportError (build it with ``python
+paper_1909_07729_b200/build.py`` or ``__graft_entry__.build()``).
 
 Names follow the C ABI: ktanh_bf16, ktanh_f32, ksigmoid_bf16, ksigmoid_f32,
 kswish_bf16, kswish_f32, kgelu_bf16, kgelu_f32, klstm_gates_bf16,
@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_PKG, "libktanh.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} not found: the K-TanH CUDA library is not built "
-        "(python -m paper_1909_07729_b200.build). There is no CPU fallback.")
+        "(python paper_1909_07729_b200/build.py). There is no CPU fallback.")
 
 _lib = ctypes.CDLL(LIB_PATH)
 
@@ -39,7 +39,7 @@ MAP_CALLS = ("ktanh_bf16", "ktanh_f32", "ksigmoid_bf16", "ksigmoid_f32",
 BWD_CALLS = ("ktanh_bwd_bf16", "ktanh_bwd_f32", "ksigmoid_bwd_bf16", "ksigmoid_bwd_f32")
 BWD_LUT_CALLS = ("kswish_bwd_bf16", "kswish_bwd_f32", "kgelu_bwd_bf16", "kgelu_bwd_f32")
 EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_create", "kt_lut_create_paper", "kt_lut_get", "kt_lut_destroy",
-                       "klstm_gates_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
+                       "klstm_gates_bf16", "klstm_cell_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
                        "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count")
 
 for _name in MAP_CALLS:
@@ -66,6 +66,8 @@ _lib.kt_lut_destroy.argtypes = [_vp]
 _lib.kt_lut_destroy.restype = None
 _lib.klstm_gates_bf16.argtypes = [_vp, _vp, _sz, _sz, ctypes.c_int, _vp, _vp]
 _lib.klstm_gates_bf16.restype = ctypes.c_int
+_lib.klstm_cell_bf16.argtypes = [_vp, _vp, _vp, _vp, _sz, _sz, _vp, _vp]
+_lib.klstm_cell_bf16.restype = ctypes.c_int
 _lib.kt_apply.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp, _vp]
 _lib.kt_apply.restype = ctypes.c_int
 _lib.kt_apply_host.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp, _vp, _sz, _vp]
@@ -281,6 +283,32 @@ def klstm_gates_bf16(x, hidden: int, tanh_quarter: int = 2, out=None, lut: Lut |
                                      hidden, tanh_quarter, lut.handle, _stream_ptr(stream)),
                "klstm_gates_bf16")
     return out
+
+
+def klstm_cell_bf16(gates, c_prev, hidden: int, c_next=None, h_next=None,
+                    lut: Lut | None = None, stream=None):
+    """Fused LSTM cell: gates [..., 4*hidden] BF16, c_prev [..., hidden] F32 ->
+    (c_next F32, h_next BF16).  c_next may be c_prev (in place)."""
+    import torch
+    if not (gates.is_cuda and c_prev.is_cuda) or gates.dtype != torch.bfloat16 \
+            or c_prev.dtype != torch.float32:
+        raise TypeError("gates: CUDA bfloat16, c_prev: CUDA float32")
+    if not (gates.is_contiguous() and c_prev.is_contiguous()):
+        raise ValueError("inputs must be contiguous")
+    rows = c_prev.numel() // hidden
+    if c_prev.numel() != rows * hidden or gates.numel() != rows * 4 * hidden:
+        raise ValueError("shapes: gates [rows, 4*hidden], c_prev [rows, hidden]")
+    if c_next is None:
+        c_next = torch.empty_like(c_prev)
+    if h_next is None:
+        h_next = torch.empty(c_prev.shape, dtype=torch.bfloat16, device=c_prev.device)
+    lut = lut or paper_lut()
+    idx = gates.device.index
+    with _on_device(idx):
+        _check(_lib.klstm_cell_bf16(gates.data_ptr(), c_prev.data_ptr(), c_next.data_ptr(),
+                                    h_next.data_ptr(), rows, hidden, lut.handle,
+                                    _stream_ptr(stream, idx)), "klstm_cell_bf16")
+    return c_next, h_next
 
 
 def apply(op: str, x, out=None, lut: Lut | None = None, stream=None):

@@ -1,6 +1,8 @@
 """Build libktanh.so (sm_100a) in-tree with nvcc.
 
-    python -m paper_1909_07729_b200.build [--force]
+    python paper_1909_07729_b200/build.py [--force]
+
+(run it as a script: importing the package needs the library it builds)
 
 The library links the CUDA runtime statically, so the .so needs only the
 driver at run time; it never links torch.

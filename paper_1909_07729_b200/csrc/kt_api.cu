@@ -361,6 +361,35 @@ KT_API kt_status klstm_gates_bf16(const uint16_t *x, uint16_t *y, size_t rows, s
   return KT_OK;
 }
 
+KT_API kt_status klstm_cell_bf16(const uint16_t *gates, const float *c_prev, float *c_next,
+                                 uint16_t *h_next, size_t rows, size_t hidden, kt_lut lut,
+                                 void *stream) {
+  if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (hidden == 0) return fail(KT_ERR_ARG, "hidden == 0");
+  if (rows > SIZE_MAX / 4 / hidden) return fail(KT_ERR_ARG, "size overflow");
+  const size_t n = rows * hidden;
+  if (n == 0) return KT_OK;
+  if (!gates || !c_prev || !c_next || !h_next) return fail(KT_ERR_ARG, "NULL pointer");
+  if ((uintptr_t)gates % 2 || (uintptr_t)h_next % 2 || (uintptr_t)c_prev % 4 || (uintptr_t)c_next % 4)
+    return fail(KT_ERR_ARG, "misaligned pointer");
+  if (overlaps(c_next, c_prev, n * 4) || overlaps(h_next, gates, n * 8) ||
+      (const void *)h_next == (const void *)gates ||
+      ((uintptr_t)h_next < (uintptr_t)c_next + n * 4 && (uintptr_t)c_next < (uintptr_t)h_next + n * 2) ||
+      ((uintptr_t)c_next < (uintptr_t)gates + n * 8 && (uintptr_t)gates < (uintptr_t)c_next + n * 4))
+    return fail(KT_ERR_ARG, "outputs overlap inputs (only c_next == c_prev is allowed)");
+  kt::LaunchInfo li;
+  kt_status s = launch_info(&li);
+  if (s != KT_OK) return s;
+  if ((s = check_device_ptr(gates, li.device, "gates")) != KT_OK) return s;
+  if ((s = check_device_ptr(c_prev, li.device, "c_prev")) != KT_OK) return s;
+  if ((s = check_device_ptr(c_next, li.device, "c_next")) != KT_OK) return s;
+  if ((s = check_device_ptr(h_next, li.device, "h_next")) != KT_OK) return s;
+  cudaError_t e = kt::launch_lstm_cell(gates, c_prev, c_next, h_next, rows, hidden, lut->words,
+                                       (cudaStream_t)stream, li);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return KT_OK;
+}
+
 KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, void *y_host, size_t n,
                                kt_lut lut, void *d_work, size_t work_bytes, void *stream) {
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");

@@ -305,6 +305,32 @@ __device__ __forceinline__ uint32_t apply_bwd_word(uint32_t a, uint32_t dy, cons
   return bwd_f32<OP>(a, dy, L.k32, L.c32);
 }
 
+// ------------------------------------------------- fused LSTM cell (NEXT-2) --
+// Reading R-LSTM-CELL: i, f, o = K-Sigmoid, g = K-TanH on the BF16
+// gates; c' = RN32(f c + i g) (i g is exact in fp32, one fma); h' =
+// RN_bf16(o K-TanH_f32(c')) computed exactly: the fp32 product is taken
+// round-toward-zero and made round-to-odd with the fma residual, so the one
+// rounding to BF16 is correct (24 >= 8 + 2 bits).
+__device__ __forceinline__ float mul_rodd(float a, float b) {
+  const float p = __fmul_rz(a, b);
+  const float r = __fmaf_rn(a, b, -p);                  // exact residual
+  const uint32_t pb = __float_as_uint(p);
+  return __uint_as_float(r != 0.0f ? (pb | 1u) : pb);
+}
+
+// 2 cells: gate words gi, gf, gg, go (BF16 pairs), c (2 floats) -> c', h (BF16 pair)
+__device__ __forceinline__ uint32_t lstm_cell2(uint32_t gi, uint32_t gf, uint32_t gg, uint32_t go,
+                                               float2 c, float2 &cn, const LaneLut &L) {
+  const float2 iv = widen2(ksigmoid_bf16x2(gi, L.w16));
+  const float2 fv = widen2(ksigmoid_bf16x2(gf, L.w16));
+  const float2 gv = widen2(ktanh_bf16x2(gg, L.w16));
+  const float2 ov = widen2(ksigmoid_bf16x2(go, L.w16));
+  cn = fma2(fv, c, mul2(iv, gv));
+  const float tl = __uint_as_float(ktanh_f32(__float_as_uint(cn.x), L.k32, L.c32));
+  const float th = __uint_as_float(ktanh_f32(__float_as_uint(cn.y), L.k32, L.c32));
+  return pack_bf16x2(mul_rodd(ov.y, th), mul_rodd(ov.x, tl));
+}
+
 // LSTM gate pair: K-TanH (is_tanh) or K-Sigmoid, same core, per-lane choice.
 __device__ __forceinline__ uint32_t lstm_bf16x2(uint32_t x, uint32_t lw, bool is_tanh) {
   const uint32_t h = is_tanh ? x : pack2(mul2(widen2(x), splat2(0.5f)));

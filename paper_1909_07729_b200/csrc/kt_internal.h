@@ -55,6 +55,11 @@ cudaError_t launch_lstm(const uint16_t *x, uint16_t *y, size_t rows, size_t hidd
                         int tanh_quarter, const LutWords &lut, cudaStream_t s,
                         const LaunchInfo &li);
 
+// Fused LSTM cell (DESIGN.md R-LSTM-CELL).
+cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *c_next,
+                             uint16_t *h_next, size_t rows, size_t hidden, const LutWords &lut,
+                             cudaStream_t s, const LaunchInfo &li);
+
 void count_launch();
 
 }  // namespace kt

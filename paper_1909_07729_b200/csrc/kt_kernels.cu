@@ -256,6 +256,69 @@ k_lstm(const uint8_t *x, uint8_t *y, uint32_t nvec, uint32_t vpr, uint32_t vpq, 
   }
 }
 
+// Fused LSTM cell, vector path: 16 consecutive cells of one row per lane
+// (hidden % 16 == 0, all pointers 32-B aligned).  Per 16 cells: 4 x 32 B of
+// gates + 64 B of c in, 64 B of c' + 32 B of h out (18 B per cell).
+__global__ void __launch_bounds__(kThreads)
+k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_t *h_next,
+            uint32_t nvec, uint32_t vpr, uint32_t hidden, const __grid_constant__ LutWords lut) {
+  const LaneLut L = load_lane_lut(lut);
+  pdl_enter();
+  const uint32_t v = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32 + (threadIdx.x & 31);
+  const bool on = v < nvec;
+  const uint32_t row = on ? v / vpr : 0, j16 = on ? v - row * vpr : 0;
+  const uint8_t *gr = gates + ((size_t)row * 4 * hidden + (size_t)j16 * 16) * 2;
+  const size_t qb = (size_t)hidden * 2;
+  const size_t cidx = (size_t)row * hidden + (size_t)j16 * 16;
+  uint32_t gi[8], gf[8], gg[8], go[8], c0[8], c1[8];
+  ld256<true>(gr, gi, on);
+  ld256<true>(gr + qb, gf, on);
+  ld256<true>(gr + 2 * qb, gg, on);
+  ld256<true>(gr + 3 * qb, go, on);
+  ld256<true>(c_prev + cidx * 4, c0, on);
+  ld256<true>(c_prev + cidx * 4 + 32, c1, on);
+  uint32_t cn0[8], cn1[8], h[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t *cs = k < 4 ? c0 : c1;
+    const int kk = (k & 3) * 2;
+    float2 cn;
+    h[k] = lstm_cell2(gi[k], gf[k], gg[k], go[k],
+                      make_float2(__uint_as_float(cs[kk]), __uint_as_float(cs[kk + 1])), cn, L);
+    uint32_t *cd = k < 4 ? cn0 : cn1;
+    cd[kk] = __float_as_uint(cn.x);
+    cd[kk + 1] = __float_as_uint(cn.y);
+  }
+  st256(c_next + cidx * 4, cn0, on);
+  st256(c_next + cidx * 4 + 32, cn1, on);
+  st256(h_next + cidx * 2, h, on);
+}
+
+// Fused LSTM cell, element fallback.
+__global__ void __launch_bounds__(kThreads)
+k_lstm_cell_elem(const uint16_t *gates, const float *c_prev, float *c_next, uint16_t *h_next,
+                 uint64_t n, uint64_t hidden, const __grid_constant__ LutWords lut) {
+  const LaneLut L = load_lane_lut(lut);
+  pdl_enter();
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t c = warp0; c * 32 < n; c += nwarps) {
+    const uint64_t i = c * 32 + (threadIdx.x & 31);
+    const bool on = i < n;
+    const uint64_t row = on ? i / hidden : 0, j = on ? i - row * hidden : 0;
+    const uint16_t *gr = gates + row * 4 * hidden + j;
+    const uint32_t gi = on ? gr[0] : 0u, gf = on ? gr[hidden] : 0u, gg = on ? gr[2 * hidden] : 0u,
+                   go = on ? gr[3 * hidden] : 0u;
+    const float cp = on ? c_prev[i] : 0.0f;
+    float2 cn;
+    const uint32_t h = lstm_cell2(gi, gf, gg, go, make_float2(cp, 0.0f), cn, L);
+    if (on) {
+      c_next[i] = cn.x;
+      h_next[i] = (uint16_t)h;
+    }
+  }
+}
+
 // LSTM gates, element fallback (any alignment / hidden).
 __global__ void __launch_bounds__(kThreads)
 k_lstm_elem(const uint16_t *__restrict__ x, uint16_t *__restrict__ y, uint64_t n, uint64_t width,
@@ -451,6 +514,28 @@ cudaError_t launch_lstm(const uint16_t *x, uint16_t *y, size_t rows, size_t hidd
   const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
   return launch(k_lstm_elem, grid, s, x, y, (uint64_t)n, (uint64_t)(4 * hidden), (uint64_t)hidden,
                 tanh_quarter, lut);
+}
+
+cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *c_next,
+                             uint16_t *h_next, size_t rows, size_t hidden, const LutWords &lut,
+                             cudaStream_t s, const LaunchInfo &li) {
+  const size_t n = rows * hidden;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(gates) | reinterpret_cast<uintptr_t>(c_prev) |
+                         reinterpret_cast<uintptr_t>(c_next) | reinterpret_cast<uintptr_t>(h_next)) %
+                        kVecBytes) == 0;
+  const uint64_t nvec = n / 16;
+  if (aligned && hidden % 16 == 0 && nvec < (1ull << 31)) {
+    const uint64_t nwarps = (nvec + 31) / 32;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, (nwarps + kWarps - 1) / kWarps);
+    return launch(k_lstm_cell, grid, s, reinterpret_cast<const uint8_t *>(gates),
+                  reinterpret_cast<const uint8_t *>(c_prev), reinterpret_cast<uint8_t *>(c_next),
+                  reinterpret_cast<uint8_t *>(h_next), (uint32_t)nvec, (uint32_t)(hidden / 16),
+                  (uint32_t)hidden, lut);
+  }
+  static const int bps = resident_blocks(k_lstm_cell_elem);
+  const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
+  return launch(k_lstm_cell_elem, grid, s, gates, c_prev, c_next, h_next, (uint64_t)n,
+                (uint64_t)hidden, lut);
 }
 
 }  // namespace kt

@@ -17,8 +17,8 @@ HEADER = os.path.join(ROOT, "include", "ktanh.h")
 
 @pytest.fixture(scope="module")
 def kt():
-    from paper_1909_07729_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__._build_module().build()
     import paper_1909_07729_b200 as kt
     return kt
 

@@ -336,3 +336,33 @@ def test_launch_counter(kt):
     kt.ktanh_bf16(x)
     kt.kgelu_bf16(x)
     assert kt.launch_count() - c0 == 2
+
+
+# ------------------------------------------------------- fused LSTM cell ---
+@pytest.mark.parametrize("rows,hidden", [(128, 1024), (33, 16), (7, 24), (5, 10), (6400, 1024)])
+def test_lstm_cell_fused(kt, rows, hidden):
+    """klstm_cell_bf16 vs the oracle (reading R-LSTM-CELL): c_next and h_next bit-exact."""
+    g = torch.Generator(device="cuda").manual_seed(rows * 31 + hidden)
+    gates = (torch.randn(rows, 4 * hidden, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    c = torch.randn(rows, hidden, device="cuda", generator=g) * 2
+    cn, hn = kt.klstm_cell_bf16(gates, c, hidden)
+    want_c, want_h = O.lstm_cell_bf16(u16(gates), u32(c), hidden)
+    assert_bitexact(u32(cn), want_c, 32, ctx="c_next")
+    assert_bitexact(u16(hn), want_h, 16, nan_by_class=True, ctx="h_next")
+    c2 = c.clone()
+    kt.klstm_cell_bf16(gates, c2, hidden, c_next=c2)              # in place over c
+    assert_bitexact(u32(c2), want_c, 32, ctx="c_next in place")
+
+
+def test_lstm_cell_specials(kt):
+    """Gates over all BF16 patterns (incl. inf/NaN), c over special F32 values."""
+    H = 16
+    x = WL.make_input("c1_exhaustive_bf16", device="cuda").view(-1)       # 65536 = 1024 rows * 4H
+    gates = x.reshape(1024, 4 * H)
+    cvals = np.array(WL.special_values_f32() + [0x3F800000, 0xC0000000], np.uint32)
+    c_bits = np.resize(cvals, 1024 * H).astype(np.uint32)
+    c = torch.from_numpy(c_bits.view(np.int32)).cuda().view(torch.float32).reshape(1024, H)
+    cn, hn = kt.klstm_cell_bf16(gates, c, H)
+    want_c, want_h = O.lstm_cell_bf16(u16(gates), c_bits, H)
+    assert_bitexact(u32(cn), want_c, 32, nan_by_class=True, ctx="c_next specials")
+    assert_bitexact(u16(hn), want_h, 16, nan_by_class=True, ctx="h_next specials")
