@@ -134,8 +134,11 @@ class Step:
         self.n = n
         es = self.cfg.elem_bytes
         self.bwd = "_bwd_" in op
+        self.cell = op == "lstm_cell"
         # algorithmic bytes: read x (+ dy for a backward) + write y
         self.bytes_per_step = (3 if self.bwd else 2) * n * es
+        if self.cell:   # gates 8 B + c 4 B in, c' 4 B + h 2 B out per cell (n/4 cells)
+            self.bytes_per_step = 18 * (n // 4)
         if sets is None:
             sets = 1 if self.bytes_per_step >= 2 * L2_BYTES else \
                 max(2, math.ceil(4 * L2_BYTES / self.bytes_per_step))
@@ -146,6 +149,13 @@ class Step:
         self.ys = [torch.empty_like(x0) for _ in range(sets)]
         self.ds = [WL.make_input(self.cfg, device=device, rank=rank, seed=self.cfg.seed + 77 + 1000 * s)
                    for s in range(sets)] if self.bwd else None
+        if self.cell:
+            H = WL.LSTM_HIDDEN
+            g = torch.Generator(device=device)
+            g.manual_seed(self.cfg.seed + 99 + rank)
+            self.cs = [torch.randn(n // (4 * H), H, generator=g, device=device) for _ in range(sets)]
+            self.cns = [torch.empty_like(c) for c in self.cs]
+            self.hns = [torch.empty(c.shape, dtype=torch.bfloat16, device=device) for c in self.cs]
         self.fn = self._bind()
 
     def _bind(self):
@@ -156,7 +166,10 @@ class Step:
 
     def run(self, i):
         s = i % self.sets
-        if self.bwd:
+        if self.cell:
+            self.kt.klstm_cell_bf16(self.xs[s], self.cs[s], WL.LSTM_HIDDEN, c_next=self.cns[s],
+                                    h_next=self.hns[s])
+        elif self.bwd:
             getattr(self.kt, self.op)(self.xs[s], self.ds[s], out=self.ys[s])
         else:
             self.fn(self.xs[s], self.ys[s])
@@ -319,7 +332,7 @@ KERNEL_NAME = {"ktanh_bf16": "k_map<0, 0, true>", "ktanh_f32": "k_map<0, 1, true
 
 EXTRA = [("c3_f32_2p28", "ktanh_f32"), ("c4_lstm_gates", "lstm"),
          ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16"),
-         ("c5_ffn_2p30", "kgelu_bwd_bf16")]
+         ("c5_ffn_2p30", "kgelu_bwd_bf16"), ("c4_lstm_gates", "lstm_cell")]
 
 
 def run_reference(args):
@@ -412,9 +425,10 @@ def main():
             st = Step(kt, key, op, device, rank)
             wts, _, _ = time_windows(st, K, W, world, device, None, min_total_s=0.3, max_windows=10)
             m_ = statistics.median(wts) / K
+            units = st.n // 4 if st.cell else st.n
             extra[f"{key}:{op}"] = {
-                "elements_per_gpu": st.n, "ms_per_step": round(m_, 5),
-                "gelem_s": round(st.n * world / (m_ / 1e3) / 1e9, 3),
+                "elements_per_gpu": units, "ms_per_step": round(m_, 5),
+                "gelem_s": round(units * world / (m_ / 1e3) / 1e9, 3),
                 "hbm_gbs_per_gpu": round(st.bytes_per_step / (m_ / 1e3) / 1e9, 1),
                 "frac_of_measured": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / peak, 4),
                 "frac_of_8tbs": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / NOMINAL_HBM_GBS, 4),
