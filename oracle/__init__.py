@@ -82,6 +82,13 @@ def lib():
             L.kto_lstm_cell_bf16.argtypes = [u16p, u32p, u32p, u16p, ctypes.c_size_t,
                                              ctypes.c_size_t, ip, ip, ip]
             L.kto_lstm_cell_bf16.restype = None
+            L.kto_build_lut_s.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip, ip,
+                                          ctypes.POINTER(ctypes.c_double)]
+            L.kto_build_lut_s.restype = None
+            L.kto_map_bf16_s.argtypes = [u16p, u16p, ctypes.c_size_t, ctypes.c_int, ip, ip, ip]
+            L.kto_map_bf16_s.restype = None
+            L.kto_bounds_s.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ip, ip]
+            L.kto_bounds_s.restype = None
             L.kto_gelu_consts.argtypes = [ctypes.c_int]
             L.kto_gelu_consts.restype = ctypes.c_uint32
             _lib = L
@@ -89,13 +96,18 @@ def lib():
 
 
 class Lut:
-    """Three 32-entry integer tables (T_E, T_r, T_b), Alg. 1 line 1."""
+    """Three integer tables (T_E, T_r, T_b), Alg. 1 line 1: 32 entries (3 mantissa
+    index bits, Table 1 layout) or 64 entries (4 bits)."""
 
     def __init__(self, E, r, b):
         self.E = np.ascontiguousarray(E, dtype=np.int32)
         self.r = np.ascontiguousarray(r, dtype=np.int32)
         self.b = np.ascontiguousarray(b, dtype=np.int32)
-        assert self.E.shape == self.r.shape == self.b.shape == (32,)
+        assert self.E.shape == self.r.shape == self.b.shape and self.E.shape[0] in (32, 64)
+
+    @property
+    def s_bits(self):
+        return 3 if self.E.shape[0] == 32 else 4
 
     def ptrs(self):
         ip = ctypes.POINTER(ctypes.c_int)
@@ -121,6 +133,23 @@ def build_lut(bmin_zero: bool = False):
     lib().kto_build_lut(int(bmin_zero), E.ctypes.data_as(ip), r.ctypes.data_as(ip),
                         b.ctypes.data_as(ip), sse.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     return Lut(E, r, b), sse
+
+
+def build_lut_s(s_bits: int, bmin_zero: bool = False):
+    """Sec. 2.4 optimizer with s mantissa index bits (s=4: the 64-interval table)."""
+    n = 4 << s_bits
+    E = np.zeros(n, np.int32); r = np.zeros(n, np.int32); b = np.zeros(n, np.int32)
+    sse = np.zeros(n, np.float64)
+    ip = ctypes.POINTER(ctypes.c_int)
+    lib().kto_build_lut_s(s_bits, int(bmin_zero), E.ctypes.data_as(ip), r.ctypes.data_as(ip),
+                          b.ctypes.data_as(ip), sse.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return Lut(E, r, b), sse
+
+
+def bounds_s(r: int, v: int, s_bits: int):
+    lo = ctypes.c_int(); hi = ctypes.c_int()
+    lib().kto_bounds_s(r, v, s_bits, ctypes.byref(lo), ctypes.byref(hi))
+    return lo.value, hi.value
 
 
 def bounds(r: int, v: int):
@@ -159,6 +188,11 @@ def map_bf16(op: str, x_u16: np.ndarray, lut: Lut | None = None) -> np.ndarray:
     x = np.ascontiguousarray(x_u16, dtype=np.uint16)
     y = np.empty_like(x)
     u16p = ctypes.POINTER(ctypes.c_uint16)
+    if lut.s_bits != 3:
+        assert op == "tanh", "64-entry tables: K-TanH only in the oracle"
+        lib().kto_map_bf16_s(x.ctypes.data_as(u16p), y.ctypes.data_as(u16p), x.size, lut.s_bits,
+                             *lut.ptrs())
+        return y
     lib().kto_map_bf16(OPS[op], x.ctypes.data_as(u16p), y.ctypes.data_as(u16p), x.size, *lut.ptrs())
     return y
 

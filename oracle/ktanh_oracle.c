@@ -171,6 +171,34 @@ uint16_t kto_ktanh_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb)
 }
 
 /* ------------------------------------------------------------------ */
+/* 64-interval variant ("Our parameter values are 8-bit only, */
+/* so we can create 64 intervals to achieve more accurate approximation"):  */
+/* s index bits of the mantissa (s = 3: Table 1 layout, 32 entries; s = 4:  */
+/* 64 entries), t = ((E & 3) << s) | (M >> (7 - s)).  Everything else is   */
+/* Algorithm 1 as above.                                                     */
+/* ------------------------------------------------------------------ */
+uint16_t kto_ktanh_bf16_s(uint16_t x, int s_bits, const int *TE, const int *Tr, const int *Tb)
+{
+    int s = (x >> 15) & 1;
+    int E = (x >> 7) & 0xFF;
+    int M = x & 0x7F;
+    double ax = fabs(kto_bf16_decode(x));
+    if (isnan(ax)) return x;
+    if (ax < T1) return x;
+    if (ax > T2) return (uint16_t)((s << 15) | (127 << 7));
+    int t = ((E & 3) << s_bits) | (M >> (7 - s_bits));
+    int Mo = (M >> Tr[t]) + Tb[t];
+    if (Mo < 0 || Mo > 127) g_overflow = 1;
+    return (uint16_t)((s << 15) | ((TE[t] & 0xFF) << 7) | (Mo & 0x7F));
+}
+
+void kto_map_bf16_s(const uint16_t *x, uint16_t *y, size_t n, int s_bits,
+                    const int *TE, const int *Tr, const int *Tb)
+{
+    for (size_t i = 0; i < n; ++i) y[i] = kto_ktanh_bf16_s(x[i], s_bits, TE, Tr, Tb);
+}
+
+/* ------------------------------------------------------------------ */
 /* Algorithm 1 on Float32, native reading A8 ("compatible    */
 /* with multiple such data formats"): same T1/T2 and 5-bit index from    */
 /* (E & 3, top 3 of the 23-bit mantissa); line 8 with p = 23:            */
@@ -434,6 +462,14 @@ void kto_bounds(int r, int v, int *bmin, int *bmax)
     *bmin = -v * (int)floor(ldexp(1.0, p - s - r));
 }
 
+/* Eq. 3 / b_max with s index bits. */
+void kto_bounds_s(int r, int v, int s_bits, int *bmin, int *bmax)
+{
+    const int p = 7;
+    *bmax = (1 << p) - 1 - (int)floor((double)((v + 1) * (1 << (p - s_bits)) - 1) / ldexp(1.0, r));
+    *bmin = -v * (int)floor(ldexp(1.0, p - s_bits - r));
+}
+
 /* ------------------------------------------------------------------ */
 /* Sec. 2.4 optimizer, Steps 1-3, reading R*:           */
 /*  Step 1: y_i = tanh(x_i) in binary64, (E_i, M_i) =   */
@@ -449,18 +485,20 @@ void kto_bounds(int r, int v, int *bmin, int *bmax)
 /*     (A17).  bmin_zero != 0 is the Sec. 3.1 ablation.      */
 /* Returns the per-interval minimum score in sse_out (may be NULL).         */
 /* ------------------------------------------------------------------ */
-void kto_build_lut(int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
+void kto_build_lut_s(int s_bits, int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
 {
     const int q = 7;
-    for (int t = 0; t < 32; ++t) {
+    const int nent = 4 << s_bits, per = 1 << (7 - s_bits);
+    for (int t = 0; t < nent; ++t) {
         /* the positive BF16 inputs of interval t with T1 <= x <= T2 */
         double xs[16], ys[16];
         int ms[16], Ei[16], Mi[16], cnt = 0;
+        (void)per;
         for (int w = 0; w < 0x7F80; ++w) {
             double xv = kto_bf16_decode((uint16_t)w);
             if (xv < T1 || xv > T2) continue;
             int E = (w >> 7) & 0xFF, M = w & 0x7F;
-            if (index_t(E, M >> 4) != t) continue;
+            if ((((E & 3) << s_bits) | (M >> (7 - s_bits))) != t) continue;
             xs[cnt] = xv;
             ms[cnt] = M;
             cnt++;
@@ -476,6 +514,7 @@ void kto_build_lut(int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
         int bestE = -1;
         double bestSSE = INFINITY;
         int Mhat_best[16];
+        if (cnt == 0) { TE[t] = 126; Tr[t] = 0; Tb[t] = 0; if (sse_out) sse_out[t] = 0; continue; }
         for (int c = 0; c < cnt; ++c) {
             int E = Ei[c] < 126 ? Ei[c] : 126;
             double sse = 0.0;
@@ -494,7 +533,7 @@ void kto_build_lut(int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
             }
         }
         /* Step 3 */
-        int v = t & 7;
+        int v = t & ((1 << s_bits) - 1);
         int bestR = -1, bestB = 0;
         long bestScore = -1;
         for (int r = 0; r <= 7; ++r) {
@@ -503,7 +542,7 @@ void kto_build_lut(int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
             bstar /= cnt;
             int b = (int)floor(bstar + 0.5);
             int bmin, bmax;
-            kto_bounds(r, v, &bmin, &bmax);
+            kto_bounds_s(r, v, s_bits, &bmin, &bmax);
             if (bmin_zero) bmin = 0;
             if (b < bmin) b = bmin;
             if (b > bmax) b = bmax;
@@ -523,6 +562,11 @@ void kto_build_lut(int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
         Tb[t] = bestB;
         if (sse_out) sse_out[t] = (double)bestScore;
     }
+}
+
+void kto_build_lut(int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
+{
+    kto_build_lut_s(3, bmin_zero, TE, Tr, Tb, sse_out);
 }
 
 /* End-to-end squared error of one interval of a LUT against binary64 tanh */

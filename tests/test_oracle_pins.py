@@ -404,3 +404,28 @@ def test_lstm_gate_routing():
         sl = slice(q * H, (q + 1) * H)
         want = O.map_bf16("tanh" if q == 2 else "sigmoid", x[:, sl])
         assert np.array_equal(y[:, sl], want)
+
+
+# --------------------------------------------------------------------------
+# 64-interval tables, NEXT-3 evaluation
+# --------------------------------------------------------------------------
+def test_generalised_optimizer_reduces_to_32_entries():
+    assert O.build_lut_s(3)[0].rows() == O.build_lut(False)[0].rows()
+
+
+def test_64_entry_bounds_exhaustive_and_accuracy():
+    """s = 4 index bits: Eq. 3 / b_max keep every reachable M_o in [0, 127]; the
+    64-interval table is no worse than the 32-interval one and within Table 2's
+    bound (the paper: "experimentally, 32 entries suffices")."""
+    for r in range(8):
+        for v in range(16):
+            lo, hi = O.bounds_s(r, v, 4)
+            for b in (lo, hi):
+                for m in range(8 * v, 8 * v + 8):
+                    assert 0 <= (m >> r) + b <= 127
+    L4, _ = O.build_lut_s(4)
+    s4 = O.error_sweep(L4)
+    s3 = O.error_sweep(O.build_lut_s(3)[0])
+    assert not O.overflow_flag()
+    assert s4["max_abs"] <= s3["max_abs"] <= 0.0167
+    assert s4["max_rel"] <= s3["max_rel"]
