@@ -147,6 +147,19 @@ KT_API kt_status klstm_cell_bf16(const uint16_t *gates, const float *c_prev, flo
                                  uint16_t *h_next, size_t rows, size_t hidden, kt_lut lut,
                                  void *stream);
 
+/* GEMM with a K-activation epilogue (fuse K-GELU into the
+ * FFN GEMM).  C[M, N] = act(RN_bf16(A[M, K] . B[N, K]^T))
+ * with A, B, C BF16 row-major (B is [N, K], like nn.Linear's weight), fp32
+ * accumulation (tcgen05 tensor cores, TMEM accumulator, TMA operand loads),
+ * epilogue = -1 (plain BF16 output) or a kt_op applied exactly as the
+ * elementwise k<op>_bf16 applies it to a BF16 tensor: the fused output is
+ * bit-identical to "epilogue -1, then k<op>_bf16".
+ * Requires M % 128 == 0, N % 256 == 0, K % 64 == 0, A and B 16-byte and C
+ * 32-byte aligned, C disjoint from A and B (KT_ERR_ARG otherwise); lut may
+ * be NULL only for epilogue -1. */
+KT_API kt_status kgemm_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M, size_t N,
+                            size_t K, int epilogue, kt_lut lut, void *stream);
+
 /* Generic dispatcher over (op, dtype); same contract as the calls above. */
 KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size_t n,
                           kt_lut lut, void *stream);

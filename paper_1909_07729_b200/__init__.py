@@ -39,7 +39,7 @@ MAP_CALLS = ("ktanh_bf16", "ktanh_f32", "ksigmoid_bf16", "ksigmoid_f32",
 BWD_CALLS = ("ktanh_bwd_bf16", "ktanh_bwd_f32", "ksigmoid_bwd_bf16", "ksigmoid_bwd_f32")
 BWD_LUT_CALLS = ("kswish_bwd_bf16", "kswish_bwd_f32", "kgelu_bwd_bf16", "kgelu_bwd_f32")
 EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_create", "kt_lut_create_paper", "kt_lut_get", "kt_lut_destroy",
-                       "klstm_gates_bf16", "klstm_cell_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
+                       "klstm_gates_bf16", "klstm_cell_bf16", "kgemm_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
                        "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count")
 
 for _name in MAP_CALLS:
@@ -68,6 +68,8 @@ _lib.klstm_gates_bf16.argtypes = [_vp, _vp, _sz, _sz, ctypes.c_int, _vp, _vp]
 _lib.klstm_gates_bf16.restype = ctypes.c_int
 _lib.klstm_cell_bf16.argtypes = [_vp, _vp, _vp, _vp, _sz, _sz, _vp, _vp]
 _lib.klstm_cell_bf16.restype = ctypes.c_int
+_lib.kgemm_bf16.argtypes = [_vp, _vp, _vp, _sz, _sz, _sz, ctypes.c_int, _vp, _vp]
+_lib.kgemm_bf16.restype = ctypes.c_int
 _lib.kt_apply.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp, _vp]
 _lib.kt_apply.restype = ctypes.c_int
 _lib.kt_apply_host.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp, _vp, _sz, _vp]
@@ -309,6 +311,29 @@ def klstm_cell_bf16(gates, c_prev, hidden: int, c_next=None, h_next=None,
                                     h_next.data_ptr(), rows, hidden, lut.handle,
                                     _stream_ptr(stream, idx)), "klstm_cell_bf16")
     return c_next, h_next
+
+
+def kgemm_bf16(A, B, epilogue: str | None = None, out=None, lut: Lut | None = None, stream=None):
+    """C = act(A @ B.T) on tcgen05 tensor cores; A [M, K], B [N, K] BF16 CUDA
+    tensors, act in {None, "tanh", "sigmoid", "swish", "gelu"}."""
+    import torch
+    if not (A.is_cuda and B.is_cuda) or A.dtype != torch.bfloat16 or B.dtype != torch.bfloat16:
+        raise TypeError("A, B must be CUDA bfloat16 tensors")
+    if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[1]:
+        raise ValueError("A [M, K], B [N, K]")
+    if not (A.is_contiguous() and B.is_contiguous()):
+        raise ValueError("A, B must be contiguous")
+    M, K = A.shape
+    N = B.shape[0]
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device=A.device)
+    epi = -1 if epilogue is None else OPS[epilogue]
+    lut = lut or paper_lut()
+    idx = A.device.index
+    with _on_device(idx):
+        _check(_lib.kgemm_bf16(A.data_ptr(), B.data_ptr(), out.data_ptr(), M, N, K, epi, lut.handle,
+                               _stream_ptr(stream, idx)), "kgemm_bf16")
+    return out
 
 
 def apply(op: str, x, out=None, lut: Lut | None = None, stream=None):

@@ -390,6 +390,34 @@ KT_API kt_status klstm_cell_bf16(const uint16_t *gates, const float *c_prev, flo
   return KT_OK;
 }
 
+KT_API kt_status kgemm_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M, size_t N,
+                            size_t K, int epilogue, kt_lut lut, void *stream) {
+  if (epilogue < -1 || epilogue > 3) return fail(KT_ERR_ARG, "epilogue must be -1 or a kt_op");
+  if (epilogue >= 0 && !lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (M == 0 || N == 0) return KT_OK;
+  if (M % 128 || N % 256 || K % 64 || K == 0)
+    return fail(KT_ERR_ARG, "kgemm_bf16 needs M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (K > 0)");
+  if (M > (1u << 31) || N > (1u << 31) || K > (1u << 31)) return fail(KT_ERR_ARG, "size too large");
+  if (!A || !B || !C) return fail(KT_ERR_ARG, "NULL pointer");
+  if ((uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)C % 32)
+    return fail(KT_ERR_ARG, "A, B must be 16-byte and C 32-byte aligned");
+  if (overlaps(C, A, M * N * 2) || (const void *)C == (const void *)A ||
+      ((uintptr_t)C < (uintptr_t)A + M * K * 2 && (uintptr_t)A < (uintptr_t)C + M * N * 2) ||
+      ((uintptr_t)C < (uintptr_t)B + N * K * 2 && (uintptr_t)B < (uintptr_t)C + M * N * 2))
+    return fail(KT_ERR_ARG, "C overlaps A or B");
+  kt::LaunchInfo li;
+  kt_status s = launch_info(&li);
+  if (s != KT_OK) return s;
+  if ((s = check_device_ptr(A, li.device, "A")) != KT_OK) return s;
+  if ((s = check_device_ptr(B, li.device, "B")) != KT_OK) return s;
+  if ((s = check_device_ptr(C, li.device, "C")) != KT_OK) return s;
+  static const kt::LutWords kNoLut = {};
+  cudaError_t e = kt::launch_gemm(epilogue, A, B, C, M, N, K, lut ? lut->words : kNoLut,
+                                  (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kgemm_bf16 launch");
+  return KT_OK;
+}
+
 KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, void *y_host, size_t n,
                                kt_lut lut, void *d_work, size_t work_bytes, void *stream) {
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");

@@ -1,0 +1,275 @@
+// kt_gemm.cu -- tcgen05 GEMM with a K-TanH-family epilogue (SURVEY.md NEXT-2:
+// "a K-GELU epilogue on the FFN GEMM output ... removes a full HBM round
+// trip"; the paper's motivation: activations matter more as
+// GEMMs accelerate).
+//
+//   C[M, N] = act( RN_bf16( A[M, K] . B[N, K]^T ) ),  A, B, C BF16 row-major,
+//   fp32 accumulation in TMEM, act in {none, K-TanH, K-Sigmoid, K-Swish,
+//   K-GELU} applied to the BF16-rounded accumulator exactly as the
+//   elementwise kernels apply it to a BF16 tensor -- so the fused output is
+//   bit-identical to "GEMM with BF16 output, then k<op>_bf16".
+//
+// Structure (one 128 x 256 output tile per CTA, 192 threads):
+//   warp 0      TMEM allocation (whole warp), then lane 0 = TMA producer:
+//               A/B tiles (128 x 64 and 256 x 64 BF16, 128-byte swizzle) into
+//               a 4-stage shared-memory ring, mbarrier expect_tx completion.
+//   warp 1      lane 0 = MMA issuer: tcgen05.mma.cta_group::1.kind::f16,
+//               M=128 N=256 K=16, four per 64-wide K block, accumulating in
+//               256 TMEM columns; tcgen05.commit frees each smem stage and,
+//               after the last K block, signals the epilogue.
+//   warps 2-5   epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes
+//               32*(w%4)..+31 = tile rows), pack to BF16 (RNE), apply the
+//               K-op with the warp-shuffle LUT, 256-bit stores.
+// Every mbarrier wait is bounded (a trap instead of a hang).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "kt_device.cuh"
+#include "kt_internal.h"
+
+namespace kt {
+
+constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
+constexpr int kGemmThreads = 192;
+constexpr uint32_t kABytes = kBM * kBK * 2;          // 16 KiB
+constexpr uint32_t kBBytes = kBN * kBK * 2;          // 32 KiB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;  // 48 KiB
+constexpr uint32_t kTmemCols = 256;
+constexpr size_t kGemmSmem = (size_t)kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t phase) {
+  uint32_t ok = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(phase) : "memory");
+    if (ok) return;
+    if (spin > (1u << 26)) __trap();   // never hang the GPU on a protocol bug
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                            uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms of
+// 1024 B (SBO), descriptor version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;                    // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // SBO = 1024 B
+  d |= (uint64_t)1 << 46;                    // version
+  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: A/B BF16, D F32, K-major both, N = 256, M = 128.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                            ((uint32_t)(kBM >> 4) << 24);
+
+template <int EPI>
+__device__ __forceinline__ uint32_t epi_word(uint32_t w, uint32_t lw) {
+  if (EPI == OP_TANH) return ktanh_bf16x2(w, lw);
+  if (EPI == OP_SIGMOID) return ksigmoid_bf16x2(w, lw);
+  if (EPI == OP_SWISH) return kswish_bf16x2(w, lw);
+  if (EPI == OP_GELU) return kgelu_bf16x2(w, lw);
+  return w;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+k_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+       uint16_t *C, uint32_t N, uint32_t K, const __grid_constant__ LutWords lut) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;                 // SW128 atoms need 1 KiB
+  const uint32_t bar = base + kStages * kStageBytes;            // barriers after the ring
+  const uint32_t full_bar = bar, empty_bar = bar + 8 * kStages, tmem_bar = bar + 16 * kStages;
+  const uint32_t tmem_slot = tmem_bar + 8;
+  uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem_raw + (tmem_slot - raw));
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+  const uint32_t nk = K / kBK;
+  const uint32_t lw = lut.bf16[lane];
+
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, 1);
+    }
+    mbar_init(tmem_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    for (uint32_t kb = 0; kb < nk; ++kb) {
+      const uint32_t s = kb % kStages;
+      if (kb >= (uint32_t)kStages) mbar_wait(empty_bar + 8 * s, ((kb / kStages) + 1) & 1);
+      const uint32_t sa = base + s * kStageBytes, sb = sa + kABytes;
+      mbar_expect_tx(full_bar + 8 * s, kStageBytes);
+      tma_load_2d(sa, &map_a, (int)(kb * kBK), (int)m0, full_bar + 8 * s);
+      tma_load_2d(sb, &map_b, (int)(kb * kBK), (int)n0, full_bar + 8 * s);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    for (uint32_t kb = 0; kb < nk; ++kb) {
+      const uint32_t s = kb % kStages;
+      mbar_wait(full_bar + 8 * s, (kb / kStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t da = umma_sdesc(base + s * kStageBytes);
+      const uint64_t db = umma_sdesc(base + s * kStageBytes + kABytes);
+#pragma unroll
+      for (int k = 0; k < kBK / 16; ++k) {
+        const uint32_t acc = (kb | k) != 0;
+        // +32 B per K=16 step inside the 128-byte swizzle atom
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       empty_bar + 8 * s)
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     tmem_bar)
+                 : "memory");
+  } else if (warp >= 2) {
+    // ---------------- epilogue ----------------
+    mbar_wait(tmem_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t q = warp & 3;                                    // TMEM lane quarter
+    const uint32_t row = m0 + 32 * q + lane;
+    uint16_t *crow = C + (size_t)row * N + n0;
+#pragma unroll 1
+    for (uint32_t c = 0; c < (uint32_t)kBN; c += 32) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((32 * q) << 16) + c;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+            "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+            "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+            "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      uint32_t o[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        o[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);
+      uint32_t o0[8], o1[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o0[j] = o[j];
+        o1[j] = o[8 + j];
+      }
+      st256(crow + c, o0, true);
+      st256(crow + c + 16, o1, true);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------- host ----
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// rows x K BF16 row-major, box (64 K-elements x box_rows rows), 128-byte swizzle
+static bool make_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t K, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {K, rows};
+  cuuint64_t strides[1] = {K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int EPI>
+static cudaError_t launch_gemm_t(const CUtensorMap &ma, const CUtensorMap &mb, uint16_t *C, size_t M,
+                                 size_t N, size_t K, const LutWords &lut, cudaStream_t s) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k_gemm<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kGemmSmem);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  dim3 grid((unsigned)(N / kBN), (unsigned)(M / kBM));
+  k_gemm<EPI><<<grid, kGemmThreads, kGemmSmem, s>>>(ma, mb, C, (uint32_t)N, (uint32_t)K, lut);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(int epi, const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M,
+                        size_t N, size_t K, const LutWords &lut, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, kBM) || !make_map(&mb, B, N, K, kBN)) return cudaErrorInvalidValue;
+  switch (epi) {
+    case -1: return launch_gemm_t<-1>(ma, mb, C, M, N, K, lut, s);
+    case OP_TANH: return launch_gemm_t<OP_TANH>(ma, mb, C, M, N, K, lut, s);
+    case OP_SIGMOID: return launch_gemm_t<OP_SIGMOID>(ma, mb, C, M, N, K, lut, s);
+    case OP_SWISH: return launch_gemm_t<OP_SWISH>(ma, mb, C, M, N, K, lut, s);
+    case OP_GELU: return launch_gemm_t<OP_GELU>(ma, mb, C, M, N, K, lut, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace kt

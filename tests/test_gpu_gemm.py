@@ -1,0 +1,65 @@
+"""tcgen05 GEMM + K-activation epilogue (NEXT-2): numerics vs a float64 matmul
+(the definition of the contraction) and bitwise equality of the fused epilogue
+with the elementwise K-op applied to the plain GEMM output."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from _cmp import assert_bitexact, ulp_dist
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1909_07729_b200 as kt
+    return kt
+
+
+def u16(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def rand_bf16(shape, seed, scale=1.0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(shape, device="cuda", generator=g) * scale).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (128, 256, 128), (256, 512, 256),
+                                   (384, 768, 1024)])
+def test_gemm_vs_float64(kt, M, N, K):
+    A, B = rand_bf16((M, K), 1, 0.5), rand_bf16((N, K), 2, 0.5)
+    C = kt.kgemm_bf16(A, B)
+    torch.cuda.synchronize()
+    a = O.bf16_to_f64(u16(A)).reshape(M, K)
+    b = O.bf16_to_f64(u16(B)).reshape(N, K)
+    exact = a @ b.T                                        # float64 reference
+    got = O.bf16_to_f64(u16(C)).reshape(M, N)
+    # one BF16 rounding of the fp32 accumulator + fp32 accumulation error
+    bound = np.abs(exact) * 2.0 ** -8 + K * 2.0 ** -23 * (np.abs(a) @ np.abs(b).T) + 1e-30
+    err = np.abs(got - exact)
+    assert np.all(err <= bound), (float(err.max()), float((err / bound).max()))
+
+
+@pytest.mark.parametrize("epi", ["tanh", "sigmoid", "swish", "gelu"])
+def test_gemm_epilogue_bitwise(kt, epi):
+    M, N, K = 256, 512, 512
+    A, B = rand_bf16((M, K), 3, 0.3), rand_bf16((N, K), 4, 0.3)
+    plain = kt.kgemm_bf16(A, B)
+    fused = kt.kgemm_bf16(A, B, epilogue=epi)
+    ref = getattr(kt, f"k{epi}_bf16")(plain)
+    torch.cuda.synchronize()
+    assert_bitexact(u16(fused), u16(ref), 16, nan_by_class=True, ctx=f"gemm+{epi}")
+    # and the epilogue itself is the oracle's K-op on the BF16 GEMM output
+    want = O.map_bf16(epi, u16(plain))
+    assert_bitexact(u16(fused), want, 16, nan_by_class=True, ctx=f"gemm+{epi} vs oracle")
+
+
+def test_gemm_bad_shapes(kt):
+    A = rand_bf16((100, 64), 5)
+    B = rand_bf16((256, 64), 6)
+    with pytest.raises(kt.KTanhError):
+        kt.kgemm_bf16(A, B)
