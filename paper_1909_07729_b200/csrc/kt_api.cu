@@ -401,8 +401,7 @@ KT_API kt_status kgemm_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, s
   if (!A || !B || !C) return fail(KT_ERR_ARG, "NULL pointer");
   if ((uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)C % 32)
     return fail(KT_ERR_ARG, "A, B must be 16-byte and C 32-byte aligned");
-  if (overlaps(C, A, M * N * 2) || (const void *)C == (const void *)A ||
-      ((uintptr_t)C < (uintptr_t)A + M * K * 2 && (uintptr_t)A < (uintptr_t)C + M * N * 2) ||
+  if (((uintptr_t)C < (uintptr_t)A + M * K * 2 && (uintptr_t)A < (uintptr_t)C + M * N * 2) ||
       ((uintptr_t)C < (uintptr_t)B + N * K * 2 && (uintptr_t)B < (uintptr_t)C + M * N * 2))
     return fail(KT_ERR_ARG, "C overlaps A or B");
   kt::LaunchInfo li;
