@@ -412,7 +412,7 @@ KT_API kt_status kgemm_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, s
   if ((s = check_device_ptr(C, li.device, "C")) != KT_OK) return s;
   static const kt::LutWords kNoLut = {};
   cudaError_t e = kt::launch_gemm(epilogue, A, B, C, M, N, K, lut ? lut->words : kNoLut,
-                                  (cudaStream_t)stream);
+                                  (cudaStream_t)stream, li.sm_count);
   if (e != cudaSuccess) return cuda_fail(e, "kgemm_bf16 launch");
   return KT_OK;
 }

@@ -34,12 +34,12 @@
 namespace kt {
 
 constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
-constexpr int kGemmThreads = 192;
 constexpr uint32_t kABytes = kBM * kBK * 2;          // 16 KiB
 constexpr uint32_t kBBytes = kBN * kBK * 2;          // 32 KiB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;  // 48 KiB
 constexpr uint32_t kTmemCols = 256;
 constexpr size_t kGemmSmem = (size_t)kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+static_assert(8 * 4 * 4 + 64 <= 256, "barrier area");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -97,20 +97,41 @@ __device__ __forceinline__ uint32_t epi_word(uint32_t w, uint32_t lw) {
   return w;
 }
 
+// Persistent variant: grid = min(tiles, SMs); each CTA walks tiles
+// blockIdx.x, += gridDim.x (n fastest within a group of kGroupM row blocks, so
+// concurrently running CTAs share B panels in L2).  Two TMEM accumulator
+// stages (2 x 256 columns = all 512): the epilogue of tile i (8 warps: lane
+// quarter = warp % 4, column half = (warp - 2) / 4) overlaps the mainloop of
+// tile i + 1.  Barriers: smem ring full/empty (continuous across tiles),
+// tmem_full[2] (MMA -> epilogue), tmem_empty[2] (epilogue -> MMA, 8 arrivals).
+constexpr int kEpiWarps = 8;
+constexpr int kGemmPThreads = 64 + 32 * kEpiWarps;
+constexpr int kGroupM = 16;
+
+__device__ __forceinline__ void tile_coords(uint32_t t, uint32_t mt, uint32_t ntiles_n, uint32_t &mb,
+                                            uint32_t &nb) {
+  const uint32_t per_group = kGroupM * ntiles_n;
+  const uint32_t g = t / per_group, r = t - g * per_group;
+  const uint32_t rows = min((uint32_t)kGroupM, mt - g * kGroupM);
+  mb = g * kGroupM + r % rows;
+  nb = r / rows;
+}
+
 template <int EPI>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kGemmPThreads, 1)
 k_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-       uint16_t *C, uint32_t N, uint32_t K, const __grid_constant__ LutWords lut) {
+       uint16_t *C, uint32_t M, uint32_t N, uint32_t K, const __grid_constant__ LutWords lut) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;                 // SW128 atoms need 1 KiB
-  const uint32_t bar = base + kStages * kStageBytes;            // barriers after the ring
-  const uint32_t full_bar = bar, empty_bar = bar + 8 * kStages, tmem_bar = bar + 16 * kStages;
-  const uint32_t tmem_slot = tmem_bar + 8;
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bar = base + kStages * kStageBytes;
+  const uint32_t full_bar = bar, empty_bar = bar + 8 * kStages;
+  const uint32_t tfull_bar = bar + 16 * kStages, tempty_bar = tfull_bar + 16;
+  const uint32_t tmem_slot = tempty_bar + 16;
   uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem_raw + (tmem_slot - raw));
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+  const uint32_t mt = M / kBM, ntn = N / kBN, ntiles = mt * ntn;
   const uint32_t nk = K / kBK;
   const uint32_t lw = lut.bf16[lane];
 
@@ -119,12 +140,15 @@ k_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtens
       mbar_init(full_bar + 8 * s, 1);
       mbar_init(empty_bar + 8 * s, 1);
     }
-    mbar_init(tmem_bar, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar + 8 * a, 1);
+      mbar_init(tempty_bar + 8 * a, kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
-                 "n"(kTmemCols));
+                 "n"(2 * kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -134,78 +158,101 @@ k_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtens
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
-    for (uint32_t kb = 0; kb < nk; ++kb) {
-      const uint32_t s = kb % kStages;
-      if (kb >= (uint32_t)kStages) mbar_wait(empty_bar + 8 * s, ((kb / kStages) + 1) & 1);
-      const uint32_t sa = base + s * kStageBytes, sb = sa + kABytes;
-      mbar_expect_tx(full_bar + 8 * s, kStageBytes);
-      tma_load_2d(sa, &map_a, (int)(kb * kBK), (int)m0, full_bar + 8 * s);
-      tma_load_2d(sb, &map_b, (int)(kb * kBK), (int)n0, full_bar + 8 * s);
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      uint32_t mb, nb;
+      tile_coords(t, mt, ntn, mb, nb);
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % kStages;
+        if (it >= (uint32_t)kStages) mbar_wait(empty_bar + 8 * s, ((it / kStages) + 1) & 1);
+        const uint32_t sa = base + s * kStageBytes, sb = sa + kABytes;
+        mbar_expect_tx(full_bar + 8 * s, kStageBytes);
+        tma_load_2d(sa, &map_a, (int)(kb * kBK), (int)(mb * kBM), full_bar + 8 * s);
+        tma_load_2d(sb, &map_b, (int)(kb * kBK), (int)(nb * kBN), full_bar + 8 * s);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    for (uint32_t kb = 0; kb < nk; ++kb) {
-      const uint32_t s = kb % kStages;
-      mbar_wait(full_bar + 8 * s, (kb / kStages) & 1);
+    uint32_t it = 0, i = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const uint32_t a = i & 1;
+      if (i >= 2) mbar_wait(tempty_bar + 8 * a, ((i / 2) + 1) & 1);   // epilogue drained stage a
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t da = umma_sdesc(base + s * kStageBytes);
-      const uint64_t db = umma_sdesc(base + s * kStageBytes + kABytes);
+      const uint32_t d = tmem + a * kTmemCols;
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % kStages;
+        mbar_wait(full_bar + 8 * s, (it / kStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = umma_sdesc(base + s * kStageBytes);
+        const uint64_t db = umma_sdesc(base + s * kStageBytes + kABytes);
 #pragma unroll
-      for (int k = 0; k < kBK / 16; ++k) {
-        const uint32_t acc = (kb | k) != 0;
-        // +32 B per K=16 step inside the 128-byte swizzle atom
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-            "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc), "r"(acc));
+        for (int k = 0; k < kBK / 16; ++k) {
+          const uint32_t acc = (kb | k) != 0;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         empty_bar + 8 * s)
+                     : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       empty_bar + 8 * s)
+                       tfull_bar + 8 * a)
                    : "memory");
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     tmem_bar)
-                 : "memory");
   } else if (warp >= 2) {
-    // ---------------- epilogue ----------------
-    mbar_wait(tmem_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t q = warp & 3;                                    // TMEM lane quarter
-    const uint32_t row = m0 + 32 * q + lane;
-    uint16_t *crow = C + (size_t)row * N + n0;
+    // ---------------- epilogue (8 warps) ----------------
+    const uint32_t q = warp & 3, half = (warp - 2) >> 2;
+    uint32_t i = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      uint32_t mb, nb;
+      tile_coords(t, mt, ntn, mb, nb);
+      const uint32_t a = i & 1;
+      mbar_wait(tfull_bar + 8 * a, (i / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t row = mb * kBM + 32 * q + lane;
+      uint16_t *crow = C + (size_t)row * N + nb * kBN + half * 128;
 #pragma unroll 1
-    for (uint32_t c = 0; c < (uint32_t)kBN; c += 32) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem + ((32 * q) << 16) + c;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-            "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-            "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-            "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      uint32_t o[16];
+      for (uint32_t c = 0; c < 128; c += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((32 * q) << 16) + a * kTmemCols + half * 128 + c;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+              "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == 96) {
+          // all of this warp's TMEM reads for tile i are done: release stage a
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar + 8 * a) : "memory");
+        }
+        uint32_t o0[8], o1[8];
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        o[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);
-      uint32_t o0[8], o1[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        o0[j] = o[j];
-        o1[j] = o[8 + j];
+        for (int j = 0; j < 8; ++j) {
+          o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);
+          o1[j] = epi_word<EPI>(
+              pack_bf16x2(__uint_as_float(r[2 * j + 17]), __uint_as_float(r[2 * j + 16])), lw);
+        }
+        st256(crow + c, o0, true);
+        st256(crow + c + 16, o1, true);
       }
-      st256(crow + c, o0, true);
-      st256(crow + c + 16, o1, true);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(2 * kTmemCols));
   }
 }
 
@@ -244,7 +291,7 @@ static bool make_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t K,
 
 template <int EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap &ma, const CUtensorMap &mb, uint16_t *C, size_t M,
-                                 size_t N, size_t K, const LutWords &lut, cudaStream_t s) {
+                                 size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -252,22 +299,24 @@ static cudaError_t launch_gemm_t(const CUtensorMap &ma, const CUtensorMap &mb, u
                                     (int)kGemmSmem);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  dim3 grid((unsigned)(N / kBN), (unsigned)(M / kBM));
-  k_gemm<EPI><<<grid, kGemmThreads, kGemmSmem, s>>>(ma, mb, C, (uint32_t)N, (uint32_t)K, lut);
+  const size_t tiles = (M / kBM) * (N / kBN);
+  const unsigned grid = (unsigned)(tiles < (size_t)sms ? tiles : (size_t)sms);
+  k_gemm<EPI><<<grid, kGemmPThreads, kGemmSmem, s>>>(ma, mb, C, (uint32_t)M, (uint32_t)N,
+                                                     (uint32_t)K, lut);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(int epi, const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M,
-                        size_t N, size_t K, const LutWords &lut, cudaStream_t s) {
+                        size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms) {
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, M, K, kBM) || !make_map(&mb, B, N, K, kBN)) return cudaErrorInvalidValue;
   switch (epi) {
-    case -1: return launch_gemm_t<-1>(ma, mb, C, M, N, K, lut, s);
-    case OP_TANH: return launch_gemm_t<OP_TANH>(ma, mb, C, M, N, K, lut, s);
-    case OP_SIGMOID: return launch_gemm_t<OP_SIGMOID>(ma, mb, C, M, N, K, lut, s);
-    case OP_SWISH: return launch_gemm_t<OP_SWISH>(ma, mb, C, M, N, K, lut, s);
-    case OP_GELU: return launch_gemm_t<OP_GELU>(ma, mb, C, M, N, K, lut, s);
+    case -1: return launch_gemm_t<-1>(ma, mb, C, M, N, K, lut, s, sms);
+    case OP_TANH: return launch_gemm_t<OP_TANH>(ma, mb, C, M, N, K, lut, s, sms);
+    case OP_SIGMOID: return launch_gemm_t<OP_SIGMOID>(ma, mb, C, M, N, K, lut, s, sms);
+    case OP_SWISH: return launch_gemm_t<OP_SWISH>(ma, mb, C, M, N, K, lut, s, sms);
+    case OP_GELU: return launch_gemm_t<OP_GELU>(ma, mb, C, M, N, K, lut, s, sms);
   }
   return cudaErrorInvalidValue;
 }
