@@ -436,6 +436,40 @@ def main():
             del st
             torch.cuda.empty_cache()
 
+    if not args.no_extra:
+        # NEXT-2: the FFN up-projection that produces config 5's [65536, 16384]
+        # activations, K-GELU fused into the tcgen05 GEMM epilogue (K = 4096)
+        Mg, Ng, Kg = WL.CONFIGS["c5_ffn_2p30"].shape[0], WL.CONFIGS["c5_ffn_2p30"].shape[1], 4096
+        gA = WL.make_input("c5_ffn_2p30", device=device, rank=rank, numel=Mg * Kg).reshape(Mg, Kg)
+        gB = (WL.make_input("c5_ffn_2p30", device=device, rank=rank, numel=Ng * Kg, seed=7)
+              .reshape(Ng, Kg) * 0.02).to(torch.bfloat16)
+        gC = torch.empty(Mg, Ng, dtype=torch.bfloat16, device=device)
+
+        class _G:
+            n, bytes_per_step, sets = Mg * Ng, 0, 1
+            kt_ = kt
+
+            def run(self, i):
+                kt.kgemm_bf16(gA, gB, epilogue="gelu", out=gC)
+        gst = _G()
+        gst.kt = kt
+        wts, _, _ = time_windows(gst, K, W, world, device, None, min_total_s=0.3, max_windows=5)
+        m_ = statistics.median(wts) / K
+        tf = 2.0 * Mg * Ng * Kg / (m_ / 1e3) / 1e12
+        bf16_peak = 1674.5
+        try:
+            bf16_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        except Exception:
+            pass
+        extra["ffn_gemm_M65536_N16384_K4096:kgemm_bf16+kgelu"] = {
+            "ms_per_step": round(m_, 4), "tflops_per_gpu": round(tf, 1),
+            "roofline": {"bound": "tensor", "peak": bf16_peak, "unit": "TFLOP/s",
+                         "frac": round(tf / bf16_peak, 4),
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (cuBLAS burst)"},
+            "note": "tcgen05 GEMM, fp32 TMEM accumulation, K-GELU applied in the epilogue"}
+        del gA, gB, gC
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(WL.CONFIGS[head_key], "tanh", device)
