@@ -389,15 +389,22 @@ def main():
     rank, local_rank, world = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU path)")
-    torch.cuda.set_device(local_rank)
-    device = torch.device("cuda", local_rank)
+    ndev = torch.cuda.device_count()
+    dev_index = local_rank % ndev           # one GPU per rank on a full node
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
     if world > 1:
-        _kd().init("nccl", device)
+        # gloo: the only collectives are timing scalars (barrier, max, sum);
+        # the data path has none (north_star item (c))
+        _kd().init("gloo")
+        if world > ndev and rank == 0:
+            print(f"warning: {world} ranks on {ndev} GPU(s): functional run, not a measurement",
+                  file=sys.stderr)
 
     import paper_1909_07729_b200 as kt
 
     peak, peak_src = measured_peaks()
-    clocks = ClockSampler(local_rank) if rank == 0 or world > 1 else None
+    clocks = ClockSampler(dev_index) if rank == 0 or world > 1 else None
     if clocks:
         clocks.start()
         time.sleep(0.3)
