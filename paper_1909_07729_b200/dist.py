@@ -49,9 +49,10 @@ def shard_view(t: torch.Tensor, world: int, rank: int, align: int = 16) -> torch
 def _reduce_scalar(v: float, op, device=None) -> float:
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(v)
-    if device is None or dist.get_backend() != "nccl":
-        device = torch.device("cuda", torch.cuda.current_device()) \
-            if dist.get_backend() == "nccl" else torch.device("cpu")
+    if dist.get_backend() != "nccl":
+        device = torch.device("cpu")            # gloo reduces host tensors
+    elif device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
     t = torch.tensor([float(v)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=op)
     return float(t.item())

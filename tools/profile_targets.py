@@ -19,11 +19,36 @@ TARGETS = {
     "swish": ("c5_ffn_2p30", lambda x, y: kt.kswish_bf16(x, out=y)),
     "sigmoid": ("c2_bf16_2p24", lambda x, y: kt.ksigmoid_bf16(x, out=y)),
     "lstm": ("c4_lstm_gates", lambda x, y: kt.klstm_gates_bf16(x, WL.LSTM_HIDDEN, 2, out=y)),
+    "gelu_bwd": ("c5_ffn_2p30", lambda x, y: kt.kgelu_bwd_bf16(x, x, out=y)),
 }
 
+
+def gemm_gelu():
+    M, N, K = 65536, 16384, 4096
+    A = WL.make_input("c5_ffn_2p30", device="cuda", numel=M * K).reshape(M, K)
+    B = (WL.make_input("c5_ffn_2p30", device="cuda", numel=N * K, seed=7).reshape(N, K) * 0.02
+         ).to(torch.bfloat16)
+    C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    for _ in range(4):
+        kt.kgemm_bf16(A, B, epilogue="gelu", out=C)
+    torch.cuda.synchronize()
+    print("gemm_gelu ok", flush=True)
+
+
+def lstm_cell():
+    x = WL.make_input("c4_lstm_gates", device="cuda")
+    c = torch.randn(x.numel() // (4 * WL.LSTM_HIDDEN), WL.LSTM_HIDDEN, device="cuda")
+    for _ in range(4):
+        kt.klstm_cell_bf16(x, c, WL.LSTM_HIDDEN)
+    torch.cuda.synchronize()
+    print("lstm_cell ok", flush=True)
+
 if __name__ == "__main__":
-    names = sys.argv[1:] or list(TARGETS)
+    names = sys.argv[1:] or list(TARGETS) + ["gemm_gelu", "lstm_cell"]
     for name in names:
+        if name in ("gemm_gelu", "lstm_cell"):
+            globals()[name]()
+            continue
         key, fn = TARGETS[name]
         x = WL.make_input(key, device="cuda")
         y = torch.empty_like(x)
