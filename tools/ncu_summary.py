@@ -28,6 +28,8 @@ KEYS = {
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
     "sm__cycles_elapsed.avg.per_second": "sm_clock",
     "dram__cycles_elapsed.avg.per_second": "dram_clock",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed":
+        "tensor_pipe_pct",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6,
         "ms": 1e-3, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "Hz": 1, "Khz": 1e3,
@@ -72,7 +74,7 @@ def summarise(rep):
 def attach_algorithmic(allk, alg_bytes):
     for tag, ks in allk.items():
         for d in ks:
-            if tag in alg_bytes and "duration" in d:
+            if alg_bytes.get(tag) and "duration" in d:
                 d["algorithmic_bytes_per_launch"] = alg_bytes[tag]
                 d["algorithmic_gbs"] = alg_bytes[tag] / d["duration"] / 1e9
 
@@ -89,8 +91,14 @@ if __name__ == "__main__":
             alg[tag] = 4 << 24
         elif "tanh_f32" in tag:
             alg[tag] = 8 << 28
+        elif "gemm" in tag:
+            alg[tag] = 0
         elif "gelu" in tag or "swish" in tag:
             alg[tag] = 4 << 30
+        elif "lstm_cell" in tag:
+            alg[tag] = 18 * 128 * 50 * 1024
+        elif "gelu_bwd" in tag:
+            alg[tag] = 6 << 30
         elif "lstm" in tag:
             alg[tag] = 4 * 128 * 50 * 4096
     attach_algorithmic(allk, alg)
@@ -100,7 +108,7 @@ if __name__ == "__main__":
     for tag, ks in allk.items():
         for d in ks:
             print(f"{tag}: {d['kernel'][:60]}")
-            for k in ("duration", "dram_read", "dram_write", "dram_gbs", "algorithmic_gbs", "dram_pct_peak", "alu_pipe_pct",
+            for k in ("duration", "dram_read", "dram_write", "dram_gbs", "algorithmic_gbs", "tensor_pipe_pct", "dram_pct_peak", "alu_pipe_pct",
                       "fma_pipe_pct", "issue_active_pct", "warps_active_pct", "regs", "grid", "sm_clock"):
                 if k in d:
                     print(f"   {k:18s} {d[k]:.4g}")
