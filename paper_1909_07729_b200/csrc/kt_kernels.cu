@@ -88,7 +88,7 @@ __device__ __forceinline__ void scalar_span(const uint8_t *xp, uint8_t *yp, uint
 template <int OP, int FMT, bool NC, bool PF>
 __global__ void __launch_bounds__(kThreads)
 k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
-      uint32_t pf_blocks, const __grid_constant__ LutWords lut) {
+      uint32_t pf_blocks, uint32_t pf_depth, const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
   const LaneLut L = load_lane_lut(lut);
   const uint32_t lane = threadIdx.x & 31;
@@ -96,10 +96,14 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
   uint8_t *yb = y + (size_t)head * es;
   const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);   // this warp's chunk
   // only the first resident wave can be waiting behind a predecessor's tail
-  if (PF && blockIdx.x < pf_blocks && lane == 0 && c * kChunkVecs < nvec) {
-    const uint64_t left = nvec - c * kChunkVecs;
-    prefetch_l2(xb + c * kChunkVecs * kVecBytes,
-                (uint32_t)((left < kChunkVecs ? left : kChunkVecs) * kVecBytes));
+  if (PF && blockIdx.x < pf_blocks && lane < pf_depth) {
+    // lane d prefetches the chunk of the warp d resident waves later
+    const uint64_t cc = c + (uint64_t)lane * pf_blocks * kWarps;
+    if (cc * kChunkVecs < nvec) {
+      const uint64_t left = nvec - cc * kChunkVecs;
+      prefetch_l2(xb + cc * kChunkVecs * kVecBytes,
+                  (uint32_t)((left < kChunkVecs ? left : kChunkVecs) * kVecBytes));
+    }
   }
   pdl_enter();
   const uint64_t base = c * kChunkVecs + lane;
@@ -359,6 +363,16 @@ static bool prefetch_enabled() {
   return on && pdl_enabled();
 }
 
+// Chunks prefetched per first-wave warp (KT_PF_DEPTH, default 1).
+static uint32_t prefetch_depth() {
+  static const uint32_t d = [] {
+    const char *e = getenv("KT_PF_DEPTH");
+    const int v = e ? atoi(e) : 1;
+    return (uint32_t)(v < 1 ? 1 : v > 8 ? 8 : v);
+  }();
+  return d;
+}
+
 template <typename... KArgs, typename... Args>
 static cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -422,11 +436,13 @@ static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &l
       static const int bps = resident_blocks(k_map<OP, FMT, true, true>);
       const uint32_t pf_blocks = (uint32_t)(li.sm_count * bps);
       return launch(k_map<OP, FMT, true, true>, grid, s, xp, yp, (uint32_t)head, nvec, tail,
-                    pf_blocks, lut);
+                    pf_blocks, prefetch_depth(), lut);
     }
-    return launch(k_map<OP, FMT, true, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, lut);
+    return launch(k_map<OP, FMT, true, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
+                  lut);
   }
-  return launch(k_map<OP, FMT, false, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, lut);
+  return launch(k_map<OP, FMT, false, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
+                lut);
 }
 
 cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const LutWords &lut,
