@@ -1,0 +1,68 @@
+"""Out-of-bounds write checks (compute-sanitizer is closed on this pool):
+every output buffer is embedded in a sentinel-filled guard band, which must
+be untouched after the call, for ragged sizes / offsets on every kernel."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+G = 64                          # guard elements on each side
+
+
+@pytest.fixture(scope="module")
+def kt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1909_07729_b200 as kt
+    return kt
+
+
+def guarded(n, dtype, off=0, sentinel=-7.0):
+    buf = torch.full((n + 2 * G + off,), sentinel, dtype=dtype, device="cuda")
+    return buf, buf[G + off:G + off + n]
+
+
+def intact(buf, n, off=0, sentinel=-7.0):
+    torch.cuda.synchronize()
+    b = buf.float().cpu().numpy()
+    return np.all(b[:G + off] == sentinel) and np.all(b[G + off + n:] == sentinel)
+
+
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 999, 4097, 65537])
+@pytest.mark.parametrize("off", [0, 1, 5])
+def test_forward_and_backward_guards(kt, n, off):
+    for dt, sfx in ((torch.bfloat16, "bf16"), (torch.float32, "f32")):
+        x = (torch.randn(n, device="cuda") * 3).to(dt)
+        dy = torch.randn(n, device="cuda").to(dt)
+        for op in ("tanh", "gelu"):
+            buf, y = guarded(n, dt, off)
+            getattr(kt, f"k{op}_{sfx}")(x, out=y)
+            assert intact(buf, n, off), (op, sfx, n, off)
+            buf, y = guarded(n, dt, off)
+            getattr(kt, f"k{op}_bwd_{sfx}")(x, dy, out=y)
+            assert intact(buf, n, off), (op, "bwd", sfx, n, off)
+
+
+@pytest.mark.parametrize("rows,H", [(3, 16), (5, 10), (7, 1024)])
+def test_lstm_guards(kt, rows, H):
+    g = (torch.randn(rows, 4 * H, device="cuda") * 1.5).to(torch.bfloat16)
+    buf, y = guarded(rows * 4 * H, torch.bfloat16)
+    kt.klstm_gates_bf16(g, H, 2, out=y.view(rows, 4 * H))
+    assert intact(buf, rows * 4 * H)
+    c = torch.randn(rows, H, device="cuda")
+    cbuf, cn = guarded(rows * H, torch.float32)
+    hbuf, hn = guarded(rows * H, torch.bfloat16)
+    kt.klstm_cell_bf16(g, c, H, c_next=cn.view(rows, H), h_next=hn.view(rows, H))
+    assert intact(cbuf, rows * H) and intact(hbuf, rows * H)
+
+
+def test_gemm_guards(kt):
+    M, N, K = 256, 512, 192
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    buf = torch.full((M * N + 2 * 4096,), -7.0, dtype=torch.bfloat16, device="cuda")
+    C = buf[4096:4096 + M * N].view(M, N)                 # 32-byte aligned interior
+    kt.kgemm_bf16(A, B, epilogue="gelu", out=C)
+    torch.cuda.synchronize()
+    b = buf.float().cpu().numpy()
+    assert np.all(b[:4096] == -7.0) and np.all(b[4096 + M * N:] == -7.0)
