@@ -417,14 +417,65 @@ KT_API kt_status kgemm_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, s
   return KT_OK;
 }
 
+// Host-buffer strategy (KT_HOST_ZEROCOPY): 0 = copy-engine pipeline,
+// 1 = one zero-copy kernel, 2 = hybrid (copy-engine H2D, the kernel stores
+// its output straight into the mapped host buffer).  Default: see
+// kt_apply_host.
+static int host_mode() {
+  const char *e = getenv("KT_HOST_ZEROCOPY");   // read per call (tests switch it)
+  const int m = e ? atoi(e) : 0;
+  return (m == 1 || m == 2) ? m : 0;
+}
+
+// Device address of a pinned, mapped host buffer; NULL for pageable memory
+// or a host allocation that is not mapped into the current device.
+static const void *mapped_device_ptr(const void *h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+  return a.devicePointer;
+}
+
 KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, void *y_host, size_t n,
                                kt_lut lut, void *d_work, size_t work_bytes, void *stream) {
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
   if ((int)op < 0 || (int)op > 3 || (int)dtype < 0 || (int)dtype > 1)
     return fail(KT_ERR_ARG, "bad op/dtype");
   if (n == 0) return KT_OK;
-  if (!x_host || !y_host || !d_work) return fail(KT_ERR_ARG, "NULL pointer");
+  if (!x_host || !y_host) return fail(KT_ERR_ARG, "NULL pointer");
   const size_t es = dtype == KT_BF16 ? 2 : 4;
+  if (n > SIZE_MAX / es) return fail(KT_ERR_ARG, "n too large");
+  {
+    const uintptr_t xa = (uintptr_t)x_host, ya = (uintptr_t)y_host;
+    if (xa % es || ya % es) return fail(KT_ERR_ARG, "pointers must be %zu-byte aligned", es);
+    if (x_host != y_host && xa < ya + n * es && ya < xa + n * es)
+      return fail(KT_ERR_ARG, "x_host and y_host overlap without being equal");
+  }
+  // Zero-copy path (KT_HOST_ZEROCOPY=1): when both host buffers are pinned
+  // and mapped into the device address space (cudaHostAlloc / torch
+  // pin_memory under UVA), ONE kernel reads x over PCIe, applies the op and
+  // writes y back over PCIe.  Measured on B200 (profiles/host_path_r01.txt):
+  // SM-initiated traffic tops out at ~80 GB/s read+write vs ~96 GB/s for the
+  // two copy engines, and the hybrid (mode 2) is within noise of the
+  // pipeline, so the copy-engine pipeline is the default.
+  const int mode = host_mode();
+  void *y_mapped = mode ? const_cast<void *>(mapped_device_ptr(y_host)) : nullptr;
+  if (mode == 1) {
+    const void *xd = mapped_device_ptr(x_host);
+    if (xd && y_mapped) {
+      kt::LaunchInfo li;
+      kt_status s = launch_info(&li);
+      if (s != KT_OK) return s;
+      cudaError_t e = kt::launch_map((int)op, (int)dtype, xd, y_mapped, n, lut->words,
+                                     (cudaStream_t)stream, li, /*sysmem=*/true);
+      if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+      return KT_OK;
+    }
+  }
+  if (!d_work) return fail(KT_ERR_ARG, "NULL pointer");
   size_t chunk = work_bytes / (2 * kBufs * es);
   chunk -= chunk % 256;
   if (chunk < 4096)
@@ -461,14 +512,17 @@ KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, voi
     const size_t cnt = (n - off < chunk) ? n - off : chunk;
     const int b = (int)(k % kBufs);
     char *dx = work + (size_t)b * 2 * chunk * es;
-    char *dy = dx + chunk * es;
+    // hybrid (mode 2): the kernel stores straight into the mapped y_host
+    char *dy = y_mapped ? static_cast<char *>(y_mapped) + off * es : dx + chunk * es;
     if (k >= (size_t)kBufs) KT_CK(cudaStreamWaitEvent(h2d, p->ev_comp[b], 0), "wait");  // dx free
     KT_CK(cudaMemcpyAsync(dx, xh + off * es, cnt * es, cudaMemcpyHostToDevice, h2d), "H2D");
     KT_CK(cudaEventRecord(p->ev_in[b], h2d), "record");
     KT_CK(cudaStreamWaitEvent(comp, p->ev_in[b], 0), "wait");
-    if (k >= (size_t)kBufs) KT_CK(cudaStreamWaitEvent(comp, p->ev_out[b], 0), "wait");  // dy free
+    if (k >= (size_t)kBufs && !y_mapped)
+      KT_CK(cudaStreamWaitEvent(comp, p->ev_out[b], 0), "wait");  // dy free
     KT_CK(kt::launch_map((int)op, (int)dtype, dx, dy, cnt, lut->words, comp, li), "kernel launch");
     KT_CK(cudaEventRecord(p->ev_comp[b], comp), "record");
+    if (y_mapped) continue;
     KT_CK(cudaStreamWaitEvent(d2h, p->ev_comp[b], 0), "wait");
     KT_CK(cudaMemcpyAsync(yh + off * es, dy, cnt * es, cudaMemcpyDeviceToHost, d2h), "D2H");
     KT_CK(cudaEventRecord(p->ev_out[b], d2h), "record");

@@ -41,10 +41,11 @@ struct LaunchInfo {
   int sm_count;
 };
 
-// Enqueue op over n elements (x, y device pointers on the current device).
-// Returns the launch status; `launches` is incremented per kernel launched.
+// Enqueue op over n elements (x, y device-accessible pointers on the current
+// device).  sysmem: x / y are mapped pinned HOST memory read and written by
+// the kernel over PCIe (kt_apply_host's zero-copy path): no L2 prefetch.
 cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const LutWords &lut,
-                       cudaStream_t s, const LaunchInfo &li);
+                       cudaStream_t s, const LaunchInfo &li, bool sysmem = false);
 
 // Backward: dx = dy * g(a) (a = saved output for tanh/sigmoid, input x for
 // swish/gelu); reading R-BWD.

@@ -412,7 +412,7 @@ static unsigned flat_grid(uint64_t nchunks) {
 
 template <int OP, int FMT>
 static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &lut, cudaStream_t s,
-                             const LaunchInfo &li) {
+                             const LaunchInfo &li, bool sysmem) {
   constexpr size_t es = (FMT == FMT_BF16) ? 2 : 4;
   const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
   const uint8_t *xp = static_cast<const uint8_t *>(x);
@@ -432,7 +432,7 @@ static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &l
   if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const unsigned grid = flat_grid(nchunks);
   if (x != y) {
-    if (prefetch_enabled()) {
+    if (prefetch_enabled() && !sysmem) {   // L2 prefetch is for HBM inputs only
       static const int bps = resident_blocks(k_map<OP, FMT, true, true>);
       const uint32_t pf_blocks = (uint32_t)(li.sm_count * bps);
       return launch(k_map<OP, FMT, true, true>, grid, s, xp, yp, (uint32_t)head, nvec, tail,
@@ -446,9 +446,9 @@ static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &l
 }
 
 cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const LutWords &lut,
-                       cudaStream_t s, const LaunchInfo &li) {
+                       cudaStream_t s, const LaunchInfo &li, bool sysmem) {
 #define KT_CASE(O, F) \
-  if (op == O && fmt == F) return launch_op<O, F>(x, y, n, lut, s, li);
+  if (op == O && fmt == F) return launch_op<O, F>(x, y, n, lut, s, li, sysmem);
   KT_CASE(OP_TANH, FMT_BF16)
   KT_CASE(OP_SIGMOID, FMT_BF16)
   KT_CASE(OP_SWISH, FMT_BF16)

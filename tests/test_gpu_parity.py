@@ -314,20 +314,48 @@ def test_lstm_shapes(kt, hidden, rows, tq):
 
 
 @pytest.mark.parametrize("fmt", ["bf16", "f32"])
-def test_apply_host_pipeline(kt, fmt):
-    """kt_apply_host: host buffers -> chunked H2D / kernel / D2H over 3 streams."""
+@pytest.mark.parametrize("mem,mode", [("pinned", "0"), ("pinned", "1"), ("pinned", "2"),
+                                      ("pageable", "1")])
+def test_apply_host_pipeline(kt, fmt, mem, mode, monkeypatch):
+    """kt_apply_host on each host strategy (KT_HOST_ZEROCOPY): 0 = chunked
+    H2D / kernel / D2H pipeline over 3 streams, 1 = one zero-copy kernel
+    reading and writing the mapped pinned buffers over PCIe, 2 = H2D
+    pipeline with the kernel storing into the mapped output.  Pageable
+    buffers always take the pipeline.  Odd element offsets exercise the
+    head/tail path; the last case runs in place."""
+    monkeypatch.setenv("KT_HOST_ZEROCOPY", mode)
     dt = torch.bfloat16 if fmt == "bf16" else torch.float32
     n = 3 * 1000003
-    x = (torch.randn(n) * 3).to(dt).pin_memory()
-    y = torch.empty_like(x).pin_memory()
+    x0 = (torch.randn(n + 8) * 3).to(dt)
+    y0 = torch.empty_like(x0)
+    if mem == "pinned":
+        x0, y0 = x0.pin_memory(), y0.pin_memory()
     work = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
-    for op in ("tanh", "gelu"):
+
+    def bits(t):
+        return t.view(torch.int16).numpy().view(np.uint16) if fmt == "bf16" else \
+            t.view(torch.int32).numpy().view(np.uint32)
+
+    for op, xo, yo in (("tanh", 0, 0), ("gelu", 0, 0), ("sigmoid", 3, 3), ("swish", 1, 5)):
+        x, y = x0[xo:xo + n], y0[yo:yo + n]
         kt.apply_host(op, x, y, work)
         torch.cuda.current_stream().synchronize()
-        xb = x.view(torch.int16).numpy().view(np.uint16) if fmt == "bf16" else x.view(torch.int32).numpy().view(np.uint32)
-        yb = y.view(torch.int16).numpy().view(np.uint16) if fmt == "bf16" else y.view(torch.int32).numpy().view(np.uint32)
-        want = O.map_bf16(op, xb) if fmt == "bf16" else O.map_f32(op, xb)
-        check(op, fmt, yb, want, f"apply_host {op}")
+        want = O.map_bf16(op, bits(x)) if fmt == "bf16" else O.map_f32(op, bits(x))
+        check(op, fmt, bits(y), want, f"apply_host {mem} {op} offsets {xo},{yo}")
+    xi = x0[:n].clone()
+    if mem == "pinned":
+        xi = xi.pin_memory()
+    want = O.map_bf16("tanh", bits(xi)) if fmt == "bf16" else O.map_f32("tanh", bits(xi))
+    kt.apply_host("tanh", xi, xi, work)
+    torch.cuda.current_stream().synchronize()
+    check("tanh", fmt, bits(xi), want, f"apply_host {mem} in place")
+
+
+def test_apply_host_rejects_overlap(kt):
+    x = torch.zeros(1 << 12, dtype=torch.bfloat16).pin_memory()
+    work = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+    with pytest.raises(RuntimeError):
+        kt.apply_host("tanh", x[:2048], x[1:2049], work)
 
 
 def test_launch_counter(kt):
