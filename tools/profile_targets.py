@@ -35,6 +35,19 @@ def gemm_gelu():
     print("gemm_gelu ok", flush=True)
 
 
+def tanh_bf16_steady():
+    """Config 2 as bench.py streams it: 8 rotating input/output sets (512 MiB,
+    > 4x L2), 16 back-to-back launches.  Capture launch 12 with
+    --cache-control none: its DRAM count then includes the write-back of the
+    dirty output lines earlier launches left in L2 (steady-state traffic)."""
+    xs = [WL.make_input("c2_bf16_2p24", device="cuda", seed=2 + 1000 * k) for k in range(8)]
+    ys = [torch.empty_like(xs[0]) for _ in range(8)]
+    for i in range(16):
+        kt.ktanh_bf16(xs[i % 8], out=ys[i % 8])
+    torch.cuda.synchronize()
+    print("tanh_bf16_steady ok", flush=True)
+
+
 def lstm_cell():
     x = WL.make_input("c4_lstm_gates", device="cuda")
     c = torch.randn(x.numel() // (4 * WL.LSTM_HIDDEN), WL.LSTM_HIDDEN, device="cuda")
@@ -46,7 +59,7 @@ def lstm_cell():
 if __name__ == "__main__":
     names = sys.argv[1:] or list(TARGETS) + ["gemm_gelu", "lstm_cell"]
     for name in names:
-        if name in ("gemm_gelu", "lstm_cell"):
+        if name in ("gemm_gelu", "lstm_cell", "tanh_bf16_steady"):
             globals()[name]()
             continue
         key, fn = TARGETS[name]
