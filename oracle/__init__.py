@@ -20,6 +20,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ktanh_oracle.c")
+_SRC_APX = os.path.join(_HERE, "apx_oracle.c")     # Table 2 comparators
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -29,11 +30,13 @@ OPS = {"tanh": 0, "sigmoid": 1, "swish": 2, "gelu": 3}
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (binary64, no FP contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    stale = not os.path.exists(_LIB) or any(
+        os.path.getmtime(_LIB) < os.path.getmtime(f) for f in (_SRC, _SRC_APX))
+    if force or stale:
         tmp = _LIB + ".tmp%d" % os.getpid()
         subprocess.check_call(
             ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-             "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+             "-fPIC", "-shared", "-o", tmp, _SRC, _SRC_APX, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -91,6 +94,27 @@ def lib():
             L.kto_bounds_s.restype = None
             L.kto_gelu_consts.argtypes = [ctypes.c_int]
             L.kto_gelu_consts.restype = ctypes.c_uint32
+            dp = ctypes.POINTER(ctypes.c_double)
+            L.kto_tanh_maclaurin.argtypes = [ctypes.c_int, dp]
+            L.kto_tanh_maclaurin.restype = None
+            L.kto_pade.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp]
+            L.kto_pade.restype = ctypes.c_int
+            L.kto_pade_sat.argtypes = [ctypes.c_int, ctypes.c_int]
+            L.kto_pade_sat.restype = ctypes.c_double
+            L.kto_minimax_piece.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp]
+            L.kto_minimax_piece.restype = ctypes.c_int
+            L.kto_taylor_piece.argtypes = [ctypes.c_int, ctypes.c_int, dp]
+            L.kto_taylor_piece.restype = ctypes.c_int
+            L.kto_apx_params.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
+            L.kto_apx_params.restype = ctypes.c_int
+            L.kto_apx_eval.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, ctypes.c_double]
+            L.kto_apx_eval.restype = ctypes.c_double
+            L.kto_apx_map_bf16.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, u16p, u16p,
+                                           ctypes.c_size_t]
+            L.kto_apx_map_bf16.restype = None
+            L.kto_apx_map_f32.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, u32p, u32p,
+                                          ctypes.c_size_t]
+            L.kto_apx_map_f32.restype = None
             _lib = L
     return _lib
 
@@ -302,3 +326,91 @@ def error_sweep(lut: Lut | None = None):
     i = int(np.argmax(err)); j = int(np.argmax(rel))
     return {"max_abs": float(err[i]), "argmax_abs": int(w[i]),
             "max_rel": float(rel[j]), "argmax_rel": int(w[j])}
+
+
+# ---------------------------------------------------------------------------
+# Table 2 comparators: Pade,
+# piecewise minimax and piecewise Taylor forms of TanH, apx_oracle.c.
+# ---------------------------------------------------------------------------
+APX_KINDS = {"pade": 0, "minimax": 1, "taylor": 2}
+APX_PIECES = 16        # reading R-CMP-LAYOUT: 16 pieces of width 1/2 on [0, 8)
+APX_WIDTH = 0.5
+APX_XSAT = 8.0
+
+
+def tanh_maclaurin(n: int) -> np.ndarray:
+    t = np.zeros(n + 1)
+    lib().kto_tanh_maclaurin(n, t.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return t
+
+
+def pade(p: int, q: int):
+    """(a[0..p], b[0..q]) with b[0] = 1, or None if (p, q) is unsupported."""
+    a = np.zeros(p + 1); b = np.zeros(q + 1)
+    dp = ctypes.POINTER(ctypes.c_double)
+    if lib().kto_pade(p, q, a.ctypes.data_as(dp), b.ctypes.data_as(dp)) != 0:
+        return None
+    return a, b
+
+
+def pade_sat(p: int, q: int) -> float:
+    return float(lib().kto_pade_sat(p, q))
+
+
+def minimax_piece(deg: int, k: int):
+    """(c[0..3] in h = x - k/2, levelled error E, Remez iterations)."""
+    c = np.zeros(4); E = np.zeros(1)
+    dp = ctypes.POINTER(ctypes.c_double)
+    it = lib().kto_minimax_piece(deg, k, c.ctypes.data_as(dp), E.ctypes.data_as(dp))
+    return c, float(E[0]), int(it)
+
+
+def taylor_piece(deg: int, k: int) -> np.ndarray:
+    c = np.zeros(4)
+    rc = lib().kto_taylor_piece(deg, k, c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    assert rc == 0
+    return c
+
+
+class Apx:
+    """One comparator: kind in APX_KINDS; (p, q) = Pade orders, or (degree, 0)."""
+
+    def __init__(self, kind: str, p: int, q: int = 0):
+        self.kind, self.p, self.q = kind, p, q
+        self.par = np.zeros(1 + 4 * APX_PIECES)
+        rc = lib().kto_apx_params(APX_KINDS[kind], p, q, self._dp())
+        if rc != 0:
+            raise ValueError(f"unsupported comparator {kind} {p}/{q}")
+
+    def _dp(self):
+        return self.par.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+    def _args(self):
+        return (APX_KINDS[self.kind], self.p, self.q, self._dp())
+
+    @property
+    def xsat(self) -> float:
+        return float(self.par[0])
+
+    def piece(self, k: int) -> np.ndarray:
+        return self.par[1 + 4 * k: 5 + 4 * k].copy()
+
+    def pade_coeffs(self):
+        return self.par[1:self.p + 2].copy(), self.par[self.p + 2:self.p + self.q + 3].copy()
+
+    def eval(self, x: float) -> float:
+        return float(lib().kto_apx_eval(*self._args(), float(x)))
+
+    def map_bf16(self, x_u16: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x_u16, dtype=np.uint16)
+        y = np.empty_like(x)
+        u16p = ctypes.POINTER(ctypes.c_uint16)
+        lib().kto_apx_map_bf16(*self._args(), x.ctypes.data_as(u16p), y.ctypes.data_as(u16p), x.size)
+        return y
+
+    def map_f32(self, x_u32: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x_u32, dtype=np.uint32)
+        y = np.empty_like(x)
+        u32p = ctypes.POINTER(ctypes.c_uint32)
+        lib().kto_apx_map_f32(*self._args(), x.ctypes.data_as(u32p), y.ctypes.data_as(u32p), x.size)
+        return y
