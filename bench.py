@@ -160,6 +160,11 @@ class Step:
 
     def _bind(self):
         kt, op = self.kt, self.op
+        if op.startswith("apx:"):             # Table 2 comparator "apx:<kind>:<p>:<q>"
+            _, kind, p, q = op.split(":")
+            apx = kt.Apx(kind, int(p), int(q))
+            call = kt.kt_apx_tanh_bf16 if self.cfg.elem_bytes == 2 else kt.kt_apx_tanh_f32
+            return lambda x, y: call(x, apx, out=y)
         if op == "lstm":
             return lambda x, y: kt.klstm_gates_bf16(x, WL.LSTM_HIDDEN, 2, out=y)
         return lambda x, y: getattr(kt, op)(x, out=y)
@@ -400,6 +405,59 @@ def run_reference(args):
     return 0
 
 
+TABLE2_MAPS = [("ktanh", None), ("sfu", "apx:sfu:0:0"), ("libm", "apx:libm:0:0"),
+               ("pade_3_2", "apx:pade:3:2"), ("pade_7_8", "apx:pade:7:8"),
+               ("minimax_2", "apx:minimax:2:0"), ("minimax_3", "apx:minimax:3:0"),
+               ("taylor_2", "apx:taylor:2:0"), ("taylor_3", "apx:taylor:3:0")]
+
+
+def table2_b200(kt, K, W, world, device, rank, peak):
+    """Table 2 on B200.  For K-TanH and
+    each float-op comparator: accuracy over every finite BF16 input (the
+    GPU's own outputs vs binary64 tanh; max |err|, max relative err over
+    x != 0, reading A11), streaming throughput on config 2 (BF16 2^24,
+    rotating sets) and register-resident SM cycles per element
+    (kt_alu_probe: the analogue of the paper's cycles per TanH)."""
+    import numpy as np
+    xall = WL.make_input("c1_exhaustive_bf16", device=device)
+    xb = xall.view(torch.int16).cpu().numpy().view(np.uint16)
+    xv = (xb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    fin = np.isfinite(xv)
+    ref = np.tanh(xv)
+    g = torch.Generator().manual_seed(2)
+    sample = (torch.randn(8192, generator=g) * 2).to(torch.bfloat16).view(torch.int16) \
+        .numpy().view(np.uint16).view(np.uint32)[:4096].copy()
+    rows = {}
+    for name, op in TABLE2_MAPS:
+        if op is None:
+            y = kt.ktanh_bf16(xall)
+            cyc, _ = kt.alu_probe("bf16", sample, lut=kt.paper_lut())
+            st = Step(kt, "c2_bf16_2p24", "ktanh_bf16", device, rank)
+        else:
+            _, kind, p, q = op.split(":")
+            A = kt.Apx(kind, int(p), int(q))
+            y = kt.kt_apx_tanh_bf16(xall, A)
+            cyc, _ = kt.alu_probe("bf16", sample, apx=A)
+            st = Step(kt, "c2_bf16_2p24", op, device, rank)
+        yb = y.view(torch.int16).cpu().numpy().view(np.uint16)
+        yv = (yb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        err = np.abs(yv[fin] - ref[fin])
+        nz = fin & (xv != 0)
+        rel = np.abs(yv[nz] - ref[nz]) / np.abs(ref[nz])
+        wts, _, _ = time_windows(st, K, W, world, device, None, min_total_s=0.3, max_windows=400)
+        m_ = statistics.median(wts) / K
+        gbs = st.bytes_per_step / (m_ / 1e3) / 1e9
+        rows[name] = {"max_abs_err": float(err.max()), "max_rel_err_pct": round(float(rel.max()) * 100, 4),
+                      "gelem_s": round(st.n * world / (m_ / 1e3) / 1e9, 2),
+                      "hbm_gbs_per_gpu": round(gbs, 1), "frac_of_measured": round(gbs / peak, 4),
+                      "sm_cycles_per_elem_per_sm": round(cyc, 4)}
+        del st
+        torch.cuda.empty_cache()
+    return {"workload": "accuracy: all finite BF16 inputs; throughput: c2_bf16_2p24 (BF16 in/out)",
+            "note": "paper Table 2 (Intel CLX AVX512, cycles per TanH per core) is context only; "
+                    "readings R-CMP-* in DESIGN.md", "rows": rows}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -505,6 +563,9 @@ def main():
             "note": "tcgen05 GEMM, fp32 TMEM accumulation, K-GELU applied in the epilogue"}
         del gA, gB, gC
         torch.cuda.empty_cache()
+
+    if not args.no_extra:
+        extra["table2_b200"] = table2_b200(kt, K, W, world, device, rank, peak)
 
     cpu = None
     if rank == 0 and not args.no_cpu:

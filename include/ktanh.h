@@ -200,6 +200,52 @@ KT_API kt_status kt_apply_bwd(kt_op op, kt_dtype dtype, const void *a, const voi
                               size_t n, kt_lut lut, void *stream);
 
 /* ---------------------------------------------------------------------- */
+/* Table 2 comparators: the float-op TanH approximations */
+/* the paper measures K-TanH against, Sec. 2.1 minimax   */
+/* and Sec. 2.2 Pade, plus the GPU's own tanh routines.  */
+/* Readings R-CMP-* (DESIGN.md):                                            */
+/*   KT_APX_PADE     [p/q], p odd, q = p +- 1 even, p + q <= 19:            */
+/*                   y = x N(x^2) / D(x^2) (the Pade approximant, built as  */
+/*                   a convergent of Lambert's continued fraction),         */
+/*                   fp32 Horner + IEEE division, min(y, 1), and +-1 for    */
+/*                   |x| >= RN32(X_p), X_p = first x > 0 where the rational */
+/*                   reaches 1 or stops increasing.                         */
+/*   KT_APX_MINIMAX  degree p in 1..3 (q ignored): 16 pieces of width 1/2   */
+/*                   on [0, 8), per-piece minimax polynomial (Remez; piece  */
+/*                   0 constrained to P(0) = 0) in h = |x| - k/2;           */
+/*                   |x| >= 8 -> +-1.                                       */
+/*   KT_APX_TAYLOR   degree p in 1..3: same layout, piece 0 = Maclaurin     */
+/*                   polynomial, piece k >= 1 = Taylor polynomial about     */
+/*                   k/2 + 1/4.                                             */
+/*   KT_APX_LIBM     tanhf() of the CUDA math library (p, q ignored).       */
+/*   KT_APX_SFU      tanh.approx.f32 / tanh.approx.bf16x2 (MUFU.TANH).      */
+/* All are odd-extended (sign restored from x), NaN passes through          */
+/* unchanged; BF16 inputs are widened exactly, evaluated in fp32 with a     */
+/* fixed operation order and rounded once (RNE) to BF16.                    */
+/* kt_apx_create: KT_ERR_ARG for an unsupported (kind, p, q).  Handles are  */
+/* immutable host objects (thread-safe), passed to kernels by value.        */
+/* kt_apx_tanh_*: same conventions as ktanh_bf16 / ktanh_f32.               */
+/* ---------------------------------------------------------------------- */
+typedef enum {
+  KT_APX_PADE = 0, KT_APX_MINIMAX = 1, KT_APX_TAYLOR = 2, KT_APX_LIBM = 3, KT_APX_SFU = 4
+} kt_apx_kind;
+typedef struct kt_apx_s *kt_apx;
+
+/* Coefficient block returned by kt_apx_coeffs, binary64 (the kernels use
+ * these rounded to fp32):  coef[0] = saturation point (X_p, or 8);
+ * Pade: coef[1 + i] = a_i (i = 0..p), coef[2 + p + i] = b_i (i = 0..q),
+ *       b_0 = 1, R(x) = sum a_i x^i / sum b_i x^i;
+ * piecewise: coef[1 + 4k + j] = c_j of piece k (powers of h, see above). */
+#define KT_APX_NCOEF 65
+
+KT_API kt_status kt_apx_create(kt_apx_kind kind, int p, int q, kt_apx *out);
+KT_API kt_status kt_apx_coeffs(kt_apx a, double coef[KT_APX_NCOEF]);
+KT_API void kt_apx_destroy(kt_apx a);   /* NULL-safe */
+KT_API kt_status kt_apx_tanh_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_apx a,
+                                  void *stream);
+KT_API kt_status kt_apx_tanh_f32(const float *x, float *y, size_t n, kt_apx a, void *stream);
+
+/* ---------------------------------------------------------------------- */
 /* Host-buffer path (the end-to-end call a user with host data makes).    */
 /* ---------------------------------------------------------------------- */
 
@@ -249,6 +295,19 @@ KT_API kt_status kt_shard_range(size_t n, int world, int rank, size_t align,
 KT_API const char *kt_status_string(kt_status s);
 KT_API const char *kt_last_error(void);      /* thread-local; "" if none */
 KT_API int kt_abi_version(void);             /* == KT_ABI_VERSION */
+
+/* In-register throughput of one map on the current GPU: the B200 analogue of
+ * Table 2's "cycles per TanH".  Pass exactly one of lut
+ * (K-TanH, Alg. 1) or apx (a comparator).  sample_host: 4096 host words of
+ * input (BF16 pairs or F32) that every thread cycles through.  One full wave
+ * of CTAs holds 16 words per thread in registers and applies the map `iters`
+ * rounds with no memory traffic; *cycles_gross = SM clock cycles per element
+ * per SM (max CTA clock64 span / elements per SM), *cycles_net = the same
+ * minus an identity map's loop cost.  SYNCHRONOUS (allocates and frees
+ * 64 KiB-scale scratch, synchronises the device): a diagnostic, not a hot-
+ * path call. */
+KT_API kt_status kt_alu_probe(kt_dtype dtype, kt_lut lut, kt_apx apx, const void *sample_host,
+                              int iters, double *cycles_net, double *cycles_gross);
 
 /* Number of kernel launches this process has issued through the library
  * (all devices, all threads); used by bench.py's gpu_launches count. */

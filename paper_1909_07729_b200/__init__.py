@@ -40,7 +40,9 @@ BWD_CALLS = ("ktanh_bwd_bf16", "ktanh_bwd_f32", "ksigmoid_bwd_bf16", "ksigmoid_b
 BWD_LUT_CALLS = ("kswish_bwd_bf16", "kswish_bwd_f32", "kgelu_bwd_bf16", "kgelu_bwd_f32")
 EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_create", "kt_lut_create_paper", "kt_lut_get", "kt_lut_destroy",
                        "klstm_gates_bf16", "klstm_cell_bf16", "kgemm_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
-                       "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count")
+                       "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count",
+                       "kt_apx_create", "kt_apx_coeffs", "kt_apx_destroy", "kt_apx_tanh_bf16",
+                       "kt_apx_tanh_f32", "kt_alu_probe")
 
 for _name in MAP_CALLS:
     _f = getattr(_lib, _name)
@@ -85,6 +87,23 @@ _lib.kt_abi_version.argtypes = []
 _lib.kt_abi_version.restype = ctypes.c_int
 _lib.kt_launch_count.argtypes = []
 _lib.kt_launch_count.restype = ctypes.c_uint64
+_lib.kt_apx_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]
+_lib.kt_apx_create.restype = ctypes.c_int
+_lib.kt_apx_coeffs.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
+_lib.kt_apx_coeffs.restype = ctypes.c_int
+_lib.kt_apx_destroy.argtypes = [_vp]
+_lib.kt_apx_destroy.restype = None
+for _name in ("kt_apx_tanh_bf16", "kt_apx_tanh_f32"):
+    _f = getattr(_lib, _name)
+    _f.argtypes = [_vp, _vp, _sz, _vp, _vp]
+    _f.restype = ctypes.c_int
+
+_lib.kt_alu_probe.argtypes = [ctypes.c_int, _vp, _vp, _vp, ctypes.c_int,
+                              ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+_lib.kt_alu_probe.restype = ctypes.c_int
+
+APX_KINDS = {"pade": 0, "minimax": 1, "taylor": 2, "libm": 3, "sfu": 4}
+APX_NCOEF = 65
 
 
 class KTanhError(RuntimeError):
@@ -372,3 +391,79 @@ def shard_range(n: int, world: int, rank: int, align: int = 16):
     _check(_lib.kt_shard_range(n, world, rank, align, ctypes.byref(b), ctypes.byref(c)),
            "kt_shard_range")
     return b.value, c.value
+
+
+# ---------------------------------------------------------------------------
+# Table 2 comparators (include/ktanh.h "Table 2 comparators")
+# ---------------------------------------------------------------------------
+class Apx:
+    """Immutable float-op TanH approximation handle (kt_apx_create):
+    kind in APX_KINDS; (p, q) = Pade orders, or (degree, 0) for minimax/taylor."""
+
+    def __init__(self, kind: str, p: int = 0, q: int = 0):
+        if kind not in APX_KINDS:
+            raise ValueError(f"kind must be one of {sorted(APX_KINDS)}")
+        self.kind, self.p, self.q = kind, p, q
+        h = _vp()
+        _check(_lib.kt_apx_create(APX_KINDS[kind], p, q, ctypes.byref(h)), "kt_apx_create")
+        self._h = h
+
+    def coeffs(self):
+        """Binary64 coefficient block (layout: KT_APX_NCOEF in include/ktanh.h)."""
+        c = (ctypes.c_double * APX_NCOEF)()
+        _check(_lib.kt_apx_coeffs(self._h, c), "kt_apx_coeffs")
+        return list(c)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __repr__(self):
+        return f"Apx({self.kind!r}, {self.p}, {self.q})"
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        lib = globals().get("_lib")
+        if h is not None and h.value and lib is not None:
+            lib.kt_apx_destroy(h)
+            self._h = _vp()
+
+
+def _make_apx_call(name, dtype_name):
+    fn = getattr(_lib, name)
+
+    def call(x, apx: Apx, out=None, stream=None):
+        import torch
+        dt = torch.bfloat16 if dtype_name == "bf16" else torch.float32
+        out = _prep(x, out, dt)
+        idx = x.device.index
+        with _on_device(idx):
+            _check(fn(x.data_ptr(), out.data_ptr(), x.numel(), apx.handle, _stream_ptr(stream, idx)),
+                   name)
+        return out
+
+    call.__name__ = name
+    call.__doc__ = f"{name}(x, apx, out=None, stream=None) -> out   (C ABI: include/ktanh.h)"
+    return call
+
+
+kt_apx_tanh_bf16 = _make_apx_call("kt_apx_tanh_bf16", "bf16")
+kt_apx_tanh_f32 = _make_apx_call("kt_apx_tanh_f32", "f32")
+
+
+def alu_probe(dtype: str, sample, lut: Lut | None = None, apx: Apx | None = None,
+              iters: int = 256):
+    """kt_alu_probe: (net, gross) SM cycles per element per SM of K-TanH (lut)
+    or a comparator (apx), register-resident.  `sample`: 4096 uint32 words
+    (numpy) -- BF16 pairs or F32 bit patterns.  Synchronous."""
+    import numpy as np
+    words = np.ascontiguousarray(sample, dtype=np.uint32)
+    if words.size != 4096:
+        raise ValueError("sample must hold 4096 words")
+    if (lut is None) == (apx is None):
+        raise ValueError("pass exactly one of lut, apx")
+    net, gross = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.kt_alu_probe(DTYPES[dtype], lut.handle if lut else None,
+                             apx.handle if apx else None, words.ctypes.data, iters,
+                             ctypes.byref(net), ctypes.byref(gross)), "kt_alu_probe")
+    return net.value, gross.value

@@ -23,6 +23,11 @@ struct kt_lut_s {
   kt::LutWords words;
 };
 
+struct kt_apx_s {
+  double coef[kt::kApxCoef];
+  kt::ApxWords words;
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -307,6 +312,66 @@ KT_API kt_status kgelu_f32(const float *x, float *y, size_t n, kt_lut lut, void 
 KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size_t n, kt_lut lut,
                           void *stream) {
   return run_map((int)op, (int)dtype, x, y, n, lut, stream);
+}
+
+// ---- Table 2 comparators --------------------------------
+KT_API kt_status kt_apx_create(kt_apx_kind kind, int p, int q, kt_apx *out) {
+  if (!out) return fail(KT_ERR_ARG, "NULL argument");
+  if ((int)kind < 0 || (int)kind > 4) return fail(KT_ERR_ARG, "bad approximation kind %d", (int)kind);
+  kt_apx_s tmp;
+  char err[256];
+  if (!kt::apx_build((int)kind, p, q, &tmp.words, tmp.coef, err, sizeof(err)))
+    return fail(KT_ERR_ARG, "%s", err);
+  kt_apx_s *A = new (std::nothrow) kt_apx_s(tmp);
+  if (!A) return fail(KT_ERR_ARG, "out of host memory");
+  *out = A;
+  return KT_OK;
+}
+
+KT_API kt_status kt_apx_coeffs(kt_apx a, double coef[KT_APX_NCOEF]) {
+  if (!a || !coef) return fail(KT_ERR_ARG, "NULL argument");
+  memcpy(coef, a->coef, sizeof(a->coef));
+  return KT_OK;
+}
+
+KT_API void kt_apx_destroy(kt_apx a) { delete a; }
+
+static kt_status run_apx(int fmt, const void *x, void *y, size_t n, kt_apx a, void *stream) {
+  if (!a) return fail(KT_ERR_ARG, "approximation handle is NULL");
+  if (n == 0) return KT_OK;
+  const size_t es = fmt == kt::FMT_BF16 ? 2 : 4;
+  kt::LaunchInfo li;
+  kt_status s = check_buffers(x, y, n, es, &li);
+  if (s != KT_OK) return s;
+  cudaError_t e = kt::launch_apx(fmt, x, y, n, a->words, (cudaStream_t)stream, li);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return KT_OK;
+}
+
+KT_API kt_status kt_apx_tanh_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_apx a, void *stream) {
+  return run_apx(kt::FMT_BF16, x, y, n, a, stream);
+}
+KT_API kt_status kt_apx_tanh_f32(const float *x, float *y, size_t n, kt_apx a, void *stream) {
+  return run_apx(kt::FMT_F32, x, y, n, a, stream);
+}
+
+KT_API kt_status kt_alu_probe(kt_dtype dtype, kt_lut lut, kt_apx apx, const void *sample_host,
+                              int iters, double *cycles_net, double *cycles_gross) {
+  if ((!lut) == (!apx)) return fail(KT_ERR_ARG, "pass exactly one of lut, apx");
+  if ((int)dtype < 0 || (int)dtype > 1) return fail(KT_ERR_ARG, "bad dtype");
+  if (!sample_host || !cycles_net || !cycles_gross || iters < 1)
+    return fail(KT_ERR_ARG, "NULL argument or iters < 1");
+  kt::LaunchInfo li;
+  kt_status s = launch_info(&li);
+  if (s != KT_OK) return s;
+  static const kt::LutWords zero_lut = {};
+  static const kt::ApxWords zero_apx = {};
+  cudaError_t e = kt::alu_probe(lut ? 1 : 2, (int)dtype, lut ? lut->words : zero_lut,
+                                apx ? apx->words : zero_apx, iters,
+                                static_cast<const uint32_t *>(sample_host), cycles_net,
+                                cycles_gross, li.sm_count);
+  if (e != cudaSuccess) return cuda_fail(e, "kt_alu_probe");
+  return KT_OK;
 }
 
 KT_API kt_status ktanh_bwd_bf16(const uint16_t *y, const uint16_t *dy, uint16_t *dx, size_t n,

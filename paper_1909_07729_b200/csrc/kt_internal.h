@@ -67,5 +67,36 @@ cudaError_t launch_gemm(int epi, const uint16_t *A, const uint16_t *B, uint16_t 
                         size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms);
 
 void count_launch();
+bool pdl_enabled();        // KT_PDL != 0
+bool prefetch_enabled();   // KT_PREFETCH != 0 (and PDL on)
+
+// ---- Table 2 comparators (kt_apx.cu) --------------------
+enum ApxKind { APX_PADE = 0, APX_MINIMAX = 1, APX_TAYLOR = 2, APX_LIBM = 3, APX_SFU = 4 };
+// Piecewise layout, reading R-CMP-LAYOUT: 16 pieces of width 1/2 on [0, 8).
+constexpr int kApxPieces = 16;
+constexpr double kApxWidth = 0.5;
+constexpr double kApxXsat = 8.0;
+constexpr int kApxCoef = 1 + 4 * kApxPieces;   // == KT_APX_NCOEF
+
+// Kernel parameter block (by value, __grid_constant__).  Pade: y = x N(s)/D(s)
+// with s = x^2, num/den in powers of s (D(0) = 1), xsat = RN32(X_p).
+// Piecewise: pc[j][k] = coefficient j of piece k (lanes 16..31 mirror 0..15).
+struct ApxWords {
+  int32_t kind, p, q, pad;
+  float xsat;
+  float num[6];
+  float den[6];
+  float pc[4][32];
+};
+
+// Derive the coefficients (host); coef[kApxCoef] receives them in binary64
+// in the layout of KT_APX_NCOEF (include/ktanh.h).  false + message if the
+// (kind, p, q) is unsupported.
+bool apx_build(int kind, int p, int q, ApxWords *w, double *coef, char *err, size_t errlen);
+// In-register throughput probe (kt_alu_probe): which = 1 K-TanH, 2 comparator.
+cudaError_t alu_probe(int which, int fmt, const LutWords &lw, const ApxWords &w, int iters,
+                      const uint32_t *host_in4096, double *cyc_net, double *cyc_gross, int sms);
+cudaError_t launch_apx(int fmt, const void *x, void *y, size_t n, const ApxWords &w,
+                       cudaStream_t s, const LaunchInfo &li);
 
 }  // namespace kt

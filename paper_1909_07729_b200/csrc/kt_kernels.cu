@@ -344,7 +344,7 @@ k_lstm_elem(const uint16_t *__restrict__ x, uint16_t *__restrict__ y, uint64_t n
 
 // ---------------------------------------------------------------- host ----
 
-static bool pdl_enabled() {
+bool pdl_enabled() {
   static const bool on = [] {
     const char *e = getenv("KT_PDL");
     return !(e && e[0] == '0');
@@ -355,7 +355,7 @@ static bool pdl_enabled() {
 // cudaLaunchKernelEx with the programmatic-stream-serialization attribute.
 // Early L2 prefetch of each warp's input chunk (before the PDL wait);
 // KT_PREFETCH=0 disables.
-static bool prefetch_enabled() {
+bool prefetch_enabled() {
   static const bool on = [] {
     const char *e = getenv("KT_PREFETCH");
     return !(e && e[0] == '0');

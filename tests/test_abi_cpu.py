@@ -137,3 +137,56 @@ def test_product_and_oracle_do_not_import_each_other():
         for m in imp.finditer(open(os.path.join(ROOT, "oracle", f)).read()):
             tgt = "".join(g or "" for g in m.groups())
             assert "paper_1909_07729_b200" not in tgt and "ktanh.h" not in tgt and "kt_" not in tgt
+
+
+# --------------------------------------------------------------------------
+# Table 2 comparators: host-side coefficient generation
+# --------------------------------------------------------------------------
+APX_CMP = [("pade", 3, 2), ("pade", 7, 8), ("pade", 1, 0), ("pade", 1, 2), ("pade", 5, 4),
+           ("pade", 5, 6), ("pade", 7, 6), ("minimax", 1, 0), ("minimax", 2, 0),
+           ("minimax", 3, 0), ("taylor", 1, 0), ("taylor", 2, 0), ("taylor", 3, 0)]
+
+
+@pytest.mark.parametrize("cfg", APX_CMP)
+def test_apx_coefficients_match_oracle(kt, cfg):
+    """The product derives its coefficients one way (Lambert convergents in
+    integers, its own Remez with Newton-refined extrema, derivative
+    polynomials in tanh(m)), the oracle another (the Pade linear system,
+    Remez with golden-section extrema, the addition formula): they agree,
+    and the fp32 saturation constants the kernels compare against are
+    identical."""
+    A = kt.Apx(*cfg)
+    B = O.Apx(*cfg)
+    c = np.array(A.coeffs())
+    assert np.float32(c[0]) == np.float32(B.par[0])
+    n = 1 + (cfg[1] + cfg[2] + 2 if cfg[0] == "pade" else 4 * O.APX_PIECES)
+    np.testing.assert_allclose(c[1:n], B.par[1:n], rtol=1e-6, atol=1e-12)
+    a32 = c[1:n].astype(np.float32).view(np.int32).astype(np.int64)
+    b32 = B.par[1:n].astype(np.float32).view(np.int32).astype(np.int64)
+    assert np.abs(a32 - b32).max() <= 1      # same sign: at most 1 fp32 ulp apart
+
+
+@pytest.mark.parametrize("bad", [("pade", 2, 2), ("pade", 3, 3), ("pade", 3, 6), ("pade", 11, 12),
+                                 ("minimax", 0, 0), ("minimax", 4, 0), ("taylor", 7, 0)])
+def test_apx_rejects_unsupported(kt, bad):
+    with pytest.raises(kt.KTanhError):
+        kt.Apx(*bad)
+
+
+def test_apx_calls_reject_host_pointers(kt):
+    import torch
+    A = kt.Apx("minimax", 3)
+    x = torch.zeros(64, dtype=torch.bfloat16)
+    with pytest.raises(TypeError):
+        kt.kt_apx_tanh_bf16(x, A)
+    buf = (ctypes.c_uint16 * 64)()
+    # a host pointer never reaches a launch (KT_ERR_ARG on a GPU box, KT_ERR_CUDA without a device)
+    st = kt._lib.kt_apx_tanh_bf16(ctypes.addressof(buf), ctypes.addressof(buf), 64, A.handle, None)
+    assert st in (kt.KT_ERR_ARG, kt.KT_ERR_CUDA)
+    lib = kt._lib
+    for f in (lib.kt_apx_tanh_bf16, lib.kt_apx_tanh_f32):
+        assert f(None, None, 0, A.handle, None) == kt.KT_OK               # n == 0: no launch
+        assert f(None, None, 16, A.handle, None) == kt.KT_ERR_ARG         # NULL with n > 0
+        assert f(ctypes.addressof(buf), ctypes.addressof(buf), 16, None, None) == kt.KT_ERR_ARG
+    assert lib.kt_apx_tanh_f32(ctypes.c_void_p(0x1002), ctypes.c_void_p(0x10002), 4, A.handle,
+                               None) == kt.KT_ERR_ARG                     # misaligned
