@@ -51,6 +51,16 @@ __device__ __forceinline__ uint32_t shfl_f(float v, uint32_t lane) {
   return __shfl_sync(0xffffffffu, __float_as_uint(v), (int)lane);
 }
 
+// This lane's coefficient j (piece = lane).  The empty volatile asm makes the
+// register value opaque: otherwise the compiler may rematerialise it inside
+// loops as a lane-indexed (divergent, serialised) constant-bank load -- seen
+// in SASS as LDC c[0x0][Rlane + ...] per round, 3x slower.
+__device__ __forceinline__ float lane_coef(const ApxWords &w, int j, uint32_t lane) {
+  float v = w.pc[j][lane];
+  asm volatile("" : "+f"(v));
+  return v;
+}
+
 // Magnitude maps a >= 0 (not NaN) -> approximation of tanh(a) in [0, 1].
 
 // Piecewise polynomial: k = floor(2a) via one round-toward-zero FMA
@@ -178,7 +188,7 @@ k_apx(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
   const uint32_t lane = threadIdx.x & 31;
   float c[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) c[j] = w.pc[j][lane];
+  for (int j = 0; j < 4; ++j) c[j] = lane_coef(w, j, lane);
   const uint8_t *xb = x + (size_t)head * es;
   uint8_t *yb = y + (size_t)head * es;
   const uint64_t ch = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -229,7 +239,7 @@ k_apx_pipe(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t 
   const uint32_t lane = threadIdx.x & 31;
   float c[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) c[j] = w.pc[j][lane];
+  for (int j = 0; j < 4; ++j) c[j] = lane_coef(w, j, lane);
   const uint8_t *xb = x + (size_t)head * es;
   uint8_t *yb = y + (size_t)head * es;
   const uint64_t nch = (nvec + kChunkVecs - 1) / kChunkVecs;
@@ -281,7 +291,7 @@ k_apx_elem(const uint8_t *x, uint8_t *y, uint64_t n, const __grid_constant__ Apx
   const uint32_t lane = threadIdx.x & 31;
   float c[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) c[j] = w.pc[j][lane];
+  for (int j = 0; j < 4; ++j) c[j] = lane_coef(w, j, lane);
   pdl_enter();
   const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
@@ -593,10 +603,11 @@ __global__ void __launch_bounds__(kThreads)
 k_alu(const uint32_t *in, uint32_t *out, long long *cyc, int iters,
       const __grid_constant__ LutWords lw, const __grid_constant__ ApxWords w) {
   const uint32_t lane = threadIdx.x & 31;
-  const LaneLut L{lw.bf16[lane], lw.f32K[lane], lw.f32C[lane]};
+  LaneLut L{lw.bf16[lane], lw.f32K[lane], lw.f32C[lane]};
+  asm volatile("" : "+r"(L.w16), "+r"(L.k32), "+r"(L.c32));   // see lane_coef
   float c[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) c[j] = w.pc[j][lane];
+  for (int j = 0; j < 4; ++j) c[j] = lane_coef(w, j, lane);
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t v[16];
 #pragma unroll

@@ -61,6 +61,15 @@ __device__ __forceinline__ LaneLut load_lane_lut(const LutWords &lut) {
   return LaneLut{lut.bf16[lane], lut.f32K[lane], lut.f32C[lane]};
 }
 
+// For the grid-stride (looping) kernels: the empty volatile asm makes the
+// lane's words opaque, so the compiler cannot rematerialise them inside the
+// loop as lane-indexed (divergent, serialised) constant-bank loads.
+__device__ __forceinline__ LaneLut load_lane_lut_reg(const LutWords &lut) {
+  LaneLut L = load_lane_lut(lut);
+  asm volatile("" : "+r"(L.w16), "+r"(L.k32), "+r"(L.c32));
+  return L;
+}
+
 // Element-wise head/tail helper: lane i handles element i (i < cnt) of the
 // range starting at p.  All 32 lanes execute apply_word (shuffle-safe).
 template <int OP, int FMT>
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(kThreads)
 k_bwd_elem(const uint8_t *a, const uint8_t *dy, uint8_t *dx, uint64_t n,
            const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
-  const LaneLut L = load_lane_lut(lut);
+  const LaneLut L = load_lane_lut_reg(lut);
   pdl_enter();
   const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
@@ -211,7 +220,7 @@ __global__ void __launch_bounds__(kThreads)
 k_map_elem(const uint8_t *__restrict__ x, uint8_t *__restrict__ y, uint64_t n,
            const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
-  const LaneLut L = load_lane_lut(lut);
+  const LaneLut L = load_lane_lut_reg(lut);
   pdl_enter();
   const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
@@ -302,7 +311,7 @@ k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_
 __global__ void __launch_bounds__(kThreads)
 k_lstm_cell_elem(const uint16_t *gates, const float *c_prev, float *c_next, uint16_t *h_next,
                  uint64_t n, uint64_t hidden, const __grid_constant__ LutWords lut) {
-  const LaneLut L = load_lane_lut(lut);
+  const LaneLut L = load_lane_lut_reg(lut);
   pdl_enter();
   const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
@@ -327,7 +336,7 @@ k_lstm_cell_elem(const uint16_t *gates, const float *c_prev, float *c_next, uint
 __global__ void __launch_bounds__(kThreads)
 k_lstm_elem(const uint16_t *__restrict__ x, uint16_t *__restrict__ y, uint64_t n, uint64_t width,
             uint64_t hidden, int tanh_quarter, const __grid_constant__ LutWords lut) {
-  const LaneLut L = load_lane_lut(lut);
+  const LaneLut L = load_lane_lut_reg(lut);
   pdl_enter();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
