@@ -160,10 +160,29 @@ __device__ __forceinline__ uint32_t ktanh_f32(uint32_t u, uint32_t lk, uint32_t 
 // GELU ~= x/2 (1 + TanH(sqrt(2/pi)(x + a x^3))).  fp32 scaffolding with
 // explicit _rn intrinsics (no contraction), one rounding to the format.
 
+// Packed BF16 arithmetic (HMUL2/HFMA2.BF16, FMA pipe): the exact result
+// rounded once to BF16 (RNE), subnormals kept.
+__device__ __forceinline__ uint32_t hmul2_bf16(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t hfma2_bf16(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+constexpr uint32_t kHalfx2 = 0x3F003F00u;   // (0.5, 0.5) in BF16
+
+// K-Sigmoid: h = RN_bf16(x/2) and RN_bf16((1 + t)/2) each in ONE packed BF16
+// instruction (exact product / fma rounded once) instead of widen + fp32 op +
+// pack: 2 FMA-pipe ops per pair instead of 2 FMA + 6 ALU.  Same values as the
+// fp32 route (x/2 is exact in fp32; 0.5 t + 0.5 is exact in fp32 whenever
+// the BF16 rounding could be affected), checked over all 65,536 patterns.
 __device__ __forceinline__ uint32_t ksigmoid_bf16x2(uint32_t x, uint32_t lw) {
-  const uint32_t h = pack2(mul2(widen2(x), splat2(0.5f)));                 // RN_bf16(x/2)
+  const uint32_t h = hmul2_bf16(x, kHalfx2);                              // RN_bf16(x/2)
   const uint32_t t = ktanh_bf16x2(h, lw);
-  return pack2(fma2(splat2(0.5f), widen2(t), splat2(0.5f)));               // RN((1+t)/2)
+  return hfma2_bf16(t, kHalfx2, kHalfx2);                                 // RN((1+t)/2)
 }
 
 __device__ __forceinline__ uint32_t kswish_bf16x2(uint32_t x, uint32_t lw) {
@@ -333,9 +352,9 @@ __device__ __forceinline__ uint32_t lstm_cell2(uint32_t gi, uint32_t gf, uint32_
 
 // LSTM gate pair: K-TanH (is_tanh) or K-Sigmoid, same core, per-lane choice.
 __device__ __forceinline__ uint32_t lstm_bf16x2(uint32_t x, uint32_t lw, bool is_tanh) {
-  const uint32_t h = is_tanh ? x : pack2(mul2(widen2(x), splat2(0.5f)));
+  const uint32_t h = is_tanh ? x : hmul2_bf16(x, kHalfx2);
   const uint32_t t = ktanh_bf16x2(h, lw);
-  return is_tanh ? t : pack2(fma2(splat2(0.5f), widen2(t), splat2(0.5f)));
+  return is_tanh ? t : hfma2_bf16(t, kHalfx2, kHalfx2);
 }
 
 // ------------------------------------------------------ streaming memory --
