@@ -362,7 +362,7 @@ KERNEL_NAME = {"ktanh_bf16": "k_map<0, 0, true>", "ktanh_f32": "k_map<0, 1, true
                "kgelu_bf16": "k_map<3, 0, true>", "kswish_bf16": "k_map<2, 0, true>",
                "lstm": "k_lstm<true>"}
 
-EXTRA = [("c3_f32_2p28", "ktanh_f32"), ("c4_lstm_gates", "lstm"),
+EXTRA = [("c3_f32_2p28", "ktanh_f32"), ("c3_f32_2p28", "ktanh_f32_via_bf16"), ("c4_lstm_gates", "lstm"),
          ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16"),
          ("c5_ffn_2p30", "kgelu_bwd_bf16"), ("c4_lstm_gates", "lstm_cell")]
 

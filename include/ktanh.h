@@ -109,6 +109,13 @@ KT_API kt_status ktanh_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut
  * mantissa bits), M_o = (M23 >> r_t) + b_t 2^16. */
 KT_API kt_status ktanh_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream);
 
+/* K-TanH of F32 data through BF16 (the alternative to
+ * reading A8; "We assume BFloat16 input for K-TanH (Float32 to
+ * BFloat16 conversion cost is not considered)"): y = widen(ktanh_bf16(
+ * RNE_bf16(x))), so every output is a BF16 value stored as F32.  NaN -> NaN
+ * (canonical quiet NaN); |x| > max BF16 rounds to inf and saturates to +-1. */
+KT_API kt_status ktanh_f32_via_bf16(const float *x, float *y, size_t n, kt_lut lut, void *stream);
+
 /* K-Sigmoid = (1 + K-TanH(x/2))/2 (reading A7).  x/2 is
  * rounded to the format, the affine step is one fp32 fma rounded once to
  * the format. */

@@ -25,7 +25,8 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-OPS = {"tanh": 0, "sigmoid": 1, "swish": 2, "gelu": 3}
+OPS = {"tanh": 0, "sigmoid": 1, "swish": 2, "gelu": 3,
+       "tanh_via_bf16": 4}     # F32 only: K-TanH of RN_bf16(x), widened (NEXT-3)
 
 
 def build(force: bool = False) -> str:

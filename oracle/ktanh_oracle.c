@@ -221,6 +221,20 @@ uint32_t kto_ktanh_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
 }
 
 /* ------------------------------------------------------------------ */
+/* K-TanH of a Float32 value through BFloat16 (the     */
+/* alternative to reading A8): "We assume BFloat16 input    */
+/* for K-TanH (Float32 to BFloat16 conversion cost is not considered)".  */
+/* Round the F32 value to the nearest BF16 (ties to even), apply Alg. 1, */
+/* and return the BF16 result as an F32 (exact widening: append 16 zero  */
+/* bits).  NaN -> the BF16 canonical NaN widened.                        */
+/* ------------------------------------------------------------------ */
+uint32_t kto_ktanh_f32_via_bf16(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    const uint16_t b = kto_bf16_encode_rne((double)f32_from_bits(x));
+    return (uint32_t)kto_ktanh_bf16(b, TE, Tr, Tb) << 16;
+}
+
+/* ------------------------------------------------------------------ */
 /* Derived activations, PAPER.md:60-71 (Sec. 1).                          */
 /*   Sigmoid(x) = (1 + TanH(x/2))/2   (parentheses garbled in the paper,  */
 /*                                     reading A7)                        */
@@ -371,7 +385,7 @@ void kto_bwd_map_f32(int op, const uint32_t *a, const uint32_t *dy, uint32_t *dx
 
 /* ------------------------------------------------------------------ */
 /* Array entry points (loops over the scalar functions above).            */
-/* op: 0 tanh, 1 sigmoid, 2 swish, 3 gelu                                 */
+/* op: 0 tanh, 1 sigmoid, 2 swish, 3 gelu (4: F32 only, tanh via BF16)   */
 /* ------------------------------------------------------------------ */
 void kto_map_bf16(int op, const uint16_t *x, uint16_t *y, size_t n,
                   const int *TE, const int *Tr, const int *Tb)
@@ -394,6 +408,7 @@ void kto_map_f32(int op, const uint32_t *x, uint32_t *y, size_t n,
         case 0: y[i] = kto_ktanh_f32(x[i], TE, Tr, Tb); break;
         case 1: y[i] = kto_ksigmoid_f32(x[i], TE, Tr, Tb); break;
         case 2: y[i] = kto_kswish_f32(x[i], TE, Tr, Tb); break;
+        case 4: y[i] = kto_ktanh_f32_via_bf16(x[i], TE, Tr, Tb); break;
         default: y[i] = kto_kgelu_f32(x[i], TE, Tr, Tb); break;
         }
     }

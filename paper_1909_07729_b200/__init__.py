@@ -35,7 +35,7 @@ OPS = {"tanh": 0, "sigmoid": 1, "swish": 2, "gelu": 3}
 DTYPES = {"bf16": 0, "f32": 1}
 
 MAP_CALLS = ("ktanh_bf16", "ktanh_f32", "ksigmoid_bf16", "ksigmoid_f32",
-             "kswish_bf16", "kswish_f32", "kgelu_bf16", "kgelu_f32")
+             "kswish_bf16", "kswish_f32", "kgelu_bf16", "kgelu_f32", "ktanh_f32_via_bf16")
 BWD_CALLS = ("ktanh_bwd_bf16", "ktanh_bwd_f32", "ksigmoid_bwd_bf16", "ksigmoid_bwd_f32")
 BWD_LUT_CALLS = ("kswish_bwd_bf16", "kswish_bwd_f32", "kgelu_bwd_bf16", "kgelu_bwd_f32")
 EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_create", "kt_lut_create_paper", "kt_lut_get", "kt_lut_destroy",
@@ -252,6 +252,7 @@ kswish_bf16 = _make_call("kswish_bf16", "bf16")
 kswish_f32 = _make_call("kswish_f32", "f32")
 kgelu_bf16 = _make_call("kgelu_bf16", "bf16")
 kgelu_f32 = _make_call("kgelu_f32", "f32")
+ktanh_f32_via_bf16 = _make_call("ktanh_f32_via_bf16", "f32")
 
 
 def _make_bwd(name, dtype_name, needs_lut):

@@ -171,7 +171,8 @@ kt_status check_buffers(const void *x, const void *y, size_t n, size_t es, kt::L
 
 kt_status run_map(int op, int fmt, const void *x, void *y, size_t n, kt_lut lut, void *stream) {
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
-  if (op < 0 || op > 3 || fmt < 0 || fmt > 1) return fail(KT_ERR_ARG, "bad op/dtype");
+  if (op < 0 || op > 4 || fmt < 0 || fmt > 1 || (op == 4 && fmt != kt::FMT_F32))
+    return fail(KT_ERR_ARG, "bad op/dtype");
   if (n == 0) return KT_OK;
   const size_t es = fmt == kt::FMT_BF16 ? 2 : 4;
   kt::LaunchInfo li;
@@ -290,6 +291,9 @@ KT_API kt_status ktanh_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut
 KT_API kt_status ktanh_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream) {
   return run_map(kt::OP_TANH, kt::FMT_F32, x, y, n, lut, stream);
 }
+KT_API kt_status ktanh_f32_via_bf16(const float *x, float *y, size_t n, kt_lut lut, void *stream) {
+  return run_map(kt::OP_TANH_VIA_BF16, kt::FMT_F32, x, y, n, lut, stream);
+}
 KT_API kt_status ksigmoid_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream) {
   return run_map(kt::OP_SIGMOID, kt::FMT_BF16, x, y, n, lut, stream);
 }
@@ -311,6 +315,7 @@ KT_API kt_status kgelu_f32(const float *x, float *y, size_t n, kt_lut lut, void 
 
 KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size_t n, kt_lut lut,
                           void *stream) {
+  if ((int)op < 0 || (int)op > 3) return fail(KT_ERR_ARG, "bad op %d", (int)op);
   return run_map((int)op, (int)dtype, x, y, n, lut, stream);
 }
 

@@ -303,8 +303,17 @@ __device__ __forceinline__ uint32_t apply_bf16x2(uint32_t x, const LaneLut &L) {
   return kgelu_bf16x2(x, L.w16);
 }
 
+// K-TanH of an F32 value through BF16 (the A8 alternative;
+// PAPER.md:256 "We assume BFloat16 input ... conversion cost is not
+// considered"): RNE to BF16 (F2FP), Alg. 1 on the BF16 bits, widen exactly.
+__device__ __forceinline__ uint32_t ktanh_f32_via_bf16(uint32_t u, uint32_t lw) {
+  const uint32_t b = pack_bf16x2(0.0f, __uint_as_float(u));     // low half = RN_bf16(x)
+  return ktanh_bf16x2(b, lw) << 16;
+}
+
 template <int OP>
 __device__ __forceinline__ uint32_t apply_f32(uint32_t u, const LaneLut &L) {
+  if (OP == OP_TANH_VIA_BF16) return ktanh_f32_via_bf16(u, L.w16);
   if (OP == OP_TANH) return ktanh_f32(u, L.k32, L.c32);
   if (OP == OP_SIGMOID) return ksigmoid_f32(u, L.k32, L.c32);
   if (OP == OP_SWISH) return kswish_f32(u, L.k32, L.c32);

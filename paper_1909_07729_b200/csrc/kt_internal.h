@@ -33,7 +33,8 @@ struct LutWords {
   uint32_t f32C[32];
 };
 
-enum Op { OP_TANH = 0, OP_SIGMOID = 1, OP_SWISH = 2, OP_GELU = 3 };
+enum Op { OP_TANH = 0, OP_SIGMOID = 1, OP_SWISH = 2, OP_GELU = 3,
+          OP_TANH_VIA_BF16 = 4 /* F32 only: RNE to BF16, Alg. 1, widen (NEXT-3) */ };
 enum Fmt { FMT_BF16 = 0, FMT_F32 = 1 };
 
 struct LaunchInfo {

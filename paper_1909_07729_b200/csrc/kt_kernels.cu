@@ -466,6 +466,7 @@ cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const 
   KT_CASE(OP_SIGMOID, FMT_F32)
   KT_CASE(OP_SWISH, FMT_F32)
   KT_CASE(OP_GELU, FMT_F32)
+  KT_CASE(OP_TANH_VIA_BF16, FMT_F32)
 #undef KT_CASE
   return cudaErrorInvalidValue;
 }

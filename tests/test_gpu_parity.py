@@ -133,6 +133,31 @@ def test_f32_patterns(kt, op):
     check(op, "f32", u32(y), O.map_f32(op, bits), f"{op} f32 patterns")
 
 
+def test_f32_via_bf16_patterns(kt):
+    """ktanh_f32_via_bf16 (NEXT-3): bit-exact vs the oracle (NaN by class) on
+    pattern classes around every BF16 rounding boundary (low 16 bits 0x7FFF,
+    0x8000, 0x8001: ties and their neighbours), random bits and specials."""
+    rng = np.random.default_rng(12)
+    hi = np.arange(1 << 16, dtype=np.uint64) << 16
+    bits = np.concatenate([
+        hi.astype(np.uint32), (hi | 0x7FFF).astype(np.uint32), (hi | 0x8000).astype(np.uint32),
+        (hi | 0x8001).astype(np.uint32),
+        rng.integers(0, 2**32, 1 << 20, dtype=np.uint64).astype(np.uint32),
+        np.array(WL.special_values_f32(), np.uint32)])
+    x = torch.from_numpy(bits.view(np.int32)).cuda().view(torch.float32)
+    y = kt.ktanh_f32_via_bf16(x)
+    assert_bitexact(u32(y), O.map_f32("tanh_via_bf16", bits), 32, nan_by_class=True,
+                    ctx="f32 via bf16")
+
+
+def test_f32_via_bf16_config3_sampled(kt):
+    x = WL.make_input("c3_f32_2p28", device="cuda")
+    y = kt.ktanh_f32_via_bf16(x)
+    idx = torch.from_numpy(np.random.default_rng(3).integers(0, x.numel(), 1 << 18)).cuda()
+    xs, ys = u32(x[idx]), u32(y[idx])
+    assert_bitexact(ys, O.map_f32("tanh_via_bf16", xs), 32, nan_by_class=True, ctx="c3 via bf16")
+
+
 # ------------------------------------------------------------ configs 2-5 ---
 def _bf16_table(op, lut=None):
     """Oracle output for every BF16 pattern (the BF16 map is a function of the

@@ -429,3 +429,50 @@ def test_64_entry_bounds_exhaustive_and_accuracy():
     assert not O.overflow_flag()
     assert s4["max_abs"] <= s3["max_abs"] <= 0.0167
     assert s4["max_rel"] <= s3["max_rel"]
+
+
+# --------------------------------------------------------------------------
+# K-TanH of F32 data through BF16
+# --------------------------------------------------------------------------
+def _f32_sample(seed=3, n=1 << 17):
+    rng = np.random.default_rng(seed)
+    x = np.concatenate([rng.uniform(-8, 8, n), rng.standard_normal(n) * 2,
+                        rng.uniform(-0.3, 0.3, n // 4)]).astype(np.float32)
+    return x
+
+
+def test_via_bf16_is_constant_on_rounding_cells():
+    """Brute force: every F32 in the rounding cell of a BF16 value b (the F32s
+    whose nearest-even BF16 is b) maps to the same output, and that output is
+    itself a BF16 value (low 16 bits zero)."""
+    rng = np.random.default_rng(11)
+    ws = rng.choice(np.flatnonzero(FINITE & (np.abs(XV) < 8)), 200, replace=False)
+    for w in ws:
+        b = int(W[w])
+        lo = (b << 16) - 0x7FFF if (b & 0x7FFF) else (b << 16)
+        cell = np.arange(max(lo, (b & 0x8000) << 16), (b << 16) + 0x8000, 97, dtype=np.int64)
+        u = cell.astype(np.uint32)
+        v = u.view(np.float32).astype(np.float64)
+        keep = np.array([O.bf16_encode_rne(t) == b for t in v])
+        y = O.map_f32("tanh_via_bf16", u[keep])
+        assert np.all(y == y[0]) and np.all((y & 0xFFFF) == 0)
+        assert (int(y[0]) >> 16) == int(O.map_bf16("tanh", np.array([b], np.uint16))[0])
+
+
+def test_via_bf16_error_bound_and_invariants():
+    """Within Table 2's bound plus the input rounding (|tanh'| <= 1, the BF16
+    rounding moves x by <= 2^-9 |x|); odd, within [-1, 1], NaN -> NaN."""
+    x = _f32_sample()
+    u = x.view(np.uint32)
+    y = O.map_f32("tanh_via_bf16", u).view(np.float32).astype(np.float64)
+    ref = np.tanh(x.astype(np.float64))
+    slack = np.minimum(np.abs(x), 4.0) * 2.0 ** -9 * (1 - np.tanh(np.minimum(np.abs(x), 4.0)) ** 2 + 1e-3)
+    assert np.all(np.abs(y - ref) <= 1.67e-2 + slack)
+    assert np.max(np.abs(y - ref)) <= 1.67e-2
+    yn = O.map_f32("tanh_via_bf16", u ^ np.uint32(0x80000000))
+    assert np.array_equal(yn, O.map_f32("tanh_via_bf16", u) ^ np.uint32(0x80000000))
+    assert np.all(np.abs(y) <= 1.0)
+    sp = np.array([np.nan, np.inf, -np.inf, 3.4e38, -3.4e38, 0.0, -0.0], np.float32).view(np.uint32)
+    ys = O.map_f32("tanh_via_bf16", sp)
+    assert (ys[0] & 0x7FFFFFFF) > 0x7F800000
+    assert list(ys[1:]) == [0x3F800000, 0xBF800000, 0x3F800000, 0xBF800000, 0, 0x80000000]
