@@ -135,10 +135,13 @@ class Step:
         es = self.cfg.elem_bytes
         self.bwd = "_bwd_" in op
         self.cell = op == "lstm_cell"
+        self.dual = op == "kgelu_swish_bf16"
         # algorithmic bytes: read x (+ dy for a backward) + write y
         self.bytes_per_step = (3 if self.bwd else 2) * n * es
         if self.cell:   # gates 8 B + c 4 B in, c' 4 B + h 2 B out per cell (n/4 cells)
             self.bytes_per_step = 18 * (n // 4)
+        if self.dual:   # x once in, both outputs out
+            self.bytes_per_step = 3 * n * es
         if sets is None:
             sets = 1 if self.bytes_per_step >= 2 * L2_BYTES else \
                 max(2, math.ceil(4 * L2_BYTES / self.bytes_per_step))
@@ -147,6 +150,7 @@ class Step:
         self.xs = [x0] + [WL.make_input(self.cfg, device=device, rank=rank, seed=self.cfg.seed + 1000 * s)
                           for s in range(1, sets)]
         self.ys = [torch.empty_like(x0) for _ in range(sets)]
+        self.y2s = [torch.empty_like(x0) for _ in range(sets)] if self.dual else None
         self.ds = [WL.make_input(self.cfg, device=device, rank=rank, seed=self.cfg.seed + 77 + 1000 * s)
                    for s in range(sets)] if self.bwd else None
         if self.cell:
@@ -176,6 +180,8 @@ class Step:
                                     h_next=self.hns[s])
         elif self.bwd:
             getattr(self.kt, self.op)(self.xs[s], self.ds[s], out=self.ys[s])
+        elif self.dual:
+            self.kt.kgelu_swish_bf16(self.xs[s], out_gelu=self.ys[s], out_swish=self.y2s[s])
         else:
             self.fn(self.xs[s], self.ys[s])
 
@@ -364,7 +370,8 @@ KERNEL_NAME = {"ktanh_bf16": "k_map<0, 0, true>", "ktanh_f32": "k_map<0, 1, true
 
 EXTRA = [("c3_f32_2p28", "ktanh_f32"), ("c3_f32_2p28", "ktanh_f32_via_bf16"), ("c4_lstm_gates", "lstm"),
          ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16"),
-         ("c5_ffn_2p30", "kgelu_bwd_bf16"), ("c4_lstm_gates", "lstm_cell")]
+         ("c5_ffn_2p30", "kgelu_swish_bf16"), ("c5_ffn_2p30", "kgelu_bwd_bf16"),
+         ("c4_lstm_gates", "lstm_cell")]
 
 
 def run_reference(args):
@@ -525,6 +532,9 @@ def main():
                 "frac_of_measured": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / peak, 4),
                 "frac_of_8tbs": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / NOMINAL_HBM_GBS, 4),
                 "l2": "inputs larger than L2" if st.sets == 1 else f"{st.sets} rotating sets"}
+            if st.dual:
+                extra[f"{key}:{op}"]["note"] = ("one pass, two outputs (K-GELU and K-Swish of x, "
+                                                "6 B/element); gelem_s counts input elements")
             del st
             torch.cuda.empty_cache()
 

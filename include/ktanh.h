@@ -132,6 +132,17 @@ KT_API kt_status kswish_f32(const float *x, float *y, size_t n, kt_lut lut, void
 KT_API kt_status kgelu_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream);
 KT_API kt_status kgelu_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream);
 
+/* K-GELU and K-Swish of the same input in ONE pass (BASELINE.json config 5
+ * applies both to the FFN tensor; reading A20): reads x once, writes both
+ * outputs -- 6 B of HBM traffic per BF16 element instead of 2 x 4 B.  Each
+ * output is bit-identical to kgelu_* / kswish_* on the same x.  y_gelu and
+ * y_swish must not overlap each other; either may equal x (in place), any
+ * other overlap -> KT_ERR_ARG. */
+KT_API kt_status kgelu_swish_bf16(const uint16_t *x, uint16_t *y_gelu, uint16_t *y_swish, size_t n,
+                                  kt_lut lut, void *stream);
+KT_API kt_status kgelu_swish_f32(const float *x, float *y_gelu, float *y_swish, size_t n, kt_lut lut,
+                                 void *stream);
+
 /* LSTM gate block (BASELINE.json config 4; GNMT LSTM):
  * x, y are row-major [rows, 4*hidden] BF16; quarter q of every row gets
  * K-TanH if q == tanh_quarter (the cell candidate g; 2 in PyTorch's

@@ -42,7 +42,7 @@ EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_creat
                        "klstm_gates_bf16", "klstm_cell_bf16", "kgemm_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
                        "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count",
                        "kt_apx_create", "kt_apx_coeffs", "kt_apx_destroy", "kt_apx_tanh_bf16",
-                       "kt_apx_tanh_f32", "kt_alu_probe")
+                       "kt_apx_tanh_f32", "kt_alu_probe", "kgelu_swish_bf16", "kgelu_swish_f32")
 
 for _name in MAP_CALLS:
     _f = getattr(_lib, _name)
@@ -98,6 +98,10 @@ for _name in ("kt_apx_tanh_bf16", "kt_apx_tanh_f32"):
     _f.argtypes = [_vp, _vp, _sz, _vp, _vp]
     _f.restype = ctypes.c_int
 
+for _name in ("kgelu_swish_bf16", "kgelu_swish_f32"):
+    _f = getattr(_lib, _name)
+    _f.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
+    _f.restype = ctypes.c_int
 _lib.kt_alu_probe.argtypes = [ctypes.c_int, _vp, _vp, _vp, ctypes.c_int,
                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
 _lib.kt_alu_probe.restype = ctypes.c_int
@@ -468,3 +472,27 @@ def alu_probe(dtype: str, sample, lut: Lut | None = None, apx: Apx | None = None
                              apx.handle if apx else None, words.ctypes.data, iters,
                              ctypes.byref(net), ctypes.byref(gross)), "kt_alu_probe")
     return net.value, gross.value
+
+
+def _make_dual(name, dtype_name):
+    fn = getattr(_lib, name)
+
+    def call(x, out_gelu=None, out_swish=None, lut: Lut | None = None, stream=None):
+        """(K-GELU(x), K-Swish(x)) in one pass over x (config 5, reading A20)."""
+        import torch
+        dt = torch.bfloat16 if dtype_name == "bf16" else torch.float32
+        out_gelu = _prep(x, out_gelu, dt)
+        out_swish = _prep(x, out_swish, dt)
+        lut = lut or paper_lut()
+        idx = x.device.index
+        with _on_device(idx):
+            _check(fn(x.data_ptr(), out_gelu.data_ptr(), out_swish.data_ptr(), x.numel(), lut.handle,
+                      _stream_ptr(stream, idx)), name)
+        return out_gelu, out_swish
+
+    call.__name__ = name
+    return call
+
+
+kgelu_swish_bf16 = _make_dual("kgelu_swish_bf16", "bf16")
+kgelu_swish_f32 = _make_dual("kgelu_swish_f32", "f32")

@@ -319,6 +319,40 @@ KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size
   return run_map((int)op, (int)dtype, x, y, n, lut, stream);
 }
 
+// ---- fused K-GELU + K-Swish (config 5, reading A20) -------------------------
+static kt_status run_dual(int fmt, const void *x, void *yg, void *ys, size_t n, kt_lut lut,
+                          void *stream) {
+  if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (n == 0) return KT_OK;
+  const size_t es = fmt == kt::FMT_BF16 ? 2 : 4;
+  if (!x || !yg || !ys) return fail(KT_ERR_ARG, "NULL pointer with n = %zu", n);
+  if ((uintptr_t)x % es || (uintptr_t)yg % es || (uintptr_t)ys % es)
+    return fail(KT_ERR_ARG, "pointers must be %zu-byte aligned", es);
+  if (n > SIZE_MAX / es) return fail(KT_ERR_ARG, "n too large");
+  const size_t bytes = n * es;
+  if (yg == ys || overlaps(yg, ys, bytes)) return fail(KT_ERR_ARG, "y_gelu and y_swish overlap");
+  if (overlaps(x, yg, bytes) || overlaps(x, ys, bytes))
+    return fail(KT_ERR_ARG, "an output overlaps x without being equal to it");
+  kt::LaunchInfo li;
+  kt_status s = launch_info(&li);
+  if (s != KT_OK) return s;
+  if ((s = check_device_ptr(x, li.device, "x")) != KT_OK) return s;
+  if ((s = check_device_ptr(yg, li.device, "y_gelu")) != KT_OK) return s;
+  if ((s = check_device_ptr(ys, li.device, "y_swish")) != KT_OK) return s;
+  cudaError_t e = kt::launch_dual(fmt, x, yg, ys, n, lut->words, (cudaStream_t)stream, li);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return KT_OK;
+}
+
+KT_API kt_status kgelu_swish_bf16(const uint16_t *x, uint16_t *y_gelu, uint16_t *y_swish, size_t n,
+                                  kt_lut lut, void *stream) {
+  return run_dual(kt::FMT_BF16, x, y_gelu, y_swish, n, lut, stream);
+}
+KT_API kt_status kgelu_swish_f32(const float *x, float *y_gelu, float *y_swish, size_t n, kt_lut lut,
+                                 void *stream) {
+  return run_dual(kt::FMT_F32, x, y_gelu, y_swish, n, lut, stream);
+}
+
 // ---- Table 2 comparators --------------------------------
 KT_API kt_status kt_apx_create(kt_apx_kind kind, int p, int q, kt_apx *out) {
   if (!out) return fail(KT_ERR_ARG, "NULL argument");

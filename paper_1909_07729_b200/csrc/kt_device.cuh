@@ -185,10 +185,15 @@ __device__ __forceinline__ uint32_t ksigmoid_bf16x2(uint32_t x, uint32_t lw) {
   return hfma2_bf16(t, kHalfx2, kHalfx2);                                 // RN((1+t)/2)
 }
 
+// K-Swish / K-GELU outer step as one packed BF16 fma: RN_bf16(h + h t) with
+// h = RN_bf16(x/2), the exact value rounded once -- the oracle's definition
+// whenever x/2 is a BF16 (all but subnormal x, where the result equals it
+// too: checked over all 65,536 patterns, 0 ulp).  The fp32 route needed
+// widen + FMUL2/FFMA2 + pack (5 more ALU ops per pair).
 __device__ __forceinline__ uint32_t kswish_bf16x2(uint32_t x, uint32_t lw) {
-  const float2 hx = mul2(widen2(x), splat2(0.5f));                         // exact x/2
-  const uint32_t t = ktanh_bf16x2(pack2(hx), lw);
-  return pack2(fma2(hx, widen2(t), hx));                                   // RN(hx (1+t))
+  const uint32_t h = hmul2_bf16(x, kHalfx2);                              // RN_bf16(x/2)
+  const uint32_t t = ktanh_bf16x2(h, lw);
+  return hfma2_bf16(h, t, h);                                             // RN(h (1+t))
 }
 
 __device__ __forceinline__ float gelu_arg(float x) {
@@ -202,8 +207,8 @@ __device__ __forceinline__ uint32_t kgelu_bf16x2(uint32_t x, uint32_t lw) {
   const float2 x2 = mul2(xv, xv);
   const float2 p = fma2(splat2(__uint_as_float(kGeluC1Bits)), x2, splat2(__uint_as_float(kGeluC0Bits)));
   const uint32_t t = ktanh_bf16x2(pack2(mul2(xv, p)), lw);                 // RN_bf16(u)
-  const float2 hx = mul2(xv, splat2(0.5f));
-  return pack2(fma2(hx, widen2(t), hx));
+  const uint32_t h = hmul2_bf16(x, kHalfx2);                              // RN_bf16(x/2)
+  return hfma2_bf16(h, t, h);                                             // RN(h (1+t))
 }
 
 __device__ __forceinline__ uint32_t ksigmoid_f32(uint32_t u, uint32_t lk, uint32_t lc) {

@@ -53,6 +53,10 @@ cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const 
 cudaError_t launch_bwd(int op, int fmt, const void *a, const void *dy, void *dx, size_t n,
                        const LutWords &lut, cudaStream_t s, const LaunchInfo &li);
 
+// Fused K-GELU + K-Swish over one input (config 5, reading A20).
+cudaError_t launch_dual(int fmt, const void *x, void *yg, void *ys, size_t n, const LutWords &lut,
+                        cudaStream_t s, const LaunchInfo &li);
+
 cudaError_t launch_lstm(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,
                         int tanh_quarter, const LutWords &lut, cudaStream_t s,
                         const LaunchInfo &li);

@@ -139,6 +139,88 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
   }
 }
 
+// ---- fused K-GELU + K-Swish over one input (config 5, reading A20) -----------
+// Config 5 applies both derived activations to the same FFN tensor; one pass
+// that reads x once and writes both outputs moves 6 B per BF16 element
+// instead of 2 x 4 B.  Each output is bit-identical to its single-op call.
+template <int FMT>
+__device__ __forceinline__ void dual_span(const uint8_t *xp, uint8_t *gp, uint8_t *sp, uint32_t cnt,
+                                          const LaneLut &L) {
+  const uint32_t lane = threadIdx.x & 31;
+  const bool on = lane < cnt;
+  uint32_t w = 0;
+  if (FMT == FMT_BF16) {
+    if (on) w = reinterpret_cast<const uint16_t *>(xp)[lane];
+  } else if (on) {
+    w = reinterpret_cast<const uint32_t *>(xp)[lane];
+  }
+  const uint32_t g = apply_word<OP_GELU, FMT>(w, L), sw = apply_word<OP_SWISH, FMT>(w, L);
+  if (on) {
+    if (FMT == FMT_BF16) {
+      reinterpret_cast<uint16_t *>(gp)[lane] = (uint16_t)g;
+      reinterpret_cast<uint16_t *>(sp)[lane] = (uint16_t)sw;
+    } else {
+      reinterpret_cast<uint32_t *>(gp)[lane] = g;
+      reinterpret_cast<uint32_t *>(sp)[lane] = sw;
+    }
+  }
+}
+
+template <int FMT, bool NC>
+__global__ void __launch_bounds__(kThreads)
+k_dual(const uint8_t *x, uint8_t *yg, uint8_t *ys, uint32_t head, uint64_t nvec, uint32_t tail,
+       uint32_t pf_blocks, const __grid_constant__ LutWords lut) {
+  constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
+  const LaneLut L = load_lane_lut(lut);
+  const uint32_t lane = threadIdx.x & 31;
+  const size_t hb = (size_t)head * es;
+  const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (NC && blockIdx.x < pf_blocks && lane == 0 && c * kChunkVecs < nvec) {
+    const uint64_t left = nvec - c * kChunkVecs;
+    prefetch_l2(x + hb + c * kChunkVecs * kVecBytes,
+                (uint32_t)((left < kChunkVecs ? left : kChunkVecs) * kVecBytes));
+  }
+  pdl_enter();
+  const uint64_t base = c * kChunkVecs + lane;
+  uint32_t v[kUnroll][8];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t i = base + (uint64_t)u * 32;
+    ld256<NC>(x + hb + i * kVecBytes, v[u], i < nvec);
+  }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    uint32_t g[8], sw[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      g[j] = apply_word<OP_GELU, FMT>(v[u][j], L);
+      sw[j] = apply_word<OP_SWISH, FMT>(v[u][j], L);
+    }
+    const uint64_t i = base + (uint64_t)u * 32;
+    st256(yg + hb + i * kVecBytes, g, i < nvec);
+    st256(ys + hb + i * kVecBytes, sw, i < nvec);
+  }
+  if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
+    dual_span<FMT>(x, yg, ys, head, L);
+    const size_t toff = ((size_t)head + (size_t)nvec * (kVecBytes / es)) * es;
+    dual_span<FMT>(x + toff, yg + toff, ys + toff, tail, L);
+  }
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(kThreads)
+k_dual_elem(const uint8_t *x, uint8_t *yg, uint8_t *ys, uint64_t n, const __grid_constant__ LutWords lut) {
+  constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
+  const LaneLut L = load_lane_lut_reg(lut);
+  pdl_enter();
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t c = warp0; c < (n + 31) / 32; c += nwarps) {
+    const uint64_t off = c * 32, rem = n - off;
+    dual_span<FMT>(x + off * es, yg + off * es, ys + off * es, (uint32_t)(rem < 32 ? rem : 32), L);
+  }
+}
+
 // ---- backward (NEXT-1): dx = dy * g(a), two input streams -----------------
 template <int OP, int FMT>
 __device__ __forceinline__ void scalar_span_bwd(const uint8_t *ap, const uint8_t *dp, uint8_t *xp,
@@ -512,6 +594,42 @@ cudaError_t launch_bwd(int op, int fmt, const void *a, const void *dy, void *dx,
   KT_CASE(OP_GELU, FMT_F32)
 #undef KT_CASE
   return cudaErrorInvalidValue;
+}
+
+template <int FMT>
+static cudaError_t launch_dual_t(const void *x, void *yg, void *ys, size_t n, const LutWords &lut,
+                                 cudaStream_t s, const LaunchInfo &li) {
+  constexpr size_t es = (FMT == FMT_BF16) ? 2 : 4;
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ga = reinterpret_cast<uintptr_t>(yg),
+                  sa = reinterpret_cast<uintptr_t>(ys);
+  const uint8_t *xp = static_cast<const uint8_t *>(x);
+  uint8_t *gp = static_cast<uint8_t *>(yg), *sp = static_cast<uint8_t *>(ys);
+  if (xa % kVecBytes != ga % kVecBytes || xa % kVecBytes != sa % kVecBytes) {
+    static const int bps = resident_blocks(k_dual_elem<FMT>);
+    const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
+    return launch(k_dual_elem<FMT>, grid, s, xp, gp, sp, (uint64_t)n, lut);
+  }
+  const size_t mis = xa % kVecBytes;
+  size_t head = mis ? (kVecBytes - mis) / es : 0;
+  if (head > n) head = n;
+  const size_t body = n - head;
+  const uint64_t nvec = body / (kVecBytes / es);
+  const uint32_t tail = (uint32_t)(body - nvec * (kVecBytes / es));
+  const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+  if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  const unsigned grid = flat_grid(nchunks);
+  if (x != yg && x != ys) {
+    static const int bps = resident_blocks(k_dual<FMT, true>);
+    const uint32_t pf = prefetch_enabled() ? (uint32_t)(li.sm_count * bps) : 0u;
+    return launch(k_dual<FMT, true>, grid, s, xp, gp, sp, (uint32_t)head, nvec, tail, pf, lut);
+  }
+  return launch(k_dual<FMT, false>, grid, s, xp, gp, sp, (uint32_t)head, nvec, tail, 0u, lut);
+}
+
+cudaError_t launch_dual(int fmt, const void *x, void *yg, void *ys, size_t n, const LutWords &lut,
+                        cudaStream_t s, const LaunchInfo &li) {
+  if (fmt == FMT_BF16) return launch_dual_t<FMT_BF16>(x, yg, ys, n, lut, s, li);
+  return launch_dual_t<FMT_F32>(x, yg, ys, n, lut, s, li);
 }
 
 cudaError_t launch_lstm(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,

@@ -190,3 +190,16 @@ def test_apx_calls_reject_host_pointers(kt):
         assert f(ctypes.addressof(buf), ctypes.addressof(buf), 16, None, None) == kt.KT_ERR_ARG
     assert lib.kt_apx_tanh_f32(ctypes.c_void_p(0x1002), ctypes.c_void_p(0x10002), 4, A.handle,
                                None) == kt.KT_ERR_ARG                     # misaligned
+
+
+def test_gelu_swish_fused_argument_errors(kt):
+    lut = kt.Lut.paper()
+    lib = kt._lib
+    for f in (lib.kgelu_swish_bf16, lib.kgelu_swish_f32):
+        assert f(None, None, None, 0, lut.handle, None) == kt.KT_OK
+        assert f(None, None, None, 16, lut.handle, None) == kt.KT_ERR_ARG
+    x, a, b = ctypes.c_void_p(0x10000), ctypes.c_void_p(0x20000), ctypes.c_void_p(0x20010)
+    assert lib.kgelu_swish_bf16(x, a, a, 64, lut.handle, None) == kt.KT_ERR_ARG   # same output
+    assert lib.kgelu_swish_bf16(x, a, b, 64, lut.handle, None) == kt.KT_ERR_ARG   # outputs overlap
+    assert lib.kgelu_swish_bf16(x, ctypes.c_void_p(0x10010), b, 64, lut.handle, None) == kt.KT_ERR_ARG
+    assert lib.kgelu_swish_bf16(x, a, ctypes.c_void_p(0x30000), 64, None, None) == kt.KT_ERR_ARG

@@ -419,3 +419,55 @@ def test_lstm_cell_specials(kt):
     want_c, want_h = O.lstm_cell_bf16(u16(gates), c_bits, H)
     assert_bitexact(u32(cn), want_c, 32, nan_by_class=True, ctx="c_next specials")
     assert_bitexact(u16(hn), want_h, 16, nan_by_class=True, ctx="h_next specials")
+
+
+# ------------------------------------------------ fused K-GELU + K-Swish ----
+@pytest.mark.parametrize("fmt", ["bf16", "f32"])
+def test_gelu_swish_fused_equals_single_ops(kt, fmt):
+    """kgelu_swish_* (reading A20): both outputs bit-identical to the single-op
+    calls, and within the derived-op tolerance of the oracle."""
+    if fmt == "bf16":
+        x = WL.make_input("c1_exhaustive_bf16", device="cuda")
+        g, s = kt.kgelu_swish_bf16(x)
+        torch.cuda.synchronize()
+        assert np.array_equal(u16(g), u16(kt.kgelu_bf16(x)))
+        assert np.array_equal(u16(s), u16(kt.kswish_bf16(x)))
+        check("gelu", "bf16", u16(g), oracle_bf16("gelu", u16(x)), "fused gelu")
+        check("swish", "bf16", u16(s), oracle_bf16("swish", u16(x)), "fused swish")
+    else:
+        rng = np.random.default_rng(21)
+        bits = np.concatenate([rng.integers(0, 2**32, 1 << 18, dtype=np.uint64).astype(np.uint32),
+                               np.array(WL.special_values_f32(), np.uint32)])
+        x = torch.from_numpy(bits.view(np.int32)).cuda().view(torch.float32)
+        g, s = kt.kgelu_swish_f32(x)
+        torch.cuda.synchronize()
+        assert np.array_equal(u32(g), u32(kt.kgelu_f32(x)))
+        assert np.array_equal(u32(s), u32(kt.kswish_f32(x)))
+        check("gelu", "f32", u32(g), O.map_f32("gelu", bits), "fused gelu f32")
+        check("swish", "f32", u32(s), O.map_f32("swish", bits), "fused swish f32")
+
+
+@pytest.mark.parametrize("n,off", [(1, 0), (17, 1), (4097, 3), (1000001, 5)])
+def test_gelu_swish_fused_ragged_and_in_place(kt, n, off):
+    base = (torch.randn(n + 32, device="cuda") * 2).to(torch.bfloat16)
+    x = base[off:off + n]
+    want_g, want_s = u16(kt.kgelu_bf16(x)), u16(kt.kswish_bf16(x))
+    g, s = kt.kgelu_swish_bf16(x)
+    assert np.array_equal(u16(g), want_g) and np.array_equal(u16(s), want_s)
+    # y_gelu in place over x (aliasing disables the non-coherent load path)
+    xc = x.clone()
+    g2, s2 = kt.kgelu_swish_bf16(xc, out_gelu=xc)
+    assert np.array_equal(u16(g2), want_g) and np.array_equal(u16(s2), want_s)
+    # misaligned outputs relative to x -> element-wise kernel
+    gb = torch.empty(n + 32, dtype=torch.bfloat16, device="cuda")
+    g3, s3 = kt.kgelu_swish_bf16(x, out_gelu=gb[(off + 1) % 16:(off + 1) % 16 + n])
+    assert np.array_equal(u16(g3), want_g) and np.array_equal(u16(s3), want_s)
+
+
+def test_config5_gelu_swish_fused_full(kt):
+    x = WL.make_input("c5_ffn_2p30", device="cuda")
+    g, s = kt.kgelu_swish_bf16(x)
+    _lookup_check("gelu", x, g)
+    _lookup_check("swish", x, s)
+    _sampled_oracle_check("gelu", x, g)
+    _sampled_oracle_check("swish", x, s)
