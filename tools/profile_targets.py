@@ -48,6 +48,25 @@ def tanh_bf16_steady():
     print("tanh_bf16_steady ok", flush=True)
 
 
+def gelu_swish():
+    x = WL.make_input("c5_ffn_2p30", device="cuda")
+    g, sw = torch.empty_like(x), torch.empty_like(x)
+    for _ in range(4):
+        kt.kgelu_swish_bf16(x, out_gelu=g, out_swish=sw)
+    torch.cuda.synchronize()
+    print("gelu_swish ok", flush=True)
+
+
+def apx_minimax3():
+    x = WL.make_input("c2_bf16_2p24", device="cuda")
+    y = torch.empty_like(x)
+    A = kt.Apx("minimax", 3)
+    for _ in range(4):
+        kt.kt_apx_tanh_bf16(x, A, out=y)
+    torch.cuda.synchronize()
+    print("apx_minimax3 ok", flush=True)
+
+
 def lstm_cell():
     x = WL.make_input("c4_lstm_gates", device="cuda")
     c = torch.randn(x.numel() // (4 * WL.LSTM_HIDDEN), WL.LSTM_HIDDEN, device="cuda")
@@ -59,7 +78,7 @@ def lstm_cell():
 if __name__ == "__main__":
     names = sys.argv[1:] or list(TARGETS) + ["gemm_gelu", "lstm_cell"]
     for name in names:
-        if name in ("gemm_gelu", "lstm_cell", "tanh_bf16_steady"):
+        if name in ("gemm_gelu", "lstm_cell", "tanh_bf16_steady", "gelu_swish", "apx_minimax3"):
             globals()[name]()
             continue
         key, fn = TARGETS[name]
