@@ -356,9 +356,27 @@ k_lstm(const uint8_t *x, uint8_t *y, uint32_t nvec, uint32_t vpr, uint32_t vpq, 
 // gates + 64 B of c in, 64 B of c' + 32 B of h out (18 B per cell).
 __global__ void __launch_bounds__(kThreads)
 k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_t *h_next,
-            uint32_t nvec, uint32_t vpr, uint32_t hidden, const __grid_constant__ LutWords lut) {
+            uint32_t nvec, uint32_t vpr, uint32_t hidden, uint32_t pf_stride,
+            const __grid_constant__ LutWords lut) {
   const LaneLut L = load_lane_lut(lut);
   pdl_enter();
+  // Optional L2 prefetch of the NEXT wave's data (KT_CELL_PF=k: the
+  // counterpart warp k resident waves later).  Measured slower on config 4
+  // (26.3 vs 20.8 us: the prefetched lines compete with the current wave's
+  // reads and writes in L2), so off by default.
+  if (pf_stride != 0 && (threadIdx.x & 31) < 5) {
+    const uint32_t v2 = ((blockIdx.x + pf_stride) * kWarps + (threadIdx.x >> 5)) * 32;
+    if (v2 < nvec) {
+      const uint32_t row2 = v2 / vpr, j2 = v2 - row2 * vpr;
+      const uint32_t cnt = min(min(32u, nvec - v2), vpr - j2);
+      const uint32_t q = threadIdx.x & 31;
+      if (q < 4)
+        prefetch_l2(gates + ((size_t)row2 * 4 * hidden + (size_t)j2 * 16) * 2 + (size_t)q * hidden * 2,
+                    cnt * 32);
+      else
+        prefetch_l2(c_prev + ((size_t)row2 * hidden + (size_t)j2 * 16) * 4, cnt * 64);
+    }
+  }
   const uint32_t v = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32 + (threadIdx.x & 31);
   const bool on = v < nvec;
   const uint32_t row = on ? v / vpr : 0, j16 = on ? v - row * vpr : 0;
@@ -671,10 +689,16 @@ cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *
   if (aligned && hidden % 16 == 0 && nvec < (1ull << 31)) {
     const uint64_t nwarps = (nvec + 31) / 32;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, (nwarps + kWarps - 1) / kWarps);
+    static const int bps = resident_blocks(k_lstm_cell);
+    static const int pf_on = [] {
+      const char *e = getenv("KT_CELL_PF");
+      return e ? atoi(e) : 0;
+    }();
+    const uint32_t pf_stride = pf_on > 0 ? (uint32_t)(li.sm_count * bps * pf_on) : 0u;
     return launch(k_lstm_cell, grid, s, reinterpret_cast<const uint8_t *>(gates),
                   reinterpret_cast<const uint8_t *>(c_prev), reinterpret_cast<uint8_t *>(c_next),
                   reinterpret_cast<uint8_t *>(h_next), (uint32_t)nvec, (uint32_t)(hidden / 16),
-                  (uint32_t)hidden, lut);
+                  (uint32_t)hidden, pf_stride, lut);
   }
   static const int bps = resident_blocks(k_lstm_cell_elem);
   const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
