@@ -316,6 +316,14 @@ bool apx_pipelined(int kind, int fmt) {
   return kind == APX_MINIMAX || kind == APX_TAYLOR;   // 4 shuffles + Horner per element
 }
 
+template <class K>
+int occupancy(K kernel) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1)
+    b = 1;
+  return b;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kernel)(KArgs...), unsigned grid, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -355,12 +363,16 @@ cudaError_t launch_apx_t(const void *x, void *y, size_t n, const ApxWords &w, cu
   if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, (nchunks + kWarps - 1) / kWarps);
   if (apx_pipelined(w.kind, FMT)) {
-    auto k = (x != y) ? k_apx_pipe<KIND, A, B, FMT, true> : k_apx_pipe<KIND, A, B, FMT, false>;
-    static int bps = 0;
-    if (bps == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, kThreads, 0) != cudaSuccess || bps < 1))
-      bps = 1;
+    if (x != y) {
+      static const int bps = occupancy(k_apx_pipe<KIND, A, B, FMT, true>);   // thread-safe init
+      const unsigned pgrid = std::min<unsigned>(grid, (unsigned)(li.sm_count * bps));
+      return launch_k(k_apx_pipe<KIND, A, B, FMT, true>, pgrid, s, xp, yp, (uint32_t)head, nvec,
+                      tail, w);
+    }
+    static const int bps = occupancy(k_apx_pipe<KIND, A, B, FMT, false>);
     const unsigned pgrid = std::min<unsigned>(grid, (unsigned)(li.sm_count * bps));
-    return launch_k(k, pgrid, s, xp, yp, (uint32_t)head, nvec, tail, w);
+    return launch_k(k_apx_pipe<KIND, A, B, FMT, false>, pgrid, s, xp, yp, (uint32_t)head, nvec, tail,
+                    w);
   }
   if (x != y) {
     const uint32_t pf = prefetch_enabled() ? (uint32_t)li.sm_count * 8u : 0u;   // 8 CTAs/SM resident

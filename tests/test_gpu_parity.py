@@ -471,3 +471,40 @@ def test_config5_gelu_swish_fused_full(kt):
     _lookup_check("swish", x, s)
     _sampled_oracle_check("gelu", x, g)
     _sampled_oracle_check("swish", x, s)
+
+
+def test_concurrent_host_threads(kt):
+    """Thread safety (include/ktanh.h: handles are immutable, calls are safe
+    from any host thread on any stream): 8 threads, each on its own stream
+    and tensors, interleave K-TanH, K-GELU, the fused pass and a comparator;
+    every result equals the single-threaded one."""
+    import threading
+    xs = [(torch.randn(1 << 20, device="cuda") * 2 + 0.1 * k).to(torch.bfloat16) for k in range(8)]
+    apx = kt.Apx("minimax", 3)
+    want = [(u16(kt.ktanh_bf16(x)), u16(kt.kgelu_bf16(x)), u16(kt.kt_apx_tanh_bf16(x, apx))) for x in xs]
+    torch.cuda.synchronize()
+    errors = []
+
+    def worker(k):
+        try:
+            s = torch.cuda.Stream()
+            x = xs[k]
+            with torch.cuda.stream(s):
+                for _ in range(20):
+                    t = kt.ktanh_bf16(x, stream=s)
+                    g, _sw = kt.kgelu_swish_bf16(x, stream=s)
+                    a = kt.kt_apx_tanh_bf16(x, apx, stream=s)
+            s.synchronize()
+            got = (u16(t), u16(g), u16(a))
+            for gg, ww in zip(got, want[k]):
+                if not np.array_equal(gg, ww):
+                    errors.append(k)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
