@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -256,6 +257,207 @@ k_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtens
   }
 }
 
+// ------------------------------------------------ CTA-pair (cta_group::2) ----
+// Two CTAs of a cluster (two SMs of one TPC) compute one 256 x 256 output
+// tile: CTA r loads rows [r*128, +128) of the A block and rows [r*128, +128)
+// of the B panel (its half of N); the leader (rank 0) issues
+// tcgen05.mma.cta_group::2 M=256 N=256 K=16, which reads both CTAs' shared
+// memory and accumulates rows r*128.. into CTA r's TMEM.  Per CTA and K block
+// that is 32 KiB of operands instead of 48 KiB for the same 128 x 256 output,
+// so 6 pipeline stages fit.  Barrier protocol:
+//   full[s]   leader only: 1 arrival (leader's expect_tx of both CTAs' bytes);
+//             both CTAs' TMA loads complete_tx on it (.cta_group::2 TMA)
+//   empty[s]  both CTAs: the leader's tcgen05.commit multicasts to both
+//   tfull[a]  both CTAs: commit multicast after the last K block of a tile
+//   tempty[a] leader only: 2 x 8 epilogue-warp arrivals (the peer's remote)
+constexpr int k2Stages = 6;
+constexpr uint32_t k2HalfBytes = 128 * kBK * 2;                // 16 KiB
+constexpr uint32_t k2StageBytes = 2 * k2HalfBytes;             // A half + B half
+constexpr size_t k2Smem = (size_t)k2Stages * k2StageBytes + 1024 + 256;
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) |
+                             ((256u >> 4) << 24);
+static_assert(8 * 2 * k2Stages + 8 * 4 + 8 <= 256, "barrier area");
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank0(uint32_t a) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(d) : "r"(a));
+  return d;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                                 uint32_t mbar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(mbar_cluster)
+      : "memory");
+}
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmPThreads, 1)
+k_gemm2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+        uint16_t *C, uint32_t M, uint32_t N, uint32_t K, const __grid_constant__ LutWords lut) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bar = base + k2Stages * k2StageBytes;
+  const uint32_t full_bar = bar, empty_bar = bar + 8 * k2Stages;
+  const uint32_t tfull_bar = bar + 16 * k2Stages, tempty_bar = tfull_bar + 16;
+  const uint32_t tmem_slot = tempty_bar + 16;
+  uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem_raw + (tmem_slot - raw));
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t mt = M / 256, ntn = N / 256, ntiles = mt * ntn;
+  const uint32_t nk = K / kBK;
+  const uint32_t lw = lut.bf16[lane];
+
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < k2Stages; ++s) {
+      mbar_init(full_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar + 8 * a, 1);
+      mbar_init(tempty_bar + 8 * a, 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "n"(2 * kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();   // barriers of both CTAs initialised before any remote use
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    uint32_t it = 0;
+    for (uint32_t t = cid; t < ntiles; t += ncl) {
+      uint32_t mb, nb;
+      tile_coords(t, mt, ntn, mb, nb);
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % k2Stages;
+        if (it >= (uint32_t)k2Stages) mbar_wait(empty_bar + 8 * s, ((it / k2Stages) + 1) & 1);
+        const uint32_t sa = base + s * k2StageBytes, sb = sa + k2HalfBytes;
+        const uint32_t fb = map_to_rank0(full_bar + 8 * s);
+        if (leader) mbar_expect_tx(full_bar + 8 * s, 2 * k2StageBytes);
+        tma_load_2d_pair(sa, &map_a, (int)(kb * kBK), (int)(mb * 256 + rank * 128), fb);
+        tma_load_2d_pair(sb, &map_b, (int)(kb * kBK), (int)(nb * 256 + rank * 128), fb);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (leader only) ----------------
+    uint32_t it = 0, i = 0;
+    for (uint32_t t = cid; t < ntiles; t += ncl, ++i) {
+      const uint32_t a = i & 1;
+      if (i >= 2) mbar_wait(tempty_bar + 8 * a, ((i / 2) + 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t d = tmem + a * kTmemCols;
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % k2Stages;
+        mbar_wait(full_bar + 8 * s, (it / k2Stages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = umma_sdesc(base + s * k2StageBytes);
+        const uint64_t db = umma_sdesc(base + s * k2StageBytes + k2HalfBytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          const uint32_t acc = (kb | k) != 0;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc2), "r"(acc));
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+            " [%0], %1;" ::"r"(empty_bar + 8 * s), "h"((uint16_t)3)
+            : "memory");
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+          " [%0], %1;" ::"r"(tfull_bar + 8 * a), "h"((uint16_t)3)
+          : "memory");
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue (8 warps, both CTAs) ----------------
+    const uint32_t q = warp & 3, half = (warp - 2) >> 2;
+    const uint32_t tempty_leader = map_to_rank0(tempty_bar);
+    uint32_t i = 0;
+    for (uint32_t t = cid; t < ntiles; t += ncl, ++i) {
+      uint32_t mb, nb;
+      tile_coords(t, mt, ntn, mb, nb);
+      const uint32_t a = i & 1;
+      mbar_wait(tfull_bar + 8 * a, (i / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t row = mb * 256 + rank * 128 + 32 * q + lane;
+      uint16_t *crow = C + (size_t)row * N + nb * 256 + half * 128;
+#pragma unroll 1
+      for (uint32_t c = 0; c < 128; c += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((32 * q) << 16) + a * kTmemCols + half * 128 + c;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+              "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == 96) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          // Relaxed: the TMEM reads are complete (wait::ld) and fenced by
+          // tcgen05.fence::before_thread_sync; a .release.cluster arrive
+          // would add a GPU-scope MEMBAR that waits for this warp's
+          // outstanding C stores (measured: it stalls the epilogue).
+          if (lane == 0) {
+            if (leader)
+              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar + 8 * a)
+                           : "memory");
+            else
+              asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                               tempty_leader + 8 * a)
+                           : "memory");
+          }
+        }
+        uint32_t o0[8], o1[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);
+          o1[j] = epi_word<EPI>(
+              pack_bf16x2(__uint_as_float(r[2 * j + 17]), __uint_as_float(r[2 * j + 16])), lw);
+        }
+        st256(crow + c, o0, true);
+        st256(crow + c + 16, o1, true);
+      }
+    }
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();   // both CTAs done with TMEM and with each other's barriers
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(2 * kTmemCols));
+  }
+}
+
 // ---------------------------------------------------------------- host ----
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -307,9 +509,54 @@ static cudaError_t launch_gemm_t(const CUtensorMap &ma, const CUtensorMap &mb, u
   return cudaGetLastError();
 }
 
+template <int EPI>
+static cudaError_t launch_gemm2_t(const CUtensorMap &ma, const CUtensorMap &mb, uint16_t *C, size_t M,
+                                  size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k_gemm2<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)k2Smem);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const size_t tiles = (M / 256) * (N / 256);
+  const size_t pairs = (size_t)(sms / 2);
+  const unsigned grid = (unsigned)(2 * (tiles < pairs ? tiles : pairs));
+  k_gemm2<EPI><<<grid, kGemmPThreads, k2Smem, s>>>(ma, mb, C, (uint32_t)M, (uint32_t)N, (uint32_t)K,
+                                                   lut);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Kernel choice (profiles/gemm_2cta_r01.txt): the CTA pair is faster for the
+// plain GEMM (1.44 vs 1.51 ms at 16384^2 x 4096; 0.40 vs 0.47 ms at
+// 65536 x 4096 x 1024), but with an activation epilogue the 1-CTA kernel is
+// as fast or faster on the FFN shapes (the epilogue no longer hides behind
+// the shorter pair mainloop).  KT_GEMM_2CTA=0/1 forces either for M % 256 == 0.
+static bool use_pair(size_t M, int epi) {
+  static const int force = [] {
+    const char *e = getenv("KT_GEMM_2CTA");
+    return e ? atoi(e) : -1;
+  }();
+  if (M % 256 != 0) return false;
+  if (force >= 0) return force != 0;
+  return epi < 0;
+}
+
 cudaError_t launch_gemm(int epi, const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M,
                         size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms) {
   CUtensorMap ma, mb;
+  if (use_pair(M, epi) && sms >= 2) {
+    if (!make_map(&ma, A, M, K, 128) || !make_map(&mb, B, N, K, 128)) return cudaErrorInvalidValue;
+    switch (epi) {
+      case -1: return launch_gemm2_t<-1>(ma, mb, C, M, N, K, lut, s, sms);
+      case OP_TANH: return launch_gemm2_t<OP_TANH>(ma, mb, C, M, N, K, lut, s, sms);
+      case OP_SIGMOID: return launch_gemm2_t<OP_SIGMOID>(ma, mb, C, M, N, K, lut, s, sms);
+      case OP_SWISH: return launch_gemm2_t<OP_SWISH>(ma, mb, C, M, N, K, lut, s, sms);
+      case OP_GELU: return launch_gemm2_t<OP_GELU>(ma, mb, C, M, N, K, lut, s, sms);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (!make_map(&ma, A, M, K, kBM) || !make_map(&mb, B, N, K, kBN)) return cudaErrorInvalidValue;
   switch (epi) {
     case -1: return launch_gemm_t<-1>(ma, mb, C, M, N, K, lut, s, sms);

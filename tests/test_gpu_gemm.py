@@ -64,3 +64,53 @@ def test_gemm_bad_shapes(kt):
     B = rand_bf16((256, 64), 6)
     with pytest.raises(kt.KTanhError):
         kt.kgemm_bf16(A, B)
+
+
+_PAIR_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1909_07729_b200 as kt
+out = {}
+for (M, N, K) in [(256, 256, 64), (512, 768, 320), (768, 512, 1024), (1024, 2048, 256)]:
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    for epi in (None, "gelu", "tanh"):
+        C = kt.kgemm_bf16(A, B, epilogue=epi)
+        out[f"{M}_{N}_{K}_{epi}"] = C.view(torch.int16).cpu().numpy()
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_gemm_cta_pair_equals_single_cta(kt, tmp_path):
+    """The CTA-pair kernel (tcgen05.mma.cta_group::2, M = 256) and the 1-CTA
+    kernel give bit-identical C, plain and with epilogues (KT_GEMM_2CTA
+    forces either; read once per process, hence the subprocesses)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "pair.py"
+    script.write_text(_PAIR_SCRIPT)
+    res = {}
+    for mode in ("0", "1"):
+        f = tmp_path / f"out{mode}.npz"
+        env = dict(os.environ, KT_GEMM_2CTA=mode)
+        subprocess.run([sys.executable, str(script), root, str(f)], check=True, env=env, timeout=300)
+        res[mode] = np.load(f)
+    for k in res["0"].files:
+        assert np.array_equal(res["0"][k], res["1"][k]), k
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (512, 768, 320), (1024, 2048, 1024)])
+def test_gemm_pair_shapes_vs_float64(kt, M, N, K):
+    """Shapes with M % 256 == 0 take the CTA-pair kernel (plain GEMM)."""
+    A, B = rand_bf16((M, K), 7, 0.5), rand_bf16((N, K), 8, 0.5)
+    C = kt.kgemm_bf16(A, B)
+    torch.cuda.synchronize()
+    a = O.bf16_to_f64(u16(A)).reshape(M, K)
+    b = O.bf16_to_f64(u16(B)).reshape(N, K)
+    exact = a @ b.T
+    got = O.bf16_to_f64(u16(C)).reshape(M, N)
+    bound = np.abs(exact) * 2.0 ** -8 + K * 2.0 ** -23 * (np.abs(a) @ np.abs(b).T) + 1e-30
+    assert np.all(np.abs(got - exact) <= bound)
