@@ -89,6 +89,20 @@ __device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr) {
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
                             ((uint32_t)(kBM >> 4) << 24);
 
+// 32 consecutive TMEM columns of this warp's 32 lanes -> r[0..31] (async;
+// complete with tcgen05.wait::ld).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t *r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
 template <int EPI>
 __device__ __forceinline__ uint32_t epi_word(uint32_t w, uint32_t lw) {
   if (EPI == OP_TANH) return ktanh_bf16x2(w, lw);
@@ -404,47 +418,40 @@ k_gemm2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUten
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t row = mb * 256 + rank * 128 + 32 * q + lane;
       uint16_t *crow = C + (size_t)row * N + nb * 256 + half * 128;
-#pragma unroll 1
-      for (uint32_t c = 0; c < 128; c += 32) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem + ((32 * q) << 16) + a * kTmemCols + half * 128 + c;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-              "=r"(r[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c == 96) {
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          // Relaxed: the TMEM reads are complete (wait::ld) and fenced by
-          // tcgen05.fence::before_thread_sync; a .release.cluster arrive
-          // would add a GPU-scope MEMBAR that waits for this warp's
-          // outstanding C stores (measured: it stalls the epilogue).
-          if (lane == 0) {
-            if (leader)
-              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar + 8 * a)
-                           : "memory");
-            else
-              asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                               tempty_leader + 8 * a)
-                           : "memory");
-          }
-        }
+      // All 128 of this warp's columns in flight at once, one wait, then the
+      // TMEM stage is released before any epilogue arithmetic (the MMA of the
+      // tile after next can start while the activation runs).
+      uint32_t r[128];
+      const uint32_t tbase = tmem + ((32 * q) << 16) + a * kTmemCols + half * 128;
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) tmem_ld32(tbase + 32 * c4, r + 32 * c4);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      // Relaxed: the TMEM reads are complete (wait::ld) and fenced by
+      // tcgen05.fence::before_thread_sync; a .release.cluster arrive would
+      // add a GPU-scope MEMBAR that waits for this warp's outstanding C
+      // stores.
+      if (lane == 0) {
+        if (leader)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar + 8 * a) : "memory");
+        else
+          asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           tempty_leader + 8 * a)
+                       : "memory");
+      }
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
         uint32_t o0[8], o1[8];
+        const uint32_t *rc = r + 32 * c4;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);
+          o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(rc[2 * j + 1]), __uint_as_float(rc[2 * j])), lw);
           o1[j] = epi_word<EPI>(
-              pack_bf16x2(__uint_as_float(r[2 * j + 17]), __uint_as_float(r[2 * j + 16])), lw);
+              pack_bf16x2(__uint_as_float(rc[2 * j + 17]), __uint_as_float(rc[2 * j + 16])), lw);
         }
-        st256(crow + c, o0, true);
-        st256(crow + c + 16, o1, true);
+        st256(crow + 32 * c4, o0, true);
+        st256(crow + 32 * c4 + 16, o1, true);
       }
     }
   }
