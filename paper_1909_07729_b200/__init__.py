@@ -17,7 +17,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libktanh.so")
+LIB_PATH = os.environ.get("KT_LIB") or os.path.join(_PKG, "libktanh.so")   # KT_LIB: dev A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

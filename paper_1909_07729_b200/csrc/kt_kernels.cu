@@ -32,7 +32,10 @@ namespace kt {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 2;                    // 32-B vectors per lane per chunk (flat: 1 chunk/warp)
+#ifndef KT_UNROLL
+#define KT_UNROLL 2
+#endif
+constexpr int kUnroll = KT_UNROLL;            // 32-B vectors per lane per chunk (flat: 1 chunk/warp)
 constexpr int kVecBytes = 32;
 constexpr int kChunkVecs = 32 * kUnroll;      // vectors per warp-chunk
 
