@@ -468,7 +468,7 @@ def table2_b200(kt, K, W, world, device, rank, peak):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ktanh", choices=["ktanh", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip configs 3-5 side measurements")

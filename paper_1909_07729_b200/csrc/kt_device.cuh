@@ -373,6 +373,22 @@ __device__ __forceinline__ uint32_t lstm_bf16x2(uint32_t x, uint32_t lw, bool is
 
 // ------------------------------------------------------ streaming memory --
 
+// L2 eviction-priority qualifiers for the streaming loads / stores (default
+// policy; dev A/B builds: -DKT_LD_EF=1 / -DKT_ST_EF=1 evict_first,
+// -DKT_ST_EL=1 evict_last).
+#if defined(KT_LD_EF) && KT_LD_EF
+#define KT_LD_L2 ".L2::evict_first"
+#else
+#define KT_LD_L2 ""
+#endif
+#if defined(KT_ST_EF) && KT_ST_EF
+#define KT_ST_L2 ".L2::evict_first"
+#elif defined(KT_ST_EL) && KT_ST_EL
+#define KT_ST_L2 ".L2::evict_last"
+#else
+#define KT_ST_L2 ""
+#endif
+
 // 32-byte (256-bit) predicated global load / store (LDG.E.256 / STG.E.256).
 // NC: read-only non-coherent path, used only when y does not alias x.
 template <bool NC>
@@ -380,7 +396,7 @@ __device__ __forceinline__ void ld256(const void *p, uint32_t (&r)[8], bool pred
   if (NC) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t"
-        "@p ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
+        "@p ld.global.nc.L1::no_allocate" KT_LD_L2 ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
           "=r"(r[7])
         : "l"(p), "r"((int)pred));
@@ -398,7 +414,7 @@ __device__ __forceinline__ void ld256(const void *p, uint32_t (&r)[8], bool pred
 __device__ __forceinline__ void st256(void *p, const uint32_t (&r)[8], bool pred) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t"
-      "@p st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n\t}" ::"l"(p),
+      "@p st.global.L1::no_allocate" KT_ST_L2 ".v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n\t}" ::"l"(p),
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
       "r"((int)pred)
       : "memory");
