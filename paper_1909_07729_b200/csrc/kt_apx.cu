@@ -231,8 +231,11 @@ k_apx(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
 // computes and stores chunk c, so memory traffic overlaps the arithmetic
 // within the warp (the flat one-chunk-per-warp shape leaves a compute-bound
 // map at ~55% of both ALU and HBM rate).
+#ifndef KT_APX_PIPE_MINB
+#define KT_APX_PIPE_MINB 3   // <= 80 regs, 3 CTAs/SM: minimax-3 BF16 1140 -> 1214 Gelem/s (apx_stream_r01.txt)
+#endif
 template <int KIND, int A, int B, int FMT, bool NC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, KT_APX_PIPE_MINB)
 k_apx_pipe(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
            const __grid_constant__ ApxWords w) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;

@@ -169,8 +169,14 @@ __device__ __forceinline__ void dual_span(const uint8_t *xp, uint8_t *gp, uint8_
   }
 }
 
+#ifndef KT_DUAL_MINB
+#define KT_DUAL_MINB 6   // 40 regs: 6 CTAs/SM (+5% on config 5, profiles/sweep_flat_r01.txt)
+#endif
+#ifndef KT_BWD_MINB
+#define KT_BWD_MINB 5    // 48 regs: 5 CTAs/SM (+17% on config 5 backward)
+#endif
 template <int FMT, bool NC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, KT_DUAL_MINB)
 k_dual(const uint8_t *x, uint8_t *yg, uint8_t *ys, uint32_t head, uint64_t nvec, uint32_t tail,
        uint32_t pf_blocks, const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
@@ -248,7 +254,7 @@ __device__ __forceinline__ void scalar_span_bwd(const uint8_t *ap, const uint8_t
 }
 
 template <int OP, int FMT, bool NC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, KT_BWD_MINB)
 k_bwd(const uint8_t *a, const uint8_t *dy, uint8_t *dx, uint32_t head, uint64_t nvec, uint32_t tail,
       const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
@@ -357,7 +363,11 @@ k_lstm(const uint8_t *x, uint8_t *y, uint32_t nvec, uint32_t vpr, uint32_t vpq, 
 // Fused LSTM cell, vector path: 16 consecutive cells of one row per lane
 // (hidden % 16 == 0, all pointers 32-B aligned).  Per 16 cells: 4 x 32 B of
 // gates + 64 B of c in, 64 B of c' + 32 B of h out (18 B per cell).
-__global__ void __launch_bounds__(kThreads)
+#ifdef KT_CELL_MINB
+__global__ void __launch_bounds__(kThreads, KT_CELL_MINB)
+#else
+__global__ void __launch_bounds__(kThreads)   // (kThreads, 1) lets ptxas take > 64 regs: slower
+#endif
 k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_t *h_next,
             uint32_t nvec, uint32_t vpr, uint32_t hidden, uint32_t pf_stride,
             const __grid_constant__ LutWords lut) {

@@ -24,5 +24,5 @@ for _ in range(50):
     ts.append(a.elapsed_time(b) / 20)
 m = statistics.median(ts)
 cells = xs[0].numel() // 4
-print(f"KT_CELL={os.environ.get("KT_CELL_PF", "default")}: {m*1e3:.2f} us/launch, "
+print(f"KT_LIB={os.environ.get('KT_LIB') or 'default'}: {m*1e3:.2f} us/launch, "
       f"{cells / m / 1e6:.1f} Gcell/s, {18 * cells / m / 1e6:.1f} GB/s")
