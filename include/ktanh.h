@@ -279,7 +279,7 @@ KT_API kt_status kt_apx_tanh_f32(const float *x, float *y, size_t n, kt_apx a, v
  * copies; pageable memory works but the copies become synchronous.
  * d_work: caller-owned device scratch of work_bytes; at least
  * 3 * 2 * 4096 * elem_size bytes (KT_ERR_ARG otherwise).  The chunk is
- * about n/8 elements (at least 1 MiB, at most work_bytes / (6 * elem_size)),
+ * about n/3 elements (at least 1 MiB, at most work_bytes / (6 * elem_size)),
  * a multiple of 256 elements.
  * Strategy knob (environment, read per call): KT_HOST_ZEROCOPY=1 runs ONE
  * kernel that reads x_host and writes y_host in place over PCIe when both
@@ -287,7 +287,10 @@ KT_API kt_status kt_apx_tanh_f32(const float *x, float *y, size_t n, kt_apx a, v
  * store straight into a mapped y_host; unset/0 (default) is the copy-engine
  * pipeline, the fastest measured on B200 (profiles/host_path_r01.txt).
  * Pageable buffers always take the pipeline.  x_host and y_host may be
- * equal (in place); any other overlap is KT_ERR_ARG.  d_work may be NULL
+ * equal (in place); any other overlap is KT_ERR_ARG.  Calls on DIFFERENT
+ * caller streams with different d_work buffers overlap on the copy engines
+ * (one call's D2H with the next one's H2D); calls that reuse the same
+ * d_work are ordered on it internally, so sharing d_work is always safe.  d_work may be NULL
  * only on the mode-1 zero-copy path. */
 KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, void *y_host,
                                size_t n, kt_lut lut, void *d_work, size_t work_bytes,

@@ -227,6 +227,13 @@ struct HostPipe {
   cudaStream_t st[kStages];
   cudaEvent_t fork, join[kStages];
   cudaEvent_t ev_in[kBufs], ev_comp[kBufs], ev_out[kBufs];
+  // Device byte range each buffer slot last used, and whether its last
+  // event is the D2H (ev_out) or, for the mapped-y mode, the kernel
+  // (ev_comp).  Cross-call reuse guard: a call on another caller stream may
+  // start while an earlier call still uses its slots; it waits for those
+  // slots only if its own work region overlaps theirs.
+  uintptr_t slot_lo[kBufs] = {}, slot_hi[kBufs] = {};
+  bool slot_mapped[kBufs] = {};
   std::mutex mu;
 };
 HostPipe g_pipe[kMaxDev];
@@ -584,9 +591,12 @@ KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, voi
   chunk -= chunk % 256;
   if (chunk < 4096)
     return fail(KT_ERR_ARG, "work_bytes too small (need >= %zu)", 2 * kBufs * es * 4096);
-  // ~8 chunks per call (at least 1 MiB each): both copy directions stay busy
-  // and the pipeline fill/drain (one chunk's H2D + D2H) stays short.
-  size_t want = (n / 8 + 255) / 256 * 256;
+  // ~3 chunks per call (one per buffer slot, at least 1 MiB each): within a
+  // call the copy directions and the kernel overlap chunk by chunk, and calls
+  // on different caller streams overlap each other's fill/drain, where fewer,
+  // larger copies run closer to the PCIe rate (config 2 end to end: 8 chunks
+  // 19.9, 4 chunks 22.0, 3 chunks 22.6 Gelem/s; profiles/host_path_r01.txt).
+  size_t want = ((n + kBufs - 1) / kBufs + 255) / 256 * 256;
   const size_t min_chunk = ((size_t)1 << 20) / es;
   if (want < min_chunk) want = min_chunk;
   if (const char *ev = getenv("KT_HOST_CHUNK")) {   // tuning override (elements)
@@ -611,6 +621,16 @@ KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, voi
   const char *xh = static_cast<const char *>(x_host);
   char *yh = static_cast<char *>(y_host);
   char *work = static_cast<char *>(d_work);
+  {
+    // earlier calls (possibly on other caller streams) whose slots overlap
+    // this call's work region must be done with them before our first H2D;
+    // later H2Ds, kernels and D2Hs of this call follow it in stream order
+    const uintptr_t lo = (uintptr_t)work, hi = lo + (uintptr_t)kBufs * 2 * chunk * es;
+    for (int j = 0; j < kBufs; ++j) {
+      if (p->slot_hi[j] > lo && p->slot_lo[j] < hi)
+        KT_CK(cudaStreamWaitEvent(h2d, p->slot_mapped[j] ? p->ev_comp[j] : p->ev_out[j], 0), "wait");
+    }
+  }
   size_t k = 0;
   for (size_t off = 0; off < n; off += chunk, ++k) {
     const size_t cnt = (n - off < chunk) ? n - off : chunk;
@@ -626,6 +646,9 @@ KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, voi
       KT_CK(cudaStreamWaitEvent(comp, p->ev_out[b], 0), "wait");  // dy free
     KT_CK(kt::launch_map((int)op, (int)dtype, dx, dy, cnt, lut->words, comp, li), "kernel launch");
     KT_CK(cudaEventRecord(p->ev_comp[b], comp), "record");
+    p->slot_lo[b] = (uintptr_t)dx;
+    p->slot_hi[b] = (uintptr_t)dx + 2 * chunk * es;
+    p->slot_mapped[b] = y_mapped != nullptr;
     if (y_mapped) continue;
     KT_CK(cudaStreamWaitEvent(d2h, p->ev_comp[b], 0), "wait");
     KT_CK(cudaMemcpyAsync(yh + off * es, dy, cnt * es, cudaMemcpyDeviceToHost, d2h), "D2H");

@@ -508,3 +508,26 @@ def test_concurrent_host_threads(kt):
     for t in th:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("shared_work", [True, False])
+def test_apply_host_cross_stream(kt, shared_work):
+    """kt_apply_host calls on two caller streams overlap on the copy engines;
+    with a SHARED d_work of different per-call chunk sizes the cross-call
+    slot guard must order them (include/ktanh.h).  Every output is checked."""
+    sizes = [1 << 22, (1 << 20) + 37, 3 << 20, 1 << 21, (1 << 22) + 1000, 1 << 20]
+    g = torch.Generator().manual_seed(31)
+    xs = [(torch.randn(n, generator=g) * 2).to(torch.bfloat16).pin_memory() for n in sizes]
+    ys = [torch.full_like(x, float("nan")).pin_memory() for x in xs]
+    works = [torch.empty(24 << 20, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for rep in range(3):
+        for i, (x, y) in enumerate(zip(xs, ys)):
+            j = i % 2
+            kt.apply_host("tanh", x, y, works[0] if shared_work else works[j], stream=streams[j])
+        torch.cuda.synchronize()
+        for x, y in zip(xs, ys):
+            want = O.map_bf16("tanh", x.view(torch.int16).numpy().view(np.uint16))
+            assert_bitexact(y.view(torch.int16).numpy().view(np.uint16), want, 16,
+                            ctx=f"cross-stream shared={shared_work} n={x.numel()}")
+            y.fill_(float("nan"))
