@@ -256,7 +256,7 @@ def time_eager(step: Step, K: int, device):
     return e0.elapsed_time(e1) / K
 
 
-E2E_STREAMS = 2
+E2E_STREAMS = int(os.environ.get("KT_E2E_STREAMS", "2"))   # dev A/B knob
 
 
 def time_e2e(kt, cfg, op, K: int, W: int, world: int, device, rank):
