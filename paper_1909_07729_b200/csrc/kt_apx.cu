@@ -749,8 +749,6 @@ cudaError_t alu_probe(int which, int fmt, const LutWords &lw, const ApxWords &w,
   return cudaSuccess;
 }
 
-namespace {
-}  // namespace
 
 bool apx_build(int kind, int p, int q, ApxWords *w, double *coef, char *err, size_t errlen) {
   memset(w, 0, sizeof(*w));
