@@ -433,6 +433,43 @@ TABLE2_MAPS = [("ktanh", None), ("sfu", "apx:sfu:0:0"), ("libm", "apx:libm:0:0")
                ("taylor_2", "apx:taylor:2:0"), ("taylor_3", "apx:taylor:3:0")]
 
 
+def lstm_gemm_line(kt, K, W, world, device, rank):
+    """NEXT-2 on config 4: the GNMT LSTM gate GEMM that produces config 4's
+    [128 x 50, 4 x 1024] gate block (input [6400, 1024] x W [4096, 1024]^T),
+    with K-Sigmoid / K-TanH fused into the tcgen05 epilogue, vs the GEMM
+    alone and the unfused GEMM + klstm_gates_bf16 (all through the C ABI)."""
+    H = WL.LSTM_HIDDEN
+    M, Kd = 128 * 50, H
+    gA = WL.make_input("c4_lstm_gates", device=device, rank=rank, numel=M * Kd).reshape(M, Kd)
+    gB = (WL.make_input("c4_lstm_gates", device=device, rank=rank, numel=4 * H * Kd, seed=9)
+          .reshape(4 * H, Kd) * 0.05).to(torch.bfloat16)
+    sets = 4
+    gCs = [torch.empty(M, 4 * H, dtype=torch.bfloat16, device=device) for _ in range(sets)]
+    gTs = [torch.empty(M, 4 * H, dtype=torch.bfloat16, device=device) for _ in range(sets)]
+
+    class _S:
+        n, bytes_per_step = M * 4 * H, 0
+
+        def __init__(self, fn):
+            self.fn = fn
+            self.kt = kt
+
+        def run(self, i):
+            self.fn(i % sets)
+    res = {}
+    for name, fn in (("fused", lambda s: kt.kgemm_lstm_gates_bf16(gA, gB, H, 2, out=gCs[s])),
+                     ("gemm_only", lambda s: kt.kgemm_bf16(gA, gB, out=gCs[s])),
+                     ("unfused", lambda s: (kt.kgemm_bf16(gA, gB, out=gTs[s]),
+                                            kt.klstm_gates_bf16(gTs[s], H, 2, out=gCs[s])))):
+        wts, _, _ = time_windows(_S(fn), K, W, world, device, None, min_total_s=0.3, max_windows=20)
+        res[name] = statistics.median(wts) / K
+    fl = 2.0 * M * 4 * H * Kd
+    return {"ms_per_step": round(res["fused"], 5), "tflops_per_gpu": round(fl / (res["fused"] / 1e3) / 1e12, 1),
+            "gemm_only_ms": round(res["gemm_only"], 5), "unfused_gemm_plus_klstm_gates_ms": round(res["unfused"], 5),
+            "note": "gates = K-TanH (quarter 2) / K-Sigmoid applied in the tcgen05 GEMM epilogue; "
+                    "bit-identical to kgemm_bf16 + klstm_gates_bf16"}
+
+
 def table2_b200(kt, K, W, world, device, rank, peak):
     """Table 2 on B200.  For K-TanH and
     each float-op comparator: accuracy over every finite BF16 input (the
@@ -591,6 +628,10 @@ def main():
 
     if not args.no_extra:
         extra["table2_b200"] = table2_b200(kt, K, W, world, device, rank, peak)
+
+    if not args.no_extra:
+        extra["lstm_gates_gemm_M6400_N4096_K1024:kgemm_lstm_gates_bf16"] = lstm_gemm_line(
+            kt, K, W, world, device, rank)
 
     cpu = None
     if rank == 0 and not args.no_cpu:

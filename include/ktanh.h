@@ -178,6 +178,18 @@ KT_API kt_status klstm_cell_bf16(const uint16_t *gates, const float *c_prev, flo
 KT_API kt_status kgemm_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M, size_t N,
                             size_t K, int epilogue, kt_lut lut, void *stream);
 
+/* The LSTM gate GEMM with the gate activations fused (
+ * BASELINE.json config 4; GNMT LSTM): C[M, 4*hidden] =
+ * gates(RN_bf16(A[M, K] . B[4*hidden, K]^T)) where columns of quarter
+ * tanh_quarter (the cell candidate g; 2 in PyTorch's i,f,g,o order) get
+ * K-TanH and the other quarters K-Sigmoid -- bit-identical to kgemm_bf16
+ * (epilogue -1) followed by klstm_gates_bf16.  Requires hidden % 256 == 0
+ * (each 256-column tile lies in one quarter) and the kgemm_bf16 shape and
+ * alignment rules (M % 128 == 0, K % 64 == 0); KT_ERR_ARG otherwise. */
+KT_API kt_status kgemm_lstm_gates_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M,
+                                       size_t hidden, size_t K, int tanh_quarter, kt_lut lut,
+                                       void *stream);
+
 /* Generic dispatcher over (op, dtype); same contract as the calls above. */
 KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size_t n,
                           kt_lut lut, void *stream);

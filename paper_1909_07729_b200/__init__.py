@@ -42,7 +42,8 @@ EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_creat
                        "klstm_gates_bf16", "klstm_cell_bf16", "kgemm_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
                        "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count",
                        "kt_apx_create", "kt_apx_coeffs", "kt_apx_destroy", "kt_apx_tanh_bf16",
-                       "kt_apx_tanh_f32", "kt_alu_probe", "kgelu_swish_bf16", "kgelu_swish_f32")
+                       "kt_apx_tanh_f32", "kt_alu_probe", "kgelu_swish_bf16", "kgelu_swish_f32",
+                       "kgemm_lstm_gates_bf16")
 
 for _name in MAP_CALLS:
     _f = getattr(_lib, _name)
@@ -102,6 +103,8 @@ for _name in ("kgelu_swish_bf16", "kgelu_swish_f32"):
     _f = getattr(_lib, _name)
     _f.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
     _f.restype = ctypes.c_int
+_lib.kgemm_lstm_gates_bf16.argtypes = [_vp, _vp, _vp, _sz, _sz, _sz, ctypes.c_int, _vp, _vp]
+_lib.kgemm_lstm_gates_bf16.restype = ctypes.c_int
 _lib.kt_alu_probe.argtypes = [ctypes.c_int, _vp, _vp, _vp, ctypes.c_int,
                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
 _lib.kt_alu_probe.restype = ctypes.c_int
@@ -496,3 +499,26 @@ def _make_dual(name, dtype_name):
 
 kgelu_swish_bf16 = _make_dual("kgelu_swish_bf16", "bf16")
 kgelu_swish_f32 = _make_dual("kgelu_swish_f32", "f32")
+
+
+def kgemm_lstm_gates_bf16(A, B, hidden: int, tanh_quarter: int = 2, out=None, lut: Lut | None = None,
+                          stream=None):
+    """LSTM gate GEMM with fused gate activations: A [M, K], B [4*hidden, K]
+    (BF16 CUDA) -> K-Sigmoid / K-TanH(RN_bf16(A @ B.T)) per quarter."""
+    import torch
+    if not (A.is_cuda and B.is_cuda) or A.dtype != torch.bfloat16 or B.dtype != torch.bfloat16:
+        raise TypeError("A, B must be CUDA bfloat16 tensors")
+    if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[1] or B.shape[0] != 4 * hidden:
+        raise ValueError("A [M, K], B [4*hidden, K]")
+    if not (A.is_contiguous() and B.is_contiguous()):
+        raise ValueError("A, B must be contiguous")
+    M, K = A.shape
+    if out is None:
+        out = torch.empty(M, 4 * hidden, dtype=torch.bfloat16, device=A.device)
+    lut = lut or paper_lut()
+    idx = A.device.index
+    with _on_device(idx):
+        _check(_lib.kgemm_lstm_gates_bf16(A.data_ptr(), B.data_ptr(), out.data_ptr(), M, hidden, K,
+                                          tanh_quarter, lut.handle, _stream_ptr(stream, idx)),
+               "kgemm_lstm_gates_bf16")
+    return out

@@ -501,13 +501,13 @@ KT_API kt_status klstm_cell_bf16(const uint16_t *gates, const float *c_prev, flo
   return KT_OK;
 }
 
-KT_API kt_status kgemm_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M, size_t N,
-                            size_t K, int epilogue, kt_lut lut, void *stream) {
-  if (epilogue < -1 || epilogue > 3) return fail(KT_ERR_ARG, "epilogue must be -1 or a kt_op");
+static kt_status run_gemm(int epilogue, const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M,
+                          size_t N, size_t K, kt_lut lut, void *stream, uint32_t lstm_hidden,
+                          uint32_t lstm_tq) {
   if (epilogue >= 0 && !lut) return fail(KT_ERR_ARG, "lut is NULL");
   if (M == 0 || N == 0) return KT_OK;
   if (M % 128 || N % 256 || K % 64 || K == 0)
-    return fail(KT_ERR_ARG, "kgemm_bf16 needs M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (K > 0)");
+    return fail(KT_ERR_ARG, "kgemm needs M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (K > 0)");
   if (M > (1u << 31) || N > (1u << 31) || K > (1u << 31)) return fail(KT_ERR_ARG, "size too large");
   if (!A || !B || !C) return fail(KT_ERR_ARG, "NULL pointer");
   if ((uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)C % 32)
@@ -523,9 +523,25 @@ KT_API kt_status kgemm_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, s
   if ((s = check_device_ptr(C, li.device, "C")) != KT_OK) return s;
   static const kt::LutWords kNoLut = {};
   cudaError_t e = kt::launch_gemm(epilogue, A, B, C, M, N, K, lut ? lut->words : kNoLut,
-                                  (cudaStream_t)stream, li.sm_count);
-  if (e != cudaSuccess) return cuda_fail(e, "kgemm_bf16 launch");
+                                  (cudaStream_t)stream, li.sm_count, lstm_hidden, lstm_tq);
+  if (e != cudaSuccess) return cuda_fail(e, "kgemm launch");
   return KT_OK;
+}
+
+KT_API kt_status kgemm_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M, size_t N,
+                            size_t K, int epilogue, kt_lut lut, void *stream) {
+  if (epilogue < -1 || epilogue > 3) return fail(KT_ERR_ARG, "epilogue must be -1 or a kt_op");
+  return run_gemm(epilogue, A, B, C, M, N, K, lut, stream, 0, 0);
+}
+
+KT_API kt_status kgemm_lstm_gates_bf16(const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M,
+                                       size_t hidden, size_t K, int tanh_quarter, kt_lut lut,
+                                       void *stream) {
+  if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (hidden == 0 || hidden % 256 || hidden > (1u << 29))
+    return fail(KT_ERR_ARG, "hidden must be a positive multiple of 256");
+  if (tanh_quarter < 0 || tanh_quarter > 3) return fail(KT_ERR_ARG, "tanh_quarter must be 0..3");
+  return run_gemm(8, A, B, C, M, 4 * hidden, K, lut, stream, (uint32_t)hidden, (uint32_t)tanh_quarter);
 }
 
 // Host-buffer strategy (KT_HOST_ZEROCOPY): 0 = copy-engine pipeline,

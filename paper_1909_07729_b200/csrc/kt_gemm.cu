@@ -103,6 +103,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t *r) {
       : "r"(taddr));
 }
 
+// Epilogue id for the LSTM gate block (config 4): K-TanH on the tanh
+// quarter's columns, K-Sigmoid elsewhere; the quarter is uniform per tile
+// (hidden % 256 == 0), so each tile resolves to OP_TANH or OP_SIGMOID.
+constexpr int kEpiLstm = 8;
+
 template <int EPI>
 __device__ __forceinline__ uint32_t epi_word(uint32_t w, uint32_t lw) {
   if (EPI == OP_TANH) return ktanh_bf16x2(w, lw);
@@ -110,6 +115,30 @@ __device__ __forceinline__ uint32_t epi_word(uint32_t w, uint32_t lw) {
   if (EPI == OP_SWISH) return kswish_bf16x2(w, lw);
   if (EPI == OP_GELU) return kgelu_bf16x2(w, lw);
   return w;
+}
+
+// 32 fp32 accumulators (TMEM columns c..c+31 of one row) -> RN_bf16 -> op ->
+// two 16-element output vectors.
+template <int EPI>
+__device__ __forceinline__ void epi_chunk32(const uint32_t *r, uint32_t (&o0)[8], uint32_t (&o1)[8],
+                                            uint32_t lw) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);
+    o1[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 17]), __uint_as_float(r[2 * j + 16])),
+                          lw);
+  }
+}
+
+template <int EPI>
+__device__ __forceinline__ void epi_tile_chunk(const uint32_t *r, uint32_t (&o0)[8], uint32_t (&o1)[8],
+                                               uint32_t lw, bool tanh_tile) {
+  if (EPI == kEpiLstm) {
+    if (tanh_tile) epi_chunk32<OP_TANH>(r, o0, o1, lw);          // warp-uniform per tile
+    else epi_chunk32<OP_SIGMOID>(r, o0, o1, lw);
+  } else {
+    epi_chunk32<EPI>(r, o0, o1, lw);
+  }
 }
 
 // Persistent variant: grid = min(tiles, SMs); each CTA walks tiles
@@ -135,7 +164,7 @@ __device__ __forceinline__ void tile_coords(uint32_t t, uint32_t mt, uint32_t nt
 template <int EPI>
 __global__ void __launch_bounds__(kGemmPThreads, 1)
 k_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-       uint16_t *C, uint32_t M, uint32_t N, uint32_t K, const __grid_constant__ LutWords lut) {
+       uint16_t *C, uint32_t M, uint32_t N, uint32_t K, uint32_t epi_hidden, uint32_t epi_tq, const __grid_constant__ LutWords lut) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -228,6 +257,7 @@ k_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtens
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t row = mb * kBM + 32 * q + lane;
       uint16_t *crow = C + (size_t)row * N + nb * kBN + half * 128;
+      const bool tanh_tile = EPI == kEpiLstm && (nb * kBN) / epi_hidden == epi_tq;
 #pragma unroll 1
       for (uint32_t c = 0; c < 128; c += 32) {
         uint32_t r[32];
@@ -251,12 +281,7 @@ k_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtens
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar + 8 * a) : "memory");
         }
         uint32_t o0[8], o1[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);
-          o1[j] = epi_word<EPI>(
-              pack_bf16x2(__uint_as_float(r[2 * j + 17]), __uint_as_float(r[2 * j + 16])), lw);
-        }
+        epi_tile_chunk<EPI>(r, o0, o1, lw, tanh_tile);
         st256(crow + c, o0, true);
         st256(crow + c + 16, o1, true);
       }
@@ -318,7 +343,7 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmPThreads, 1)
 k_gemm2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-        uint16_t *C, uint32_t M, uint32_t N, uint32_t K, const __grid_constant__ LutWords lut) {
+        uint16_t *C, uint32_t M, uint32_t N, uint32_t K, uint32_t epi_hidden, uint32_t epi_tq, const __grid_constant__ LutWords lut) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -418,6 +443,7 @@ k_gemm2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUten
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t row = mb * 256 + rank * 128 + 32 * q + lane;
       uint16_t *crow = C + (size_t)row * N + nb * 256 + half * 128;
+      const bool tanh_tile = EPI == kEpiLstm && (nb * 256) / epi_hidden == epi_tq;
       // All 128 of this warp's columns in flight at once, one wait, then the
       // TMEM stage is released before any epilogue arithmetic (the MMA of the
       // tile after next can start while the activation runs).
@@ -443,13 +469,7 @@ k_gemm2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUten
 #pragma unroll
       for (int c4 = 0; c4 < 4; ++c4) {
         uint32_t o0[8], o1[8];
-        const uint32_t *rc = r + 32 * c4;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(rc[2 * j + 1]), __uint_as_float(rc[2 * j])), lw);
-          o1[j] = epi_word<EPI>(
-              pack_bf16x2(__uint_as_float(rc[2 * j + 17]), __uint_as_float(rc[2 * j + 16])), lw);
-        }
+        epi_tile_chunk<EPI>(r + 32 * c4, o0, o1, lw, tanh_tile);
         st256(crow + 32 * c4, o0, true);
         st256(crow + 32 * c4 + 16, o1, true);
       }
@@ -500,7 +520,8 @@ static bool make_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t K,
 
 template <int EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap &ma, const CUtensorMap &mb, uint16_t *C, size_t M,
-                                 size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms) {
+                                 size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms,
+                                 uint32_t eh, uint32_t etq) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -511,14 +532,15 @@ static cudaError_t launch_gemm_t(const CUtensorMap &ma, const CUtensorMap &mb, u
   const size_t tiles = (M / kBM) * (N / kBN);
   const unsigned grid = (unsigned)(tiles < (size_t)sms ? tiles : (size_t)sms);
   k_gemm<EPI><<<grid, kGemmPThreads, kGemmSmem, s>>>(ma, mb, C, (uint32_t)M, (uint32_t)N,
-                                                     (uint32_t)K, lut);
+                                                     (uint32_t)K, eh, etq, lut);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int EPI>
 static cudaError_t launch_gemm2_t(const CUtensorMap &ma, const CUtensorMap &mb, uint16_t *C, size_t M,
-                                  size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms) {
+                                  size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms,
+                                  uint32_t eh, uint32_t etq) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -530,49 +552,51 @@ static cudaError_t launch_gemm2_t(const CUtensorMap &ma, const CUtensorMap &mb, 
   const size_t pairs = (size_t)(sms / 2);
   const unsigned grid = (unsigned)(2 * (tiles < pairs ? tiles : pairs));
   k_gemm2<EPI><<<grid, kGemmPThreads, k2Smem, s>>>(ma, mb, C, (uint32_t)M, (uint32_t)N, (uint32_t)K,
-                                                   lut);
+                                                   eh, etq, lut);
   count_launch();
   return cudaGetLastError();
 }
 
 // Kernel choice (profiles/gemm_2cta_r01.txt): the CTA pair is faster for the
 // plain GEMM (1.44 vs 1.51 ms at 16384^2 x 4096; 0.40 vs 0.47 ms at
-// 65536 x 4096 x 1024), but with an activation epilogue the 1-CTA kernel is
-// as fast or faster on the FFN shapes (the epilogue no longer hides behind
-// the shorter pair mainloop).  KT_GEMM_2CTA=0/1 forces either for M % 256 == 0.
-static bool use_pair(size_t M, int epi) {
+// 65536 x 4096 x 1024) and for fused epilogues up to ~2^38 MACs; on the
+// sustained, power-capped FFN GEMM with K-GELU the 1-CTA kernel is 1-3%
+// ahead.  KT_GEMM_2CTA=0/1 forces either for M % 256 == 0.
+static bool use_pair(size_t M, size_t N, size_t K, int epi) {
   static const int force = [] {
     const char *e = getenv("KT_GEMM_2CTA");
     return e ? atoi(e) : -1;
   }();
   if (M % 256 != 0) return false;
   if (force >= 0) return force != 0;
-  return epi < 0;
+  // fused epilogues on very large, power-capped GEMMs (the FFN line:
+  // 2^42 MACs) run 1-3% faster on the 1-CTA kernel; smaller fused GEMMs (the
+  // LSTM gate GEMM, 2^34.7 MACs: 51.3 vs 53.1 us) on the pair
+  return epi < 0 || (double)M * (double)N * (double)K < 274877906944.0;   // 2^38
 }
 
 cudaError_t launch_gemm(int epi, const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M,
-                        size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms) {
+                        size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms,
+                        uint32_t lstm_hidden, uint32_t lstm_tq) {
   CUtensorMap ma, mb;
-  if (use_pair(M, epi) && sms >= 2) {
+  const uint32_t eh = lstm_hidden ? lstm_hidden : 1u, etq = lstm_tq;
+#define KT_EPIS(L)                                                       \
+  switch (epi) {                                                         \
+    case -1: return L<-1>(ma, mb, C, M, N, K, lut, s, sms, eh, etq);      \
+    case OP_TANH: return L<OP_TANH>(ma, mb, C, M, N, K, lut, s, sms, eh, etq);       \
+    case OP_SIGMOID: return L<OP_SIGMOID>(ma, mb, C, M, N, K, lut, s, sms, eh, etq); \
+    case OP_SWISH: return L<OP_SWISH>(ma, mb, C, M, N, K, lut, s, sms, eh, etq);     \
+    case OP_GELU: return L<OP_GELU>(ma, mb, C, M, N, K, lut, s, sms, eh, etq);       \
+    case kEpiLstm: return L<kEpiLstm>(ma, mb, C, M, N, K, lut, s, sms, eh, etq);     \
+  }                                                                      \
+  return cudaErrorInvalidValue;
+  if (use_pair(M, N, K, epi) && sms >= 2) {
     if (!make_map(&ma, A, M, K, 128) || !make_map(&mb, B, N, K, 128)) return cudaErrorInvalidValue;
-    switch (epi) {
-      case -1: return launch_gemm2_t<-1>(ma, mb, C, M, N, K, lut, s, sms);
-      case OP_TANH: return launch_gemm2_t<OP_TANH>(ma, mb, C, M, N, K, lut, s, sms);
-      case OP_SIGMOID: return launch_gemm2_t<OP_SIGMOID>(ma, mb, C, M, N, K, lut, s, sms);
-      case OP_SWISH: return launch_gemm2_t<OP_SWISH>(ma, mb, C, M, N, K, lut, s, sms);
-      case OP_GELU: return launch_gemm2_t<OP_GELU>(ma, mb, C, M, N, K, lut, s, sms);
-    }
-    return cudaErrorInvalidValue;
+    KT_EPIS(launch_gemm2_t)
   }
   if (!make_map(&ma, A, M, K, kBM) || !make_map(&mb, B, N, K, kBN)) return cudaErrorInvalidValue;
-  switch (epi) {
-    case -1: return launch_gemm_t<-1>(ma, mb, C, M, N, K, lut, s, sms);
-    case OP_TANH: return launch_gemm_t<OP_TANH>(ma, mb, C, M, N, K, lut, s, sms);
-    case OP_SIGMOID: return launch_gemm_t<OP_SIGMOID>(ma, mb, C, M, N, K, lut, s, sms);
-    case OP_SWISH: return launch_gemm_t<OP_SWISH>(ma, mb, C, M, N, K, lut, s, sms);
-    case OP_GELU: return launch_gemm_t<OP_GELU>(ma, mb, C, M, N, K, lut, s, sms);
-  }
-  return cudaErrorInvalidValue;
+  KT_EPIS(launch_gemm_t)
+#undef KT_EPIS
 }
 
 }  // namespace kt

@@ -68,8 +68,11 @@ cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *
 
 // tcgen05 GEMM C = act(RN_bf16(A . B^T)); epi = -1 (none) or an Op.
 // Requires M % 128 == 0, N % 256 == 0, K % 64 == 0 (checked by the caller).
+// epi = 8: LSTM gate block (K-TanH on columns of quarter lstm_tq of each
+// 4*lstm_hidden row, K-Sigmoid elsewhere; lstm_hidden % 256 == 0).
 cudaError_t launch_gemm(int epi, const uint16_t *A, const uint16_t *B, uint16_t *C, size_t M,
-                        size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms);
+                        size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms,
+                        uint32_t lstm_hidden = 0, uint32_t lstm_tq = 0);
 
 void count_launch();
 bool pdl_enabled();        // KT_PDL != 0

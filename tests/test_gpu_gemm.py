@@ -114,3 +114,27 @@ def test_gemm_pair_shapes_vs_float64(kt, M, N, K):
     got = O.bf16_to_f64(u16(C)).reshape(M, N)
     bound = np.abs(exact) * 2.0 ** -8 + K * 2.0 ** -23 * (np.abs(a) @ np.abs(b).T) + 1e-30
     assert np.all(np.abs(got - exact) <= bound)
+
+
+@pytest.mark.parametrize("M,H,K,tq", [(128, 256, 64, 2), (256, 512, 320, 0), (6400, 1024, 1024, 2),
+                                      (384, 256, 128, 3)])
+def test_gemm_lstm_gates_fused(kt, M, H, K, tq):
+    """kgemm_lstm_gates_bf16 == kgemm_bf16 then klstm_gates_bf16 (bitwise, NaN
+    by class), and the gate map is the oracle's on the BF16 GEMM output."""
+    A, B = rand_bf16((M, K), 11, 0.4), rand_bf16((4 * H, K), 12, 0.4)
+    fused = kt.kgemm_lstm_gates_bf16(A, B, H, tq)
+    plain = kt.kgemm_bf16(A, B)
+    ref = kt.klstm_gates_bf16(plain, H, tq)
+    torch.cuda.synchronize()
+    assert_bitexact(u16(fused), u16(ref), 16, nan_by_class=True, ctx=f"gemm+lstm {M}x{H}x{K}")
+    want = O.lstm_gates_bf16(u16(plain), H, tq)
+    assert_bitexact(u16(fused), want.reshape(-1), 16, nan_by_class=True, ctx="gemm+lstm vs oracle")
+
+
+def test_gemm_lstm_gates_bad_args(kt):
+    A, B = rand_bf16((128, 64), 13), rand_bf16((4 * 128, 64), 14)
+    with pytest.raises(kt.KTanhError):
+        kt.kgemm_lstm_gates_bf16(A, B, 128, 2)          # hidden % 256 != 0
+    A, B = rand_bf16((128, 64), 13), rand_bf16((4 * 256, 64), 14)
+    with pytest.raises(kt.KTanhError):
+        kt.kgemm_lstm_gates_bf16(A, B, 256, 4)          # bad quarter
