@@ -456,8 +456,16 @@ def lstm_gemm_line(kt, K, W, world, device, rank):
 
         def run(self, i):
             self.fn(i % sets)
+    cs = [torch.randn(M, H, device=device) for _ in range(sets)]
+    cns = [torch.empty_like(c) for c in cs]
+    hns = [torch.empty(M, H, dtype=torch.bfloat16, device=device) for _ in range(sets)]
     res = {}
     for name, fn in (("fused", lambda s: kt.kgemm_lstm_gates_bf16(gA, gB, H, 2, out=gCs[s])),
+                     ("gemm_cell_fused", lambda s: kt.kgemm_lstm_cell_bf16(gA, gB, cs[s], H, c_next=cns[s],
+                                                                           h_next=hns[s])),
+                     ("gemm_then_cell", lambda s: (kt.kgemm_bf16(gA, gB, out=gTs[s]),
+                                                   kt.klstm_cell_bf16(gTs[s], cs[s], H, c_next=cns[s],
+                                                                      h_next=hns[s]))),
                      ("gemm_only", lambda s: kt.kgemm_bf16(gA, gB, out=gCs[s])),
                      ("unfused", lambda s: (kt.kgemm_bf16(gA, gB, out=gTs[s]),
                                             kt.klstm_gates_bf16(gTs[s], H, 2, out=gCs[s])))):
@@ -466,6 +474,8 @@ def lstm_gemm_line(kt, K, W, world, device, rank):
     fl = 2.0 * M * 4 * H * Kd
     return {"ms_per_step": round(res["fused"], 5), "tflops_per_gpu": round(fl / (res["fused"] / 1e3) / 1e12, 1),
             "gemm_only_ms": round(res["gemm_only"], 5), "unfused_gemm_plus_klstm_gates_ms": round(res["unfused"], 5),
+            "gemm_with_fused_cell_ms": round(res["gemm_cell_fused"], 5),
+            "gemm_then_klstm_cell_ms": round(res["gemm_then_cell"], 5),
             "note": "gates = K-TanH (quarter 2) / K-Sigmoid applied in the tcgen05 GEMM epilogue; "
                     "bit-identical to kgemm_bf16 + klstm_gates_bf16"}
 

@@ -190,6 +190,19 @@ KT_API kt_status kgemm_lstm_gates_bf16(const uint16_t *A, const uint16_t *B, uin
                                        size_t hidden, size_t K, int tanh_quarter, kt_lut lut,
                                        void *stream);
 
+/* The LSTM step core with the cell fused into the gate GEMM's epilogue
+ * (GNMT LSTM): gates = RN_bf16(A[M, K] .
+ * B[4*hidden, K]^T) with B's rows in PyTorch's i, f, g, o blocks, then
+ * exactly klstm_cell_bf16's cell (c_next = RN32(f c_prev + i g), h_next =
+ * RN_bf16(o K-TanH_f32(c_next)), i, f, o = K-Sigmoid, g = K-TanH) -- the gate
+ * block is never written.  Bit-identical to kgemm_bf16 then klstm_cell_bf16.
+ * c_prev, c_next [M, hidden] F32, h_next [M, hidden] BF16, row-major;
+ * c_next may equal c_prev.  Requires M % 128 == 0, hidden % 64 == 0,
+ * K % 64 == 0, A, B 16-byte and c/h 32-byte aligned; KT_ERR_ARG otherwise. */
+KT_API kt_status kgemm_lstm_cell_bf16(const uint16_t *A, const uint16_t *B, const float *c_prev,
+                                      float *c_next, uint16_t *h_next, size_t M, size_t hidden,
+                                      size_t K, kt_lut lut, void *stream);
+
 /* Generic dispatcher over (op, dtype); same contract as the calls above. */
 KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size_t n,
                           kt_lut lut, void *stream);

@@ -43,7 +43,7 @@ EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_creat
                        "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count",
                        "kt_apx_create", "kt_apx_coeffs", "kt_apx_destroy", "kt_apx_tanh_bf16",
                        "kt_apx_tanh_f32", "kt_alu_probe", "kgelu_swish_bf16", "kgelu_swish_f32",
-                       "kgemm_lstm_gates_bf16")
+                       "kgemm_lstm_gates_bf16", "kgemm_lstm_cell_bf16")
 
 for _name in MAP_CALLS:
     _f = getattr(_lib, _name)
@@ -105,6 +105,8 @@ for _name in ("kgelu_swish_bf16", "kgelu_swish_f32"):
     _f.restype = ctypes.c_int
 _lib.kgemm_lstm_gates_bf16.argtypes = [_vp, _vp, _vp, _sz, _sz, _sz, ctypes.c_int, _vp, _vp]
 _lib.kgemm_lstm_gates_bf16.restype = ctypes.c_int
+_lib.kgemm_lstm_cell_bf16.argtypes = [_vp, _vp, _vp, _vp, _vp, _sz, _sz, _sz, _vp, _vp]
+_lib.kgemm_lstm_cell_bf16.restype = ctypes.c_int
 _lib.kt_alu_probe.argtypes = [ctypes.c_int, _vp, _vp, _vp, ctypes.c_int,
                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
 _lib.kt_alu_probe.restype = ctypes.c_int
@@ -522,3 +524,29 @@ def kgemm_lstm_gates_bf16(A, B, hidden: int, tanh_quarter: int = 2, out=None, lu
                                           tanh_quarter, lut.handle, _stream_ptr(stream, idx)),
                "kgemm_lstm_gates_bf16")
     return out
+
+
+def kgemm_lstm_cell_bf16(A, B, c_prev, hidden: int, c_next=None, h_next=None, lut: Lut | None = None,
+                         stream=None):
+    """Gate GEMM + fused LSTM cell: A [M, K], B [4*hidden, K] (i,f,g,o row
+    blocks) BF16, c_prev [M, hidden] F32 -> (c_next F32, h_next BF16)."""
+    import torch
+    if not (A.is_cuda and B.is_cuda and c_prev.is_cuda) or A.dtype != torch.bfloat16 \
+            or B.dtype != torch.bfloat16 or c_prev.dtype != torch.float32:
+        raise TypeError("A, B: CUDA bfloat16; c_prev: CUDA float32")
+    M, K = A.shape
+    if B.shape != (4 * hidden, K) or c_prev.numel() != M * hidden:
+        raise ValueError("A [M, K], B [4*hidden, K], c_prev [M, hidden]")
+    if not (A.is_contiguous() and B.is_contiguous() and c_prev.is_contiguous()):
+        raise ValueError("inputs must be contiguous")
+    if c_next is None:
+        c_next = torch.empty_like(c_prev)
+    if h_next is None:
+        h_next = torch.empty(c_prev.shape, dtype=torch.bfloat16, device=c_prev.device)
+    lut = lut or paper_lut()
+    idx = A.device.index
+    with _on_device(idx):
+        _check(_lib.kgemm_lstm_cell_bf16(A.data_ptr(), B.data_ptr(), c_prev.data_ptr(),
+                                         c_next.data_ptr(), h_next.data_ptr(), M, hidden, K,
+                                         lut.handle, _stream_ptr(stream, idx)), "kgemm_lstm_cell_bf16")
+    return c_next, h_next

@@ -544,6 +544,44 @@ KT_API kt_status kgemm_lstm_gates_bf16(const uint16_t *A, const uint16_t *B, uin
   return run_gemm(8, A, B, C, M, 4 * hidden, K, lut, stream, (uint32_t)hidden, (uint32_t)tanh_quarter);
 }
 
+KT_API kt_status kgemm_lstm_cell_bf16(const uint16_t *A, const uint16_t *B, const float *c_prev,
+                                      float *c_next, uint16_t *h_next, size_t M, size_t hidden,
+                                      size_t K, kt_lut lut, void *stream) {
+  if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (M == 0 || hidden == 0) return KT_OK;
+  if (M % 128 || hidden % 64 || K % 64 || K == 0)
+    return fail(KT_ERR_ARG, "needs M %% 128 == 0, hidden %% 64 == 0, K %% 64 == 0 (K > 0)");
+  if (M > (1u << 31) || 4 * hidden > (1u << 31) || K > (1u << 31)) return fail(KT_ERR_ARG, "too large");
+  if (!A || !B || !c_prev || !c_next || !h_next) return fail(KT_ERR_ARG, "NULL pointer");
+  if ((uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)c_prev % 32 || (uintptr_t)c_next % 32 ||
+      (uintptr_t)h_next % 32)
+    return fail(KT_ERR_ARG, "A, B must be 16-byte and c_prev, c_next, h_next 32-byte aligned");
+  const size_t cb = M * hidden * 4, hb = M * hidden * 2;
+  if (overlaps(c_next, c_prev, cb)) return fail(KT_ERR_ARG, "c_next overlaps c_prev without being equal");
+  const void *ins[3] = {A, B, c_prev};
+  const size_t inb[3] = {M * K * 2, 4 * hidden * K * 2, cb};
+  for (int j = 0; j < 3; ++j) {
+    const uintptr_t p0 = (uintptr_t)ins[j], p1 = p0 + inb[j];
+    const uintptr_t h0 = (uintptr_t)h_next, h1 = h0 + hb;
+    if (h0 < p1 && p0 < h1) return fail(KT_ERR_ARG, "h_next overlaps an input");
+    if (j < 2) {
+      const uintptr_t c0 = (uintptr_t)c_next, c1 = c0 + cb;
+      if (c0 < p1 && p0 < c1) return fail(KT_ERR_ARG, "c_next overlaps A or B");
+    }
+  }
+  kt::LaunchInfo li;
+  kt_status s = launch_info(&li);
+  if (s != KT_OK) return s;
+  const void *dev_ptrs[5] = {A, B, c_prev, c_next, h_next};
+  const char *names[5] = {"A", "B", "c_prev", "c_next", "h_next"};
+  for (int j = 0; j < 5; ++j)
+    if ((s = check_device_ptr(dev_ptrs[j], li.device, names[j])) != KT_OK) return s;
+  cudaError_t e = kt::launch_gemm_cell(A, B, c_prev, c_next, h_next, M, hidden, K, lut->words,
+                                       (cudaStream_t)stream, li.sm_count);
+  if (e != cudaSuccess) return cuda_fail(e, "kgemm_lstm_cell launch");
+  return KT_OK;
+}
+
 // Host-buffer strategy (KT_HOST_ZEROCOPY): 0 = copy-engine pipeline,
 // 1 = one zero-copy kernel, 2 = hybrid (copy-engine H2D, the kernel stores
 // its output straight into the mapped host buffer).  Default: see

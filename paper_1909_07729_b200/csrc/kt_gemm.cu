@@ -296,6 +296,166 @@ k_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtens
   }
 }
 
+// ------------------------------------- GEMM + fused LSTM cell (NEXT-2) ----
+// gates = RN_bf16(A[M, K] . B[4H, K]^T) with B in PyTorch's row-block order
+// (i, f, g, o), then the cell of klstm_cell_bf16 -- without writing the gate
+// block: c_next = RN32(f c_prev + i g), h_next = RN_bf16(o K-TanH_f32(c_next)),
+// i, f, o = K-Sigmoid, g = K-TanH of the BF16 gates (reading R-LSTM-CELL).
+// A tile covers 128 rows x 64 hidden units: its B operand is the four
+// 64-row boxes B[q*H + 64 nb .. +64) (q = i, f, g, o) stacked in shared
+// memory -- the same 256-row, 128-byte-swizzled layout as one 256-row box --
+// so TMEM column q*64 + u holds gate q of unit u.  Epilogue warp (lane
+// quarter, unit half) loads gates i, f, g, o of its 32 units (4 x 32 columns)
+// and c_prev of its row, and writes c_next (F32) and h_next (BF16).  The MMA
+// side is k_gemm's.  10 bytes of cell traffic per element instead of 8 (gate
+// write) + 18 (cell kernel).
+__global__ void __launch_bounds__(kGemmPThreads, 1)
+k_gemm_cell(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b64,
+            const float *c_prev, float *c_next, uint16_t *h_next, uint32_t M, uint32_t H, uint32_t K,
+            const __grid_constant__ LutWords lut) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bar = base + kStages * kStageBytes;
+  const uint32_t full_bar = bar, empty_bar = bar + 8 * kStages;
+  const uint32_t tfull_bar = bar + 16 * kStages, tempty_bar = tfull_bar + 16;
+  const uint32_t tmem_slot = tempty_bar + 16;
+  uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem_raw + (tmem_slot - raw));
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t mt = M / kBM, ntn = H / 64, ntiles = mt * ntn;
+  const uint32_t nk = K / kBK;
+
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar + 8 * a, 1);
+      mbar_init(tempty_bar + 8 * a, kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "n"(2 * kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: A box + four 64-row B boxes ----------------
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      uint32_t mb, nb;
+      tile_coords(t, mt, ntn, mb, nb);
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % kStages;
+        if (it >= (uint32_t)kStages) mbar_wait(empty_bar + 8 * s, ((it / kStages) + 1) & 1);
+        const uint32_t sa = base + s * kStageBytes, sb = sa + kABytes;
+        mbar_expect_tx(full_bar + 8 * s, kStageBytes);
+        tma_load_2d(sa, &map_a, (int)(kb * kBK), (int)(mb * kBM), full_bar + 8 * s);
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+          tma_load_2d(sb + q * (64 * kBK * 2), &map_b64, (int)(kb * kBK), (int)(q * H + nb * 64),
+                      full_bar + 8 * s);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (as k_gemm) ----------------
+    uint32_t it = 0, i = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const uint32_t a = i & 1;
+      if (i >= 2) mbar_wait(tempty_bar + 8 * a, ((i / 2) + 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t d = tmem + a * kTmemCols;
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % kStages;
+        mbar_wait(full_bar + 8 * s, (it / kStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = umma_sdesc(base + s * kStageBytes);
+        const uint64_t db = umma_sdesc(base + s * kStageBytes + kABytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          const uint32_t acc = (kb | k) != 0;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         empty_bar + 8 * s)
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       tfull_bar + 8 * a)
+                   : "memory");
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue: LSTM cell of 32 units of one row ----------------
+    const LaneLut L{lut.bf16[lane], lut.f32K[lane], lut.f32C[lane]};
+    const uint32_t q = warp & 3, half = (warp - 2) >> 2;
+    uint32_t i = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      uint32_t mb, nb;
+      tile_coords(t, mt, ntn, mb, nb);
+      const uint32_t a = i & 1;
+      const uint32_t row = mb * kBM + 32 * q + lane;
+      const size_t cbase = (size_t)row * H + nb * 64 + half * 32;     // first unit of this thread
+      uint32_t cp[4][8];                                              // c_prev, 32 floats
+#pragma unroll
+      for (int v = 0; v < 4; ++v) ld256<true>(c_prev + cbase + 8 * v, cp[v], true);
+      mbar_wait(tfull_bar + 8 * a, (i / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t r[128];                                                // i, f, g, o x 32 units
+      const uint32_t tbase = tmem + ((32 * q) << 16) + a * kTmemCols + half * 32;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) tmem_ld32(tbase + 64 * g, r + 32 * g);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar + 8 * a) : "memory");
+      uint32_t cn[4][8], h[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {                                  // units 2k, 2k + 1
+        const uint32_t gi = pack_bf16x2(__uint_as_float(r[2 * k + 1]), __uint_as_float(r[2 * k]));
+        const uint32_t gf = pack_bf16x2(__uint_as_float(r[32 + 2 * k + 1]), __uint_as_float(r[32 + 2 * k]));
+        const uint32_t gg = pack_bf16x2(__uint_as_float(r[64 + 2 * k + 1]), __uint_as_float(r[64 + 2 * k]));
+        const uint32_t go = pack_bf16x2(__uint_as_float(r[96 + 2 * k + 1]), __uint_as_float(r[96 + 2 * k]));
+        float2 cnv;
+        h[k] = lstm_cell2(gi, gf, gg, go,
+                          make_float2(__uint_as_float(cp[k >> 2][(2 * k) & 7]),
+                                      __uint_as_float(cp[k >> 2][(2 * k + 1) & 7])),
+                          cnv, L);
+        cn[k >> 2][(2 * k) & 7] = __float_as_uint(cnv.x);
+        cn[k >> 2][(2 * k + 1) & 7] = __float_as_uint(cnv.y);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) st256(c_next + cbase + 8 * v, cn[v], true);
+      uint32_t h0[8], h1[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        h0[j] = h[j];
+        h1[j] = h[8 + j];
+      }
+      st256(h_next + cbase, h0, true);
+      st256(h_next + cbase + 16, h1, true);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(2 * kTmemCols));
+  }
+}
+
 // ------------------------------------------------ CTA-pair (cta_group::2) ----
 // Two CTAs of a cluster (two SMs of one TPC) compute one 256 x 256 output
 // tile: CTA r loads rows [r*128, +128) of the A block and rows [r*128, +128)
@@ -597,6 +757,26 @@ cudaError_t launch_gemm(int epi, const uint16_t *A, const uint16_t *B, uint16_t 
   if (!make_map(&ma, A, M, K, kBM) || !make_map(&mb, B, N, K, kBN)) return cudaErrorInvalidValue;
   KT_EPIS(launch_gemm_t)
 #undef KT_EPIS
+}
+
+cudaError_t launch_gemm_cell(const uint16_t *A, const uint16_t *B, const float *c_prev, float *c_next,
+                             uint16_t *h_next, size_t M, size_t H, size_t K, const LutWords &lut,
+                             cudaStream_t s, int sms) {
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, kBM) || !make_map(&mb, B, 4 * H, K, 64)) return cudaErrorInvalidValue;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k_gemm_cell, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kGemmSmem);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const size_t tiles = (M / kBM) * (H / 64);
+  const unsigned grid = (unsigned)(tiles < (size_t)sms ? tiles : (size_t)sms);
+  k_gemm_cell<<<grid, kGemmPThreads, kGemmSmem, s>>>(ma, mb, c_prev, c_next, h_next, (uint32_t)M,
+                                                     (uint32_t)H, (uint32_t)K, lut);
+  count_launch();
+  return cudaGetLastError();
 }
 
 }  // namespace kt

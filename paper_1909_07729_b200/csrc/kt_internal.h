@@ -74,6 +74,12 @@ cudaError_t launch_gemm(int epi, const uint16_t *A, const uint16_t *B, uint16_t 
                         size_t N, size_t K, const LutWords &lut, cudaStream_t s, int sms,
                         uint32_t lstm_hidden = 0, uint32_t lstm_tq = 0);
 
+// tcgen05 GEMM with the LSTM cell fused into its epilogue (B in i,f,g,o
+// row blocks of H rows; H % 64 == 0, M % 128 == 0, K % 64 == 0).
+cudaError_t launch_gemm_cell(const uint16_t *A, const uint16_t *B, const float *c_prev, float *c_next,
+                             uint16_t *h_next, size_t M, size_t H, size_t K, const LutWords &lut,
+                             cudaStream_t s, int sms);
+
 void count_launch();
 bool pdl_enabled();        // KT_PDL != 0
 bool prefetch_enabled();   // KT_PREFETCH != 0 (and PDL on)

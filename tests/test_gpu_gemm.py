@@ -138,3 +138,34 @@ def test_gemm_lstm_gates_bad_args(kt):
     A, B = rand_bf16((128, 64), 13), rand_bf16((4 * 256, 64), 14)
     with pytest.raises(kt.KTanhError):
         kt.kgemm_lstm_gates_bf16(A, B, 256, 4)          # bad quarter
+
+
+@pytest.mark.parametrize("M,H,K", [(128, 64, 64), (256, 192, 320), (6400, 1024, 1024), (384, 128, 128)])
+def test_gemm_lstm_cell_fused(kt, M, H, K):
+    """kgemm_lstm_cell_bf16 == kgemm_bf16 then klstm_cell_bf16 (bitwise), and
+    the oracle's cell on the BF16 gate block; c_next in place over c_prev."""
+    A, B = rand_bf16((M, K), 21, 0.4), rand_bf16((4 * H, K), 22, 0.4)
+    g = torch.Generator(device="cuda").manual_seed(23)
+    c = torch.randn(M, H, device="cuda", generator=g) * 2
+    cn, hn = kt.kgemm_lstm_cell_bf16(A, B, c, H)
+    gates = kt.kgemm_bf16(A, B)
+    cn_ref, hn_ref = kt.klstm_cell_bf16(gates, c, H)
+    torch.cuda.synchronize()
+    assert torch.equal(cn.view(torch.int32), cn_ref.view(torch.int32)), "c_next"
+    assert torch.equal(hn.view(torch.int16), hn_ref.view(torch.int16)), "h_next"
+    if M * H <= 1 << 17:
+        wc, wh = O.lstm_cell_bf16(u16(gates), c.view(torch.int32).cpu().numpy().view(np.uint32), H)
+        assert np.array_equal(cn.view(torch.int32).cpu().numpy().view(np.uint32).reshape(-1), wc)
+        assert np.array_equal(u16(hn).reshape(-1), wh)
+    c2 = c.clone()
+    cn2, hn2 = kt.kgemm_lstm_cell_bf16(A, B, c2, H, c_next=c2)        # in place
+    torch.cuda.synchronize()
+    assert torch.equal(cn2.view(torch.int32), cn_ref.view(torch.int32))
+    assert torch.equal(hn2.view(torch.int16), hn_ref.view(torch.int16))
+
+
+def test_gemm_lstm_cell_bad_args(kt):
+    A, B = rand_bf16((128, 64), 24), rand_bf16((4 * 96, 64), 25)
+    c = torch.zeros(128, 96, device="cuda")
+    with pytest.raises(kt.KTanhError):
+        kt.kgemm_lstm_cell_bf16(A, B, c, 96)                             # hidden % 64 != 0
