@@ -66,3 +66,35 @@ def test_gemm_guards(kt):
     torch.cuda.synchronize()
     b = buf.float().cpu().numpy()
     assert np.all(b[:4096] == -7.0) and np.all(b[4096 + M * N:] == -7.0)
+
+
+@pytest.mark.parametrize("epi", [None, "gelu"])
+def test_gemm_pair_guards(kt, epi):
+    """CTA-pair kernel (M % 256 == 0) writes nothing outside C."""
+    M, N, K = 512, 768, 128
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    buf = torch.full((M * N + 2 * 4096,), -7.0, dtype=torch.bfloat16, device="cuda")
+    C = buf[4096:4096 + M * N].view(M, N)
+    kt.kgemm_bf16(A, B, epilogue=epi, out=C)
+    torch.cuda.synchronize()
+    b = buf.float().cpu().numpy()
+    assert np.all(b[:4096] == -7.0) and np.all(b[4096 + M * N:] == -7.0)
+
+
+def test_gemm_lstm_guards(kt):
+    """Fused gate GEMM and GEMM + cell write only their outputs."""
+    M, H, K = 256, 256, 128
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(4 * H, K, device="cuda").to(torch.bfloat16)
+    gbuf = torch.full((M * 4 * H + 2 * 4096,), -7.0, dtype=torch.bfloat16, device="cuda")
+    kt.kgemm_lstm_gates_bf16(A, B, H, 2, out=gbuf[4096:4096 + M * 4 * H].view(M, 4 * H))
+    cbuf = torch.full((M * H + 2 * 4096,), -7.0, dtype=torch.float32, device="cuda")
+    hbuf = torch.full((M * H + 2 * 4096,), -7.0, dtype=torch.bfloat16, device="cuda")
+    c = torch.randn(M, H, device="cuda")
+    kt.kgemm_lstm_cell_bf16(A, B, c, H, c_next=cbuf[4096:4096 + M * H].view(M, H),
+                            h_next=hbuf[4096:4096 + M * H].view(M, H))
+    torch.cuda.synchronize()
+    for buf, n in ((gbuf, M * 4 * H), (cbuf, M * H), (hbuf, M * H)):
+        b = buf.float().cpu().numpy()
+        assert np.all(b[:4096] == -7.0) and np.all(b[4096 + n:] == -7.0)
