@@ -9,7 +9,12 @@ epi = sys.argv[4] if len(sys.argv) > 4 and sys.argv[4] != "none" else None
 A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
 B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
 C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-for _ in range(4):
+if epi == "cell":            # N = 4 * hidden: GEMM + fused LSTM cell
+    c = torch.randn(M, N // 4, device="cuda")
+    for _ in range(4):
+        kt.kgemm_lstm_cell_bf16(A, B, c, N // 4)
+else:
+  for _ in range(4):
     kt.kgemm_bf16(A, B, epilogue=epi, out=C)
 torch.cuda.synchronize()
 print("ok", flush=True)
