@@ -147,16 +147,20 @@ __device__ __forceinline__ uint32_t ktanh_bf16x2(uint32_t x, uint32_t lw) {
 }
 
 // Algorithm 1 on one F32 (native reading A8).  lk = f32K[lane], lc = f32C[lane].
+// The region tests compare u << 1 (|x| shifted up, sign dropped -- it is the
+// umulhi operand anyway, computed on the FMA pipe) instead of masking |x|:
+// bypass (|x| < T1 or NaN) is ONE unsigned range test
+// (u2 - 2 T1) > (2 inf - 2 T1); the sign is ORed in once after the
+// saturation select.  6 ALU-pipe ops instead of 10.
 __device__ __forceinline__ uint32_t ktanh_f32(uint32_t u, uint32_t lk, uint32_t lc) {
-  const uint32_t mag = u & 0x7fffffffu;
-  const uint32_t s = u & 0x80000000u;
   const uint32_t K = shfl_lut(lk, u >> 20);        // line 6-7, t = bits [24:20]
   const uint32_t C = shfl_lut(lc, u >> 20);
-  const uint32_t ym = __umulhi(u << 1, K) + C;     // line 8: C_t + (|x| >> r_t)
-  uint32_t y = s | ym;
-  y = (mag > kT2f) ? (s | 0x3F800000u) : y;        // line 4 (NaN overridden below)
-  y = (mag < kT1f || mag > kInff) ? u : y;         // line 3, NaN passthrough (A6)
-  return y;
+  const uint32_t u2 = u << 1;
+  const uint32_t ym = __umulhi(u2, K) + C;         // line 8: C_t + (|x| >> r_t)
+  uint32_t y = (u2 > (kT2f << 1)) ? 0x3F800000u : ym;                  // line 4
+  y |= u & 0x80000000u;                                                // s_o = s_i
+  const bool byp = (u2 - (kT1f << 1)) > ((kInff << 1) - (kT1f << 1));  // line 3, or NaN (A6)
+  return byp ? u : y;
 }
 
 // ------------------------------------------------------- derived (Sec. 1) --
