@@ -566,6 +566,8 @@ def main():
     K, W = args.steps, args.warmup
     head_key, head_op = "c2_bf16_2p24", "ktanh_bf16"
     step = Step(kt, head_key, head_op, device, rank)
+    import hashlib
+    input_sha = hashlib.sha256(step.xs[0].view(torch.int16).cpu().numpy().tobytes()).hexdigest()
     windows, clk, lps = time_windows(step, K, W, world, device, clocks)
     ms_win = statistics.median(windows)
     ms = ms_win / K
@@ -657,6 +659,7 @@ def main():
             "ms_per_step": round(ms, 6), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "config": {"workload": head_key, "desc": WL.CONFIGS[head_key].desc,
+                       "input_sha256": input_sha,
                        "elements_per_gpu": WL.CONFIGS[head_key].numel, "call": head_op,
                        "parallelism": f"{world} independent shards (seed+rank), no collective",
                        "l2": f"{sets} rotating input/output sets ({sets * 4 * WL.CONFIGS[head_key].numel >> 20} MiB > 4x L2)",
