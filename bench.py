@@ -164,6 +164,11 @@ class Step:
 
     def _bind(self):
         kt, op = self.kt, self.op
+        if op == "ktanh64_bf16":              # 64-interval kernel, Table 1 split in halves
+            E32, r32, b32 = kt.paper_lut().tables()
+            t64 = [(((t >> 4) << 3) | ((t & 15) >> 1)) for t in range(64)]
+            h = kt.Lut64([E32[i] for i in t64], [r32[i] for i in t64], [b32[i] for i in t64])
+            return lambda x, y: kt.ktanh64_bf16(x, h, out=y)
         if op.startswith("apx:"):             # Table 2 comparator "apx:<kind>:<p>:<q>"
             _, kind, p, q = op.split(":")
             apx = kt.Apx(kind, int(p), int(q))
@@ -415,7 +420,7 @@ KERNEL_NAME = {"ktanh_bf16": "k_map<0, 0, true>", "ktanh_f32": "k_map<0, 1, true
                "kgelu_bf16": "k_map<3, 0, true>", "kswish_bf16": "k_map<2, 0, true>",
                "lstm": "k_lstm<true>"}
 
-EXTRA = [("c3_f32_2p28", "ktanh_f32"), ("c3_f32_2p28", "ktanh_f32_via_bf16"), ("c4_lstm_gates", "lstm"),
+EXTRA = [("c2_bf16_2p24", "ktanh64_bf16"), ("c3_f32_2p28", "ktanh_f32"), ("c3_f32_2p28", "ktanh_f32_via_bf16"), ("c4_lstm_gates", "lstm"),
          ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16"),
          ("c5_ffn_2p30", "kgelu_swish_bf16"), ("c5_ffn_2p30", "kgelu_bwd_bf16"),
          ("c4_lstm_gates", "lstm_cell")]

@@ -96,6 +96,17 @@ KT_API kt_status kt_lut_get(kt_lut lut, int32_t E[32], int32_t r[32], int32_t b[
 /* Release a handle; NULL is a no-op. */
 KT_API void kt_lut_destroy(kt_lut lut);
 
+/* 64-interval tables ("we can use 64 entries by choosing 4
+ * bits of mantissa").  Index t = ((E & 3) << 4) | (M >> 3)
+ * (2 exponent LSBs, 4 mantissa MSBs); validation as kt_lut_create with the
+ * 8-mantissa intervals m in [8v, 8v + 7], v = t & 15.  A separate handle
+ * type: only ktanh64_bf16 takes it. */
+typedef struct kt_lut64_s *kt_lut64;
+KT_API kt_status kt_lut64_create(const int32_t E[64], const int32_t r[64], const int32_t b[64],
+                                 kt_lut64 *out);
+KT_API kt_status kt_lut64_get(kt_lut64 lut, int32_t E[64], int32_t r[64], int32_t b[64]);
+KT_API void kt_lut64_destroy(kt_lut64 lut);   /* NULL-safe */
+
 /* ---------------------------------------------------------------------- */
 /* Elementwise maps over device memory (conventions above).               */
 /* ---------------------------------------------------------------------- */
@@ -103,6 +114,10 @@ KT_API void kt_lut_destroy(kt_lut lut);
 /* K-TanH, Algorithm 1 on BF16 bit patterns.  Bit-exact
  * with the paper's algorithm; NaN passes through unchanged (A6). */
 KT_API kt_status ktanh_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream);
+
+/* K-TanH (Algorithm 1) on BF16 with a 64-interval table: lane i holds
+ * entries i and 32 + i, both shuffled, one selected by bit 5 of t. */
+KT_API kt_status ktanh64_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut64 lut, void *stream);
 
 /* K-TanH on F32, native reading A8 ("compatible with multiple
  * such data formats"): same thresholds and 5-bit index (E & 3, top 3

@@ -43,7 +43,8 @@ EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_creat
                        "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count",
                        "kt_apx_create", "kt_apx_coeffs", "kt_apx_destroy", "kt_apx_tanh_bf16",
                        "kt_apx_tanh_f32", "kt_alu_probe", "kgelu_swish_bf16", "kgelu_swish_f32",
-                       "kgemm_lstm_gates_bf16", "kgemm_lstm_cell_bf16")
+                       "kgemm_lstm_gates_bf16", "kgemm_lstm_cell_bf16", "kt_lut64_create",
+                       "kt_lut64_get", "kt_lut64_destroy", "ktanh64_bf16")
 
 for _name in MAP_CALLS:
     _f = getattr(_lib, _name)
@@ -103,6 +104,14 @@ for _name in ("kgelu_swish_bf16", "kgelu_swish_f32"):
     _f = getattr(_lib, _name)
     _f.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
     _f.restype = ctypes.c_int
+_lib.kt_lut64_create.argtypes = [_c_i32p, _c_i32p, _c_i32p, ctypes.POINTER(_vp)]
+_lib.kt_lut64_create.restype = ctypes.c_int
+_lib.kt_lut64_get.argtypes = [_vp, _c_i32p, _c_i32p, _c_i32p]
+_lib.kt_lut64_get.restype = ctypes.c_int
+_lib.kt_lut64_destroy.argtypes = [_vp]
+_lib.kt_lut64_destroy.restype = None
+_lib.ktanh64_bf16.argtypes = [_vp, _vp, _sz, _vp, _vp]
+_lib.ktanh64_bf16.restype = ctypes.c_int
 _lib.kgemm_lstm_gates_bf16.argtypes = [_vp, _vp, _vp, _sz, _sz, _sz, ctypes.c_int, _vp, _vp]
 _lib.kgemm_lstm_gates_bf16.restype = ctypes.c_int
 _lib.kgemm_lstm_cell_bf16.argtypes = [_vp, _vp, _vp, _vp, _vp, _sz, _sz, _sz, _vp, _vp]
@@ -550,3 +559,42 @@ def kgemm_lstm_cell_bf16(A, B, c_prev, hidden: int, c_next=None, h_next=None, lu
                                          c_next.data_ptr(), h_next.data_ptr(), M, hidden, K,
                                          lut.handle, _stream_ptr(stream, idx)), "kgemm_lstm_cell_bf16")
     return c_next, h_next
+
+
+class Lut64:
+    """64-interval parameter table, for ktanh64_bf16."""
+
+    def __init__(self, E, r, b):
+        if any(len(a) != 64 for a in (E, r, b)):
+            raise ValueError("tables must have 64 entries")
+        arr = [(ctypes.c_int32 * 64)(*[int(v) for v in a]) for a in (E, r, b)]
+        h = _vp()
+        _check(_lib.kt_lut64_create(arr[0], arr[1], arr[2], ctypes.byref(h)), "kt_lut64_create")
+        self._h = h
+
+    def tables(self):
+        E, r, b = ((ctypes.c_int32 * 64)() for _ in range(3))
+        _check(_lib.kt_lut64_get(self._h, E, r, b), "kt_lut64_get")
+        return list(E), list(r), list(b)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        lib = globals().get("_lib")
+        if h is not None and h.value and lib is not None:
+            lib.kt_lut64_destroy(h)
+            self._h = _vp()
+
+
+def ktanh64_bf16(x, lut64: Lut64, out=None, stream=None):
+    """K-TanH on BF16 with a 64-interval table (C ABI ktanh64_bf16)."""
+    import torch
+    out = _prep(x, out, torch.bfloat16)
+    idx = x.device.index
+    with _on_device(idx):
+        _check(_lib.ktanh64_bf16(x.data_ptr(), out.data_ptr(), x.numel(), lut64.handle,
+                                 _stream_ptr(stream, idx)), "ktanh64_bf16")
+    return out

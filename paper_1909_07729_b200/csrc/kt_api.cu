@@ -23,6 +23,11 @@ struct kt_lut_s {
   kt::LutWords words;
 };
 
+struct kt_lut64_s {
+  int32_t E[64], r[64], b[64];
+  kt::LutWords64 words;
+};
+
 struct kt_apx_s {
   double coef[kt::kApxCoef];
   kt::ApxWords words;
@@ -291,6 +296,62 @@ KT_API kt_status kt_lut_get(kt_lut lut, int32_t E[32], int32_t r[32], int32_t b[
 }
 
 KT_API void kt_lut_destroy(kt_lut lut) { delete lut; }
+
+// ---- 64-interval tables -------------------
+// Index t = ((E & 3) << 4) | (M >> 3): entry t covers the 8 mantissas
+// m in [8v, 8v + 7], v = t & 15, of input exponent E_in(t) = 125 + (((t >> 4)
+// + 3) & 3); for E_in = 128 only m <= 0x70 (|x| <= T2) is reachable.
+KT_API kt_status kt_lut64_create(const int32_t E[64], const int32_t r[64], const int32_t b[64],
+                                 kt_lut64 *out) {
+  if (!E || !r || !b || !out) return fail(KT_ERR_ARG, "NULL argument");
+  kt_lut64_s tmp;
+  for (int t = 0; t < 64; ++t) {
+    if (r[t] < 0 || r[t] > 7) return fail(KT_ERR_LUT, "r[%d] = %d outside [0, 7]", t, r[t]);
+    if (E[t] < 1 || E[t] > 127) return fail(KT_ERR_LUT, "E[%d] = %d outside [1, 127]", t, E[t]);
+    const int ei = 125 + (((t >> 4) + 3) & 3);
+    const int v = t & 15;
+    int lo = 8 * v, hi = 8 * v + 7;
+    if (ei == 128) hi = hi < 0x70 ? hi : 0x70;   // only |x| <= 3.75 reaches the table
+    for (int m = lo; m <= hi; ++m) {
+      const int mo = (m >> r[t]) + b[t];
+      if (mo < 0 || mo > 127)
+        return fail(KT_ERR_LUT, "entry %d: (m=%d >> r=%d) + b=%d = %d leaves [0, 127]", t, m, r[t],
+                    b[t], mo);
+      if (E[t] == 127 && mo != 0)
+        return fail(KT_ERR_LUT, "entry %d: E=127 with M_o=%d != 0 gives |y| > 1", t, mo);
+    }
+    tmp.E[t] = E[t];
+    tmp.r[t] = r[t];
+    tmp.b[t] = b[t];
+    const int32_t d16 = (E[t] << 7) + b[t] - (1 << (7 - r[t]));
+    tmp.words.w[t] = ((uint32_t)(ei + 16 + r[t]) << 23) | ((uint32_t)d16 & 0xFFFFu);
+  }
+  kt_lut64_s *L = new (std::nothrow) kt_lut64_s(tmp);
+  if (!L) return fail(KT_ERR_ARG, "out of host memory");
+  *out = L;
+  return KT_OK;
+}
+
+KT_API kt_status kt_lut64_get(kt_lut64 lut, int32_t E[64], int32_t r[64], int32_t b[64]) {
+  if (!lut || !E || !r || !b) return fail(KT_ERR_ARG, "NULL argument");
+  memcpy(E, lut->E, sizeof(lut->E));
+  memcpy(r, lut->r, sizeof(lut->r));
+  memcpy(b, lut->b, sizeof(lut->b));
+  return KT_OK;
+}
+
+KT_API void kt_lut64_destroy(kt_lut64 lut) { delete lut; }
+
+KT_API kt_status ktanh64_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut64 lut, void *stream) {
+  if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (n == 0) return KT_OK;
+  kt::LaunchInfo li;
+  kt_status s = check_buffers(x, y, n, 2, &li);
+  if (s != KT_OK) return s;
+  cudaError_t e = kt::launch_map64(x, y, n, lut->words, (cudaStream_t)stream, li);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return KT_OK;
+}
 
 KT_API kt_status ktanh_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream) {
   return run_map(kt::OP_TANH, kt::FMT_BF16, x, y, n, lut, stream);

@@ -146,6 +146,30 @@ __device__ __forceinline__ uint32_t ktanh_bf16x2(uint32_t x, uint32_t lw) {
   return o | (x & kSignx2);                        // s_o = s_i
 }
 
+// Algorithm 1 with the 64-interval table of PAPER.md:223 (4 mantissa index
+// bits): t = (E & 3) : (M >> 3) = bits [8:3] of each half.
+// Lane i holds entries i (w0) and 32 + i (w1); both are shuffled from lane
+// t & 31 and bit 5 of t (bit 8 of the half) picks one.  The words have the
+// same form as the 32-entry ones (the RZ-add identity does not depend on the
+// number of index bits).
+__device__ __forceinline__ uint32_t ktanh64_bf16x2(uint32_t x, uint32_t w0, uint32_t w1) {
+  const uint32_t il = x >> 3, ih = x >> 19;
+  const uint32_t l0 = shfl_lut(w0, il), l1 = shfl_lut(w1, il);
+  const uint32_t h0 = shfl_lut(w0, ih), h1 = shfl_lut(w1, ih);
+  const uint32_t Ll = (x & 0x100u) ? l1 : l0;
+  const uint32_t Lh = (x & 0x1000000u) ? h1 : h0;
+  const float ql = __fadd_rz(fabsf(__uint_as_float(x << 16)), __uint_as_float(Ll));
+  const float qh = __fadd_rz(fabsf(__uint_as_float(x)), __uint_as_float(Lh));
+  const uint32_t ymag = __byte_perm(__float_as_uint(ql), __float_as_uint(qh), 0x5410);
+  uint32_t mag;
+  asm("abs.bf16x2 %0, %1;" : "=r"(mag) : "r"(x));
+  const uint32_t byp = hset2_ltu(mag, kT1x2);
+  const uint32_t sat = hset2_gt(mag, kT2x2);
+  const uint32_t m = bsel(sat, kOnex2, ymag);
+  const uint32_t o = bsel(byp, x, m);
+  return o | (x & kSignx2);
+}
+
 // Algorithm 1 on one F32 (native reading A8).  lk = f32K[lane], lc = f32C[lane].
 // The region tests compare u << 1 (|x| shifted up, sign dropped -- it is the
 // umulhi operand anyway, computed on the FMA pipe) instead of masking |x|:

@@ -33,6 +33,12 @@ struct LutWords {
   uint32_t f32C[32];
 };
 
+// 64-interval table: per-entry words of the same form as
+// LutWords::bf16, entry t in w[t] (lane i loads w[i] and w[32 + i]).
+struct LutWords64 {
+  uint32_t w[64];
+};
+
 enum Op { OP_TANH = 0, OP_SIGMOID = 1, OP_SWISH = 2, OP_GELU = 3,
           OP_TANH_VIA_BF16 = 4 /* F32 only: RNE to BF16, Alg. 1, widen (NEXT-3) */ };
 enum Fmt { FMT_BF16 = 0, FMT_F32 = 1 };
@@ -47,6 +53,10 @@ struct LaunchInfo {
 // the kernel over PCIe (kt_apply_host's zero-copy path): no L2 prefetch.
 cudaError_t launch_map(int op, int fmt, const void *x, void *y, size_t n, const LutWords &lut,
                        cudaStream_t s, const LaunchInfo &li, bool sysmem = false);
+
+// K-TanH BF16 with a 64-entry table (x, y as for launch_map).
+cudaError_t launch_map64(const void *x, void *y, size_t n, const LutWords64 &lut, cudaStream_t s,
+                         const LaunchInfo &li);
 
 // Backward: dx = dy * g(a) (a = saved output for tanh/sigmoid, input x for
 // swish/gelu); reading R-BWD.

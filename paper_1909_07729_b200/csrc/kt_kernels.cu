@@ -142,6 +142,70 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
   }
 }
 
+// ---- K-TanH BF16 with the 64-interval table (NEXT-3) -------------------------
+// Same streaming shape as k_map (flat, 256-bit, PDL, first-wave L2 prefetch).
+__device__ __forceinline__ void span64(const uint8_t *xp, uint8_t *yp, uint32_t cnt, uint32_t w0,
+                                       uint32_t w1) {
+  const uint32_t lane = threadIdx.x & 31;
+  const bool on = lane < cnt;
+  const uint32_t v = on ? reinterpret_cast<const uint16_t *>(xp)[lane] : 0u;
+  const uint32_t r = ktanh64_bf16x2(v, w0, w1);
+  if (on) reinterpret_cast<uint16_t *>(yp)[lane] = (uint16_t)r;
+}
+
+template <bool NC>
+__global__ void __launch_bounds__(kThreads)
+k_map64(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail, uint32_t pf_blocks,
+        const __grid_constant__ LutWords64 lut) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w0 = lut.w[lane], w1 = lut.w[32 + lane];
+  const uint8_t *xb = x + (size_t)head * 2;
+  uint8_t *yb = y + (size_t)head * 2;
+  const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (NC && blockIdx.x < pf_blocks && lane == 0 && c * kChunkVecs < nvec) {
+    const uint64_t left = nvec - c * kChunkVecs;
+    prefetch_l2(xb + c * kChunkVecs * kVecBytes,
+                (uint32_t)((left < kChunkVecs ? left : kChunkVecs) * kVecBytes));
+  }
+  pdl_enter();
+  const uint64_t base = c * kChunkVecs + lane;
+  uint32_t v[kUnroll][8];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t i = base + (uint64_t)u * 32;
+    ld256<NC>(xb + i * kVecBytes, v[u], i < nvec);
+  }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[u][j] = ktanh64_bf16x2(v[u][j], w0, w1);
+  }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t i = base + (uint64_t)u * 32;
+    st256(yb + i * kVecBytes, v[u], i < nvec);
+  }
+  if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
+    span64(x, y, head, w0, w1);
+    const size_t toff = ((size_t)head + (size_t)nvec * 16) * 2;
+    span64(x + toff, y + toff, tail, w0, w1);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_map64_elem(const uint8_t *x, uint8_t *y, uint64_t n, const __grid_constant__ LutWords64 lut) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t w0 = lut.w[lane], w1 = lut.w[32 + lane];
+  asm volatile("" : "+r"(w0), "+r"(w1));
+  pdl_enter();
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t c = warp0; c < (n + 31) / 32; c += nwarps) {
+    const uint64_t off = c * 32, rem = n - off;
+    span64(x + off * 2, y + off * 2, (uint32_t)(rem < 32 ? rem : 32), w0, w1);
+  }
+}
+
 // ---- fused K-GELU + K-Swish over one input (config 5, reading A20) -----------
 // Config 5 applies both derived activations to the same FFN tensor; one pass
 // that reads x once and writes both outputs moves 6 B per BF16 element
@@ -625,6 +689,33 @@ cudaError_t launch_bwd(int op, int fmt, const void *a, const void *dy, void *dx,
   KT_CASE(OP_GELU, FMT_F32)
 #undef KT_CASE
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_map64(const void *x, void *y, size_t n, const LutWords64 &lut, cudaStream_t s,
+                         const LaunchInfo &li) {
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+  const uint8_t *xp = static_cast<const uint8_t *>(x);
+  uint8_t *yp = static_cast<uint8_t *>(y);
+  if ((xa % kVecBytes) != (ya % kVecBytes)) {
+    static const int bps = resident_blocks(k_map64_elem);
+    const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
+    return launch(k_map64_elem, grid, s, xp, yp, (uint64_t)n, lut);
+  }
+  const size_t mis = xa % kVecBytes;
+  size_t head = mis ? (kVecBytes - mis) / 2 : 0;
+  if (head > n) head = n;
+  const size_t body = n - head;
+  const uint64_t nvec = body / 16;
+  const uint32_t tail = (uint32_t)(body - nvec * 16);
+  const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+  if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  const unsigned grid = flat_grid(nchunks);
+  if (x != y) {
+    static const int bps = resident_blocks(k_map64<true>);
+    const uint32_t pf = prefetch_enabled() ? (uint32_t)(li.sm_count * bps) : 0u;
+    return launch(k_map64<true>, grid, s, xp, yp, (uint32_t)head, nvec, tail, pf, lut);
+  }
+  return launch(k_map64<false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, lut);
 }
 
 template <int FMT>

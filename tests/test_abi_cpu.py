@@ -203,3 +203,24 @@ def test_gelu_swish_fused_argument_errors(kt):
     assert lib.kgelu_swish_bf16(x, a, b, 64, lut.handle, None) == kt.KT_ERR_ARG   # outputs overlap
     assert lib.kgelu_swish_bf16(x, ctypes.c_void_p(0x10010), b, 64, lut.handle, None) == kt.KT_ERR_ARG
     assert lib.kgelu_swish_bf16(x, a, ctypes.c_void_p(0x30000), 64, None, None) == kt.KT_ERR_ARG
+
+
+def test_lut64_roundtrip_and_validation(kt):
+    """64-interval tables: the Sec. 2.4 optimizer's s = 4 table
+    is accepted and round-trips; out-of-bounds entries are KT_ERR_LUT."""
+    L4, _ = O.build_lut_s(4)
+    h = kt.Lut64(L4.E, L4.r, L4.b)
+    E, r, b = h.tables()
+    assert E == list(L4.E) and r == list(L4.r) and b == list(L4.b)
+    bad_b = list(L4.b)
+    t = 20                                      # v = 4: m in [32, 39]
+    bad_b[t] = 127 - (32 >> L4.r[t]) + 1        # M_o = 128 for m = 32
+    with pytest.raises(kt.KTanhError) as e:
+        kt.Lut64(L4.E, L4.r, bad_b)
+    assert e.value.status == kt.KT_ERR_LUT
+    with pytest.raises(kt.KTanhError):
+        kt.Lut64(L4.E, [8] * 64, L4.b)          # r > 7
+    with pytest.raises(ValueError):
+        kt.Lut64(L4.E[:32], L4.r[:32], L4.b[:32])
+    assert kt._lib.ktanh64_bf16(None, None, 0, h.handle, None) == kt.KT_OK
+    assert kt._lib.ktanh64_bf16(None, None, 16, h.handle, None) == kt.KT_ERR_ARG

@@ -531,3 +531,70 @@ def test_apply_host_cross_stream(kt, shared_work):
             assert_bitexact(y.view(torch.int16).numpy().view(np.uint16), want, 16,
                             ctx=f"cross-stream shared={shared_work} n={x.numel()}")
             y.fill_(float("nan"))
+
+
+# ----------------------------------------------- 64-interval tables (NEXT-3) ----
+@pytest.fixture(scope="module")
+def lut64(kt):
+    L4, _ = O.build_lut_s(4)
+    return L4, kt.Lut64(L4.E, L4.r, L4.b)
+
+
+def test_ktanh64_exhaustive(kt, lut64):
+    """ktanh64_bf16 with the s = 4 optimizer table: bit-exact vs the oracle's
+    64-interval Alg. 1 on every BF16 pattern (NaN passes through)."""
+    L4, h = lut64
+    x = WL.make_input("c1_exhaustive_bf16", device="cuda")
+    y = kt.ktanh64_bf16(x, h)
+    torch.cuda.synchronize()
+    assert_bitexact(u16(y), O.map_bf16("tanh", u16(x), L4), 16, ctx="ktanh64 exhaustive")
+
+
+@pytest.mark.parametrize("n,xoff,yoff", [(1, 0, 0), (33, 1, 1), (1000003, 5, 5), (4099, 1, 2)])
+def test_ktanh64_ragged(kt, lut64, n, xoff, yoff):
+    L4, h = lut64
+    base = (torch.randn(n + 64, device="cuda") * 2).to(torch.bfloat16)
+    x = base[xoff:xoff + n]
+    ybuf = torch.full((n + 64,), float("nan"), dtype=torch.bfloat16, device="cuda")
+    y = ybuf[yoff:yoff + n]
+    kt.ktanh64_bf16(x, h, out=y)
+    torch.cuda.synchronize()
+    assert_bitexact(u16(y), O.map_bf16("tanh", u16(x), L4), 16, ctx=f"ktanh64 n={n}")
+    yb = u16(ybuf)
+    assert np.all((yb[:yoff] & 0x7FFF) > 0x7F80) and np.all((yb[yoff + n:] & 0x7FFF) > 0x7F80)
+
+
+def test_ktanh64_config2_and_random_tables(kt, lut64):
+    """Config 2 at full size (oracle table lookup) and random valid 64-entry
+    tables (r in 0..7, b within the Sec. 2.4 bounds with s = 4)."""
+    L4, h = lut64
+    x = WL.make_input("c2_bf16_2p24", device="cuda")
+    y = kt.ktanh64_bf16(x, h)
+    table = torch.from_numpy(O.map_bf16("tanh", O.all_bf16(), L4).view(np.int16).copy()).cuda()
+    want = table[x.view(torch.int16).to(torch.int32) & 0xFFFF]
+    assert torch.equal(y.view(torch.int16), want)
+    rng = np.random.default_rng(64)
+    xa = WL.make_input("c1_exhaustive_bf16", device="cuda")
+    for _ in range(3):
+        E, r, b = L4.E.copy(), L4.r.copy(), L4.b.copy()
+        for t in range(64):
+            r[t] = rng.integers(0, 8)
+            lo, hi = O.bounds_s(int(r[t]), t & 15, 4)
+            if (t >> 4) == 0 and (t & 15) == 14:
+                hi = 127 - (112 >> int(r[t]))
+            b[t] = rng.integers(lo, hi + 1)
+            E[t] = rng.integers(100, 127)
+        L = O.Lut(E, r, b)
+        hh = kt.Lut64(E, r, b)
+        assert_bitexact(u16(kt.ktanh64_bf16(xa, hh)), O.map_bf16("tanh", u16(xa), L), 16,
+                        ctx="ktanh64 random table")
+
+
+def test_ktanh64_with_split_table1_equals_ktanh(kt):
+    """Table 1 split into 64 intervals (each 32-entry interval's (E, r, b) on
+    both of its halves) gives exactly the 32-entry K-TanH on every pattern."""
+    E32, r32, b32 = kt.paper_lut().tables()
+    t64 = [(((t >> 4) << 3) | ((t & 15) >> 1)) for t in range(64)]
+    h = kt.Lut64([E32[i] for i in t64], [r32[i] for i in t64], [b32[i] for i in t64])
+    x = WL.make_input("c1_exhaustive_bf16", device="cuda")
+    assert torch.equal(kt.ktanh64_bf16(x, h).view(torch.int16), kt.ktanh_bf16(x).view(torch.int16))
