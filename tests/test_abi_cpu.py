@@ -133,7 +133,7 @@ def test_product_and_oracle_do_not_import_each_other():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 for m in imp.finditer(open(os.path.join(dp, f)).read()):
                     assert "oracle" not in "".join(g or "" for g in m.groups()), (f, m.group(0))
-    for f in ("ktanh_oracle.c", "__init__.py"):
+    for f in ("ktanh_oracle.c", "apx_oracle.c", "__init__.py"):
         for m in imp.finditer(open(os.path.join(ROOT, "oracle", f)).read()):
             tgt = "".join(g or "" for g in m.groups())
             assert "paper_1909_07729_b200" not in tgt and "ktanh.h" not in tgt and "kt_" not in tgt
@@ -224,3 +224,77 @@ def test_lut64_roundtrip_and_validation(kt):
         kt.Lut64(L4.E[:32], L4.r[:32], L4.b[:32])
     assert kt._lib.ktanh64_bf16(None, None, 0, h.handle, None) == kt.KT_OK
     assert kt._lib.ktanh64_bf16(None, None, 16, h.handle, None) == kt.KT_ERR_ARG
+
+
+
+# --------------------------------------------------------------------------
+# Property-based checks of the host logic (hypothesis)
+# --------------------------------------------------------------------------
+from hypothesis import given, settings, strategies as st
+
+
+@settings(max_examples=300, deadline=None)
+@given(n=st.integers(0, 1 << 40), world=st.integers(1, 64), align=st.integers(1, 4096))
+def test_shard_range_properties(kt, n, world, align):
+    """kt_shard_range: the shards tile [0, n) in rank order, every non-empty
+    shard starts on a multiple of `align`, and no shard exceeds
+    ceil(n / world) rounded up to `align`."""
+    cap = -(-(-(-n // world)) // align) * align
+    pos = 0
+    for rank in range(world):
+        b, c = kt.shard_range(n, world, rank, align)
+        assert b == pos or c == 0
+        assert c == 0 or b % align == 0
+        assert c <= cap
+        pos = b + c if c else pos
+    assert pos == n
+
+
+def _lut_ok(E, r, b):
+    """include/ktanh.h's validation rule, restated from the header: r in
+    0..7, E in 1..127; for every mantissa the table path can reach in entry t
+    (16v..16v+15, v = t & 7; only m = 112 when E & 3 == 0 i.e. E = 128),
+    0 <= (m >> r) + b <= 127 (BF16) and the F32 M_o stays in [0, 2^23);
+    E = 127 only if every reachable M_o is 0 (BF16 and F32)."""
+    for t in range(32):
+        if not (0 <= r[t] <= 7 and 1 <= E[t] <= 127):
+            return False
+        v = t & 7
+        ms = [112] if (t >> 3) == 0 and v == 7 else list(range(16 * v, 16 * v + 16))
+        for m in ms:
+            mo = (m >> r[t]) + b[t]
+            if not 0 <= mo <= 127 or (E[t] == 127 and mo != 0):
+                return False
+        lo23 = ms[0] << 16
+        hi23 = lo23 if len(ms) == 1 else (ms[-1] << 16) | 0xFFFF
+        if (lo23 >> r[t]) + b[t] * 65536 < 0 or (hi23 >> r[t]) + b[t] * 65536 > 0x7FFFFF:
+            return False
+        if E[t] == 127 and (hi23 >> r[t]) + b[t] * 65536 != 0:
+            return False
+    return True
+
+
+@settings(max_examples=200, deadline=None)
+@given(data=st.data())
+def test_lut_validation_matches_the_rule(kt, data):
+    """Random tables near Table 1: kt_lut_create accepts exactly those the
+    documented rule accepts (KT_ERR_LUT otherwise)."""
+    T = O.table1()
+    E, r, b = list(T.E), list(T.r), list(T.b)
+    for _ in range(data.draw(st.integers(1, 4))):
+        t = data.draw(st.integers(0, 31))
+        which = data.draw(st.sampled_from(["E", "r", "b"]))
+        if which == "E":
+            E[t] = data.draw(st.sampled_from([0, 1, 100, 125, 126, 127, 128]))
+        elif which == "r":
+            r[t] = data.draw(st.integers(-1, 8))
+        else:
+            b[t] = data.draw(st.integers(-130, 130))
+    ok = _lut_ok(E, r, b)
+    try:
+        kt.Lut.from_tables(E, r, b)
+        accepted = True
+    except kt.KTanhError as e:
+        assert e.status == kt.KT_ERR_LUT
+        accepted = False
+    assert accepted == ok, (E, r, b)
