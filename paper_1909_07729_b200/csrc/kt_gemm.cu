@@ -645,6 +645,169 @@ k_gemm2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUten
   }
 }
 
+// CTA-pair version of k_gemm_cell: a cluster computes 256 rows x 64 units;
+// CTA r loads gates 2r, 2r + 1 (its half of the 256 B rows).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmPThreads, 1)
+k_gemm2_cell(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b64,
+             const float *c_prev, float *c_next, uint16_t *h_next, uint32_t M, uint32_t H, uint32_t K,
+             const __grid_constant__ LutWords lut) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bar = base + k2Stages * k2StageBytes;
+  const uint32_t full_bar = bar, empty_bar = bar + 8 * k2Stages;
+  const uint32_t tfull_bar = bar + 16 * k2Stages, tempty_bar = tfull_bar + 16;
+  const uint32_t tmem_slot = tempty_bar + 16;
+  uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem_raw + (tmem_slot - raw));
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t mt = M / 256, ntn = H / 64, ntiles = mt * ntn;
+  const uint32_t nk = K / kBK;
+
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < k2Stages; ++s) {
+      mbar_init(full_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar + 8 * a, 1);
+      mbar_init(tempty_bar + 8 * a, 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "n"(2 * kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();   // barriers of both CTAs initialised before any remote use
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    uint32_t it = 0;
+    for (uint32_t t = cid; t < ntiles; t += ncl) {
+      uint32_t mb, nb;
+      tile_coords(t, mt, ntn, mb, nb);
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % k2Stages;
+        if (it >= (uint32_t)k2Stages) mbar_wait(empty_bar + 8 * s, ((it / k2Stages) + 1) & 1);
+        const uint32_t sa = base + s * k2StageBytes, sb = sa + k2HalfBytes;
+        const uint32_t fb = map_to_rank0(full_bar + 8 * s);
+        if (leader) mbar_expect_tx(full_bar + 8 * s, 2 * k2StageBytes);
+        tma_load_2d_pair(sa, &map_a, (int)(kb * kBK), (int)(mb * 256 + rank * 128), fb);
+        // this CTA's half of N = gates 2r, 2r + 1 (64 rows each) of units [64 nb, +64)
+        tma_load_2d_pair(sb, &map_b64, (int)(kb * kBK), (int)((2 * rank) * H + nb * 64), fb);
+        tma_load_2d_pair(sb + 64 * kBK * 2, &map_b64, (int)(kb * kBK), (int)((2 * rank + 1) * H + nb * 64),
+                         fb);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (leader only) ----------------
+    uint32_t it = 0, i = 0;
+    for (uint32_t t = cid; t < ntiles; t += ncl, ++i) {
+      const uint32_t a = i & 1;
+      if (i >= 2) mbar_wait(tempty_bar + 8 * a, ((i / 2) + 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t d = tmem + a * kTmemCols;
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % k2Stages;
+        mbar_wait(full_bar + 8 * s, (it / k2Stages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = umma_sdesc(base + s * k2StageBytes);
+        const uint64_t db = umma_sdesc(base + s * k2StageBytes + k2HalfBytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          const uint32_t acc = (kb | k) != 0;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+              "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc2), "r"(acc));
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+            " [%0], %1;" ::"r"(empty_bar + 8 * s), "h"((uint16_t)3)
+            : "memory");
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+          " [%0], %1;" ::"r"(tfull_bar + 8 * a), "h"((uint16_t)3)
+          : "memory");
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue: LSTM cell, both CTAs (as k_gemm_cell) ----------------
+    const LaneLut L{lut.bf16[lane], lut.f32K[lane], lut.f32C[lane]};
+    const uint32_t q = warp & 3, half = (warp - 2) >> 2;
+    const uint32_t tempty_leader = map_to_rank0(tempty_bar);
+    uint32_t i = 0;
+    for (uint32_t t = cid; t < ntiles; t += ncl, ++i) {
+      uint32_t mb, nb;
+      tile_coords(t, mt, ntn, mb, nb);
+      const uint32_t a = i & 1;
+      const uint32_t row = mb * 256 + rank * 128 + 32 * q + lane;
+      const size_t cbase = (size_t)row * H + nb * 64 + half * 32;
+      uint32_t cp[4][8];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) ld256<true>(c_prev + cbase + 8 * v, cp[v], true);
+      mbar_wait(tfull_bar + 8 * a, (i / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t r[128];
+      const uint32_t tbase = tmem + ((32 * q) << 16) + a * kTmemCols + half * 32;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) tmem_ld32(tbase + 64 * g, r + 32 * g);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar + 8 * a) : "memory");
+        else
+          asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           tempty_leader + 8 * a)
+                       : "memory");
+      }
+      uint32_t cn[4][8], h[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t gi = pack_bf16x2(__uint_as_float(r[2 * k + 1]), __uint_as_float(r[2 * k]));
+        const uint32_t gf = pack_bf16x2(__uint_as_float(r[32 + 2 * k + 1]), __uint_as_float(r[32 + 2 * k]));
+        const uint32_t gg = pack_bf16x2(__uint_as_float(r[64 + 2 * k + 1]), __uint_as_float(r[64 + 2 * k]));
+        const uint32_t go = pack_bf16x2(__uint_as_float(r[96 + 2 * k + 1]), __uint_as_float(r[96 + 2 * k]));
+        float2 cnv;
+        h[k] = lstm_cell2(gi, gf, gg, go,
+                          make_float2(__uint_as_float(cp[k >> 2][(2 * k) & 7]),
+                                      __uint_as_float(cp[k >> 2][(2 * k + 1) & 7])),
+                          cnv, L);
+        cn[k >> 2][(2 * k) & 7] = __float_as_uint(cnv.x);
+        cn[k >> 2][(2 * k + 1) & 7] = __float_as_uint(cnv.y);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) st256(c_next + cbase + 8 * v, cn[v], true);
+      uint32_t h0[8], h1[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        h0[j] = h[j];
+        h1[j] = h[8 + j];
+      }
+      st256(h_next + cbase, h0, true);
+      st256(h_next + cbase + 16, h1, true);
+    }
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();   // both CTAs done with TMEM and with each other's barriers
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(2 * kTmemCols));
+  }
+}
+
 // ---------------------------------------------------------------- host ----
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -763,6 +926,22 @@ cudaError_t launch_gemm_cell(const uint16_t *A, const uint16_t *B, const float *
                              uint16_t *h_next, size_t M, size_t H, size_t K, const LutWords &lut,
                              cudaStream_t s, int sms) {
   CUtensorMap ma, mb;
+  if (use_pair(M, 4 * H, K, OP_TANH) && sms >= 2) {
+    if (!make_map(&ma, A, M, K, 128) || !make_map(&mb, B, 4 * H, K, 64)) return cudaErrorInvalidValue;
+    static std::once_flag once2;
+    static cudaError_t attr_err2 = cudaSuccess;
+    std::call_once(once2, [] {
+      attr_err2 = cudaFuncSetAttribute(k_gemm2_cell, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)k2Smem);
+    });
+    if (attr_err2 != cudaSuccess) return attr_err2;
+    const size_t tiles = (M / 256) * (H / 64), pairs = (size_t)(sms / 2);
+    const unsigned grid = (unsigned)(2 * (tiles < pairs ? tiles : pairs));
+    k_gemm2_cell<<<grid, kGemmPThreads, k2Smem, s>>>(ma, mb, c_prev, c_next, h_next, (uint32_t)M,
+                                                     (uint32_t)H, (uint32_t)K, lut);
+    count_launch();
+    return cudaGetLastError();
+  }
   if (!make_map(&ma, A, M, K, kBM) || !make_map(&mb, B, 4 * H, K, 64)) return cudaErrorInvalidValue;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
