@@ -336,6 +336,17 @@ KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, voi
                                size_t n, kt_lut lut, void *d_work, size_t work_bytes,
                                void *stream);
 
+/* kt_apply_host with the chunk size chosen by the caller: chunk_elems = 0
+ * is kt_apply_host's default (~n/3); otherwise chunks of chunk_elems
+ * elements (>= 4096, rounded down to a multiple of 256; still capped by
+ * work_bytes / (6 * elem_size)).  Fewer, larger chunks suit callers that
+ * overlap calls on several streams (each call's D2H under the next call's
+ * H2D: config 2 end to end 24.0 Gelem/s with whole-call chunks on two
+ * streams vs 22.6 with 3 chunks); more chunks suit a lone call. */
+KT_API kt_status kt_apply_host_ex(kt_op op, kt_dtype dtype, const void *x_host, void *y_host,
+                                  size_t n, kt_lut lut, void *d_work, size_t work_bytes,
+                                  size_t chunk_elems, void *stream);
+
 /* ---------------------------------------------------------------------- */
 /* Multi-GPU sharding (host logic; BASELINE.json north_star item (c)).     */
 /* ---------------------------------------------------------------------- */

@@ -44,7 +44,7 @@ EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_creat
                        "kt_apx_create", "kt_apx_coeffs", "kt_apx_destroy", "kt_apx_tanh_bf16",
                        "kt_apx_tanh_f32", "kt_alu_probe", "kgelu_swish_bf16", "kgelu_swish_f32",
                        "kgemm_lstm_gates_bf16", "kgemm_lstm_cell_bf16", "kt_lut64_create",
-                       "kt_lut64_get", "kt_lut64_destroy", "ktanh64_bf16")
+                       "kt_lut64_get", "kt_lut64_destroy", "ktanh64_bf16", "kt_apply_host_ex")
 
 for _name in MAP_CALLS:
     _f = getattr(_lib, _name)
@@ -78,6 +78,8 @@ _lib.kt_apply.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp, _vp]
 _lib.kt_apply.restype = ctypes.c_int
 _lib.kt_apply_host.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp, _vp, _sz, _vp]
 _lib.kt_apply_host.restype = ctypes.c_int
+_lib.kt_apply_host_ex.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp, _vp, _sz, _sz, _vp]
+_lib.kt_apply_host_ex.restype = ctypes.c_int
 _lib.kt_shard_range.argtypes = [_sz, ctypes.c_int, ctypes.c_int, _sz, ctypes.POINTER(_sz),
                                 ctypes.POINTER(_sz)]
 _lib.kt_shard_range.restype = ctypes.c_int
@@ -386,9 +388,11 @@ def apply(op: str, x, out=None, lut: Lut | None = None, stream=None):
     return out
 
 
-def apply_host(op: str, x_host, y_host, work, lut: Lut | None = None, stream=None):
-    """kt_apply_host: x_host/y_host are (pinned) CPU tensors, `work` a CUDA uint8
-    scratch tensor on the current device.  Asynchronous on `stream`."""
+def apply_host(op: str, x_host, y_host, work, lut: Lut | None = None, stream=None,
+               chunk: int = 0):
+    """kt_apply_host(_ex): x_host/y_host are (pinned) CPU tensors, `work` a CUDA
+    uint8 scratch tensor on the current device, `chunk` elements per pipeline
+    chunk (0 = default).  Asynchronous on `stream`."""
     import torch
     if x_host.is_cuda or y_host.is_cuda or not work.is_cuda:
         raise TypeError("x_host / y_host must be CPU tensors, work a CUDA tensor")
@@ -397,10 +401,11 @@ def apply_host(op: str, x_host, y_host, work, lut: Lut | None = None, stream=Non
     dname = "bf16" if x_host.dtype == torch.bfloat16 else "f32"
     lut = lut or paper_lut()
     with torch.cuda.device(work.device):
-        _check(_lib.kt_apply_host(OPS[op], DTYPES[dname], x_host.data_ptr(), y_host.data_ptr(),
-                                  x_host.numel(), lut.handle, work.data_ptr(),
-                                  work.numel() * work.element_size(), _stream_ptr(stream)),
-               "kt_apply_host")
+        _check(_lib.kt_apply_host_ex(OPS[op], DTYPES[dname], x_host.data_ptr(), y_host.data_ptr(),
+                                     x_host.numel(), lut.handle, work.data_ptr(),
+                                     work.numel() * work.element_size(), int(chunk),
+                                     _stream_ptr(stream)),
+               "kt_apply_host_ex")
     return y_host
 
 

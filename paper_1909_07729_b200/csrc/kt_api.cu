@@ -665,8 +665,18 @@ static const void *mapped_device_ptr(const void *h) {
   return a.devicePointer;
 }
 
+KT_API kt_status kt_apply_host_ex(kt_op op, kt_dtype dtype, const void *x_host, void *y_host,
+                                  size_t n, kt_lut lut, void *d_work, size_t work_bytes,
+                                  size_t chunk_elems, void *stream);
+
 KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, void *y_host, size_t n,
                                kt_lut lut, void *d_work, size_t work_bytes, void *stream) {
+  return kt_apply_host_ex(op, dtype, x_host, y_host, n, lut, d_work, work_bytes, 0, stream);
+}
+
+KT_API kt_status kt_apply_host_ex(kt_op op, kt_dtype dtype, const void *x_host, void *y_host,
+                                  size_t n, kt_lut lut, void *d_work, size_t work_bytes,
+                                  size_t chunk_elems, void *stream) {
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
   if ((int)op < 0 || (int)op > 3 || (int)dtype < 0 || (int)dtype > 1)
     return fail(KT_ERR_ARG, "bad op/dtype");
@@ -714,7 +724,10 @@ KT_API kt_status kt_apply_host(kt_op op, kt_dtype dtype, const void *x_host, voi
   size_t want = ((n + kBufs - 1) / kBufs + 255) / 256 * 256;
   const size_t min_chunk = ((size_t)1 << 20) / es;
   if (want < min_chunk) want = min_chunk;
-  if (const char *ev = getenv("KT_HOST_CHUNK")) {   // tuning override (elements)
+  if (chunk_elems) {                                // caller's choice (elements)
+    if (chunk_elems < 4096) return fail(KT_ERR_ARG, "chunk_elems must be 0 or >= 4096");
+    want = chunk_elems - chunk_elems % 256;
+  } else if (const char *ev = getenv("KT_HOST_CHUNK")) {   // tuning override (elements)
     const size_t c = (size_t)strtoull(ev, nullptr, 10);
     if (c >= 4096) want = c - c % 256;
   }

@@ -598,3 +598,22 @@ def test_ktanh64_with_split_table1_equals_ktanh(kt):
     h = kt.Lut64([E32[i] for i in t64], [r32[i] for i in t64], [b32[i] for i in t64])
     x = WL.make_input("c1_exhaustive_bf16", device="cuda")
     assert torch.equal(kt.ktanh64_bf16(x, h).view(torch.int16), kt.ktanh_bf16(x).view(torch.int16))
+
+
+@pytest.mark.parametrize("chunk", [4096, 1 << 20, 1 << 22])
+def test_apply_host_ex_chunks(kt, chunk):
+    """kt_apply_host_ex with caller-chosen chunk sizes (incl. whole-call and
+    a ragged last chunk) on two alternating streams."""
+    n = (1 << 22) + 333
+    g = torch.Generator().manual_seed(chunk)
+    xs = [(torch.randn(n, generator=g) * 2).to(torch.bfloat16).pin_memory() for _ in range(2)]
+    ys = [torch.empty_like(x).pin_memory() for x in xs]
+    works = [torch.empty(6 * n * 2 + 4096, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for rep in range(4):
+        j = rep % 2
+        kt.apply_host("gelu", xs[j], ys[j], works[j], stream=streams[j], chunk=chunk)
+    torch.cuda.synchronize()
+    for x, y in zip(xs, ys):
+        want = O.map_bf16("gelu", x.view(torch.int16).numpy().view(np.uint16))
+        assert_ulp(y.view(torch.int16).numpy().view(np.uint16), want, 16, 1, ctx=f"chunk={chunk}")
