@@ -93,6 +93,19 @@ def lib():
             L.kto_map_bf16_s.restype = None
             L.kto_bounds_s.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ip, ip]
             L.kto_bounds_s.restype = None
+            L.kto_bounds_sp.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ip, ip]
+            L.kto_bounds_sp.restype = None
+            L.kto_build_lut_sp.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ip, ip, ip,
+                                           ctypes.POINTER(ctypes.c_double)]
+            L.kto_build_lut_sp.restype = ctypes.c_int
+            L.kto_map_f32_p.argtypes = [ctypes.c_int, u32p, u32p, ctypes.c_size_t, ip, ip, ip,
+                                        ctypes.c_int]
+            L.kto_map_f32_p.restype = None
+            L.kto_bwd_map_f32_p.argtypes = [ctypes.c_int, u32p, u32p, u32p, ctypes.c_size_t, ip, ip,
+                                            ip, ctypes.c_int]
+            L.kto_bwd_map_f32_p.restype = None
+            L.kto_ktanh_f32_p23.argtypes = [ctypes.c_uint32, ip, ip, ip]
+            L.kto_ktanh_f32_p23.restype = ctypes.c_uint32
             L.kto_gelu_consts.argtypes = [ctypes.c_int]
             L.kto_gelu_consts.restype = ctypes.c_uint32
             dp = ctypes.POINTER(ctypes.c_double)
@@ -122,13 +135,18 @@ def lib():
 
 class Lut:
     """Three integer tables (T_E, T_r, T_b), Alg. 1 line 1: 32 entries (3 mantissa
-    index bits, Table 1 layout) or 64 entries (4 bits)."""
+    index bits, Table 1 layout) or 64 entries (4 bits).  p = the
+    mantissa width b is expressed in: 7 (BF16 tables such as Table 1; on F32
+    data b is scaled by 2^16, reading A8) or 23 (F32-only tables re-optimised
+    at p = 23)."""
 
-    def __init__(self, E, r, b):
+    def __init__(self, E, r, b, p: int = 7):
         self.E = np.ascontiguousarray(E, dtype=np.int32)
         self.r = np.ascontiguousarray(r, dtype=np.int32)
         self.b = np.ascontiguousarray(b, dtype=np.int32)
+        self.p = int(p)
         assert self.E.shape == self.r.shape == self.b.shape and self.E.shape[0] in (32, 64)
+        assert self.p in (7, 23)
 
     @property
     def s_bits(self):
@@ -171,6 +189,34 @@ def build_lut_s(s_bits: int, bmin_zero: bool = False):
     return Lut(E, r, b), sse
 
 
+def build_lut_sp(s_bits: int, p: int, bmin_zero: bool = False):
+    """Sec. 2.4 optimizer with s index bits and p mantissa bits (p = 23: the
+    F32-native table); returns (Lut(p=p), per-interval score)."""
+    key = (s_bits, p, bool(bmin_zero))
+    if key not in _SP_CACHE:
+        n = 4 << s_bits
+        E = np.zeros(n, np.int32); r = np.zeros(n, np.int32); b = np.zeros(n, np.int32)
+        sse = np.zeros(n, np.float64)
+        ip = ctypes.POINTER(ctypes.c_int)
+        rc = lib().kto_build_lut_sp(s_bits, p, int(bmin_zero), E.ctypes.data_as(ip),
+                                    r.ctypes.data_as(ip), b.ctypes.data_as(ip),
+                                    sse.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        if rc != 0:
+            raise ValueError(f"unsupported (s, p) = ({s_bits}, {p})")
+        _SP_CACHE[key] = (E, r, b, sse)
+    E, r, b, sse = _SP_CACHE[key]
+    return Lut(E.copy(), r.copy(), b.copy(), p=p), sse.copy()
+
+
+_SP_CACHE: dict = {}
+
+
+def bounds_sp(r: int, v: int, s_bits: int, p: int):
+    lo = ctypes.c_int(); hi = ctypes.c_int()
+    lib().kto_bounds_sp(r, v, s_bits, p, ctypes.byref(lo), ctypes.byref(hi))
+    return lo.value, hi.value
+
+
 def bounds_s(r: int, v: int, s_bits: int):
     lo = ctypes.c_int(); hi = ctypes.c_int()
     lib().kto_bounds_s(r, v, s_bits, ctypes.byref(lo), ctypes.byref(hi))
@@ -210,6 +256,7 @@ def _lut(lut):
 def map_bf16(op: str, x_u16: np.ndarray, lut: Lut | None = None) -> np.ndarray:
     """y = op(x) for a uint16 array of BF16 bit patterns (any shape)."""
     lut = _lut(lut)
+    assert lut.p == 7, "p = 23 tables are F32-only"
     x = np.ascontiguousarray(x_u16, dtype=np.uint16)
     y = np.empty_like(x)
     u16p = ctypes.POINTER(ctypes.c_uint16)
@@ -228,7 +275,10 @@ def map_f32(op: str, x_u32: np.ndarray, lut: Lut | None = None) -> np.ndarray:
     x = np.ascontiguousarray(x_u32, dtype=np.uint32)
     y = np.empty_like(x)
     u32p = ctypes.POINTER(ctypes.c_uint32)
-    lib().kto_map_f32(OPS[op], x.ctypes.data_as(u32p), y.ctypes.data_as(u32p), x.size, *lut.ptrs())
+    assert lut.s_bits == 3
+    assert not (op == "tanh_via_bf16" and lut.p != 7), "via-BF16 needs a BF16 table"
+    lib().kto_map_f32_p(OPS[op], x.ctypes.data_as(u32p), y.ctypes.data_as(u32p), x.size,
+                        *lut.ptrs(), lut.p)
     return y
 
 
@@ -252,8 +302,8 @@ def bwd_f32(op: str, a_u32: np.ndarray, dy_u32: np.ndarray, lut: Lut | None = No
     assert a.shape == d.shape
     y = np.empty_like(a)
     u32p = ctypes.POINTER(ctypes.c_uint32)
-    lib().kto_bwd_map_f32(OPS[op], a.ctypes.data_as(u32p), d.ctypes.data_as(u32p),
-                          y.ctypes.data_as(u32p), a.size, *lut.ptrs())
+    lib().kto_bwd_map_f32_p(OPS[op], a.ctypes.data_as(u32p), d.ctypes.data_as(u32p),
+                            y.ctypes.data_as(u32p), a.size, *lut.ptrs(), lut.p)
     return y
 
 

@@ -35,11 +35,16 @@
  *                                               error bounds vs the true derivative)
  *   kto_build_lut (Sec. 2.4 optimizer) ........ pinned (Table 1 match counts,
  *                                               SSE dominance, Table 2 ablation)
+ *   kto_build_lut_sp at p = 23 (NEXT-3) ....... pinned (tests/test_oracle_f32_tables.py:
+ *                                               brute-force Step 3 optimality with
+ *                                               numpy's RNE, validity, dominance)
+ *   kto_map_f32_p / kto_bwd_map_f32_p (pb=23) . pinned (lifted Table 1 == A8)
  *   kto_bounds ................................ pinned (exhaustive no-overflow)
  */
 #include <math.h>
 #include <stddef.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #ifndef M_PI
@@ -204,7 +209,10 @@ void kto_map_bf16_s(const uint16_t *x, uint16_t *y, size_t n, int s_bits,
 /* (E & 3, top 3 of the 23-bit mantissa); line 8 with p = 23:            */
 /* M_o = (M_i >> r_t) + b_t * 2^(23-7)  (b_t is in units of 2^-7).        */
 /* ------------------------------------------------------------------ */
-uint32_t kto_ktanh_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+/* pb = the mantissa width b_t is expressed in: 7 (reading A8, Table 1's    */
+/* BF16-unit b, scaled by 2^16) or 23 (an F32 table re-optimised at p = 23, */
+/* M_o = (M_i >> r_t) + b_t).                             */
+static uint32_t ktanh_f32_pb(uint32_t x, const int *TE, const int *Tr, const int *Tb, int pb)
 {
     uint32_t s = x >> 31;
     int E = (int)((x >> 23) & 0xFF);
@@ -215,9 +223,19 @@ uint32_t kto_ktanh_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
     if (ax > T2) return (s << 31) | (127u << 23);         /* line 4 */
     int t = index_t(E, (int)(M >> 20));                   /* line 6 */
     int Et = TE[t], rt = Tr[t], bt = Tb[t];               /* line 7 */
-    int32_t Mo = (M >> rt) + bt * 65536;                  /* line 8, p = 23 */
+    int32_t Mo = (M >> rt) + bt * (1 << (23 - pb));       /* line 8, p = 23 */
     if (Mo < 0 || Mo > 0x7FFFFF) g_overflow = 1;
     return (s << 31) | ((uint32_t)(Et & 0xFF) << 23) | ((uint32_t)Mo & 0x7FFFFF);
+}
+
+uint32_t kto_ktanh_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    return ktanh_f32_pb(x, TE, Tr, Tb, 7);
+}
+
+uint32_t kto_ktanh_f32_p23(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    return ktanh_f32_pb(x, TE, Tr, Tb, 23);
 }
 
 /* ------------------------------------------------------------------ */
@@ -276,13 +294,18 @@ uint16_t kto_ksigmoid_bf16(uint16_t x, const int *TE, const int *Tr, const int *
     return kto_bf16_encode_rne((1.0 + tv) / 2.0);
 }
 
-uint32_t kto_ksigmoid_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+static uint32_t ksigmoid_f32_pb(uint32_t x, const int *TE, const int *Tr, const int *Tb, int pb)
 {
     double xv = (double)f32_from_bits(x);
     float h = (float)(xv / 2.0);                          /* x/2 in F32 (RNE) */
-    uint32_t t = kto_ktanh_f32(bits_from_f32(h), TE, Tr, Tb);
+    uint32_t t = ktanh_f32_pb(bits_from_f32(h), TE, Tr, Tb, pb);
     double tv = (double)f32_from_bits(t);
     return bits_from_f32((float)((1.0 + tv) / 2.0));
+}
+
+uint32_t kto_ksigmoid_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    return ksigmoid_f32_pb(x, TE, Tr, Tb, 7);
 }
 
 uint16_t kto_kswish_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb)
@@ -294,13 +317,18 @@ uint16_t kto_kswish_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb
     return kto_bf16_encode_rne(xv * (1.0 + tv) / 2.0);   /* x * Sigmoid(x) */
 }
 
-uint32_t kto_kswish_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+static uint32_t kswish_f32_pb(uint32_t x, const int *TE, const int *Tr, const int *Tb, int pb)
 {
     double xv = (double)f32_from_bits(x);
     float h = (float)(xv / 2.0);
-    uint32_t t = kto_ktanh_f32(bits_from_f32(h), TE, Tr, Tb);
+    uint32_t t = ktanh_f32_pb(bits_from_f32(h), TE, Tr, Tb, pb);
     double tv = (double)f32_from_bits(t);
     return bits_from_f32((float)(xv * (1.0 + tv) / 2.0));
+}
+
+uint32_t kto_kswish_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    return kswish_f32_pb(x, TE, Tr, Tb, 7);
 }
 
 uint16_t kto_kgelu_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb)
@@ -313,13 +341,18 @@ uint16_t kto_kgelu_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb)
     return kto_bf16_encode_rne(xv / 2.0 * (1.0 + tv));
 }
 
-uint32_t kto_kgelu_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+static uint32_t kgelu_f32_pb(uint32_t x, const int *TE, const int *Tr, const int *Tb, int pb)
 {
     float xf = f32_from_bits(x);
     float u = gelu_arg_f32(xf);
-    uint32_t t = kto_ktanh_f32(bits_from_f32(u), TE, Tr, Tb);
+    uint32_t t = ktanh_f32_pb(bits_from_f32(u), TE, Tr, Tb, pb);
     double tv = (double)f32_from_bits(t);
     return bits_from_f32((float)((double)xf / 2.0 * (1.0 + tv)));
+}
+
+uint32_t kto_kgelu_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
+{
+    return kgelu_f32_pb(x, TE, Tr, Tb, 7);
 }
 
 /* ------------------------------------------------------------------ */
@@ -358,17 +391,23 @@ uint16_t kto_bwd_bf16(int op, uint16_t a, uint16_t dy, const int *TE, const int 
     return kto_bf16_encode_rne(dv * bwd_factor(op, av, tv));
 }
 
-uint32_t kto_bwd_f32(int op, uint32_t a, uint32_t dy, const int *TE, const int *Tr, const int *Tb)
+static uint32_t bwd_f32_pb(int op, uint32_t a, uint32_t dy, const int *TE, const int *Tr,
+                           const int *Tb, int pb)
 {
     double av = (double)f32_from_bits(a), dv = (double)f32_from_bits(dy), tv = 0.0;
     if (op == 2) {
         float h = (float)(av / 2.0);
-        tv = (double)f32_from_bits(kto_ktanh_f32(bits_from_f32(h), TE, Tr, Tb));
+        tv = (double)f32_from_bits(ktanh_f32_pb(bits_from_f32(h), TE, Tr, Tb, pb));
     } else if (op == 3) {
         float u = gelu_arg_f32((float)av);
-        tv = (double)f32_from_bits(kto_ktanh_f32(bits_from_f32(u), TE, Tr, Tb));
+        tv = (double)f32_from_bits(ktanh_f32_pb(bits_from_f32(u), TE, Tr, Tb, pb));
     }
     return bits_from_f32((float)(dv * bwd_factor(op, av, tv)));
+}
+
+uint32_t kto_bwd_f32(int op, uint32_t a, uint32_t dy, const int *TE, const int *Tr, const int *Tb)
+{
+    return bwd_f32_pb(op, a, dy, TE, Tr, Tb, 7);
 }
 
 void kto_bwd_map_bf16(int op, const uint16_t *a, const uint16_t *dy, uint16_t *dx, size_t n,
@@ -377,10 +416,16 @@ void kto_bwd_map_bf16(int op, const uint16_t *a, const uint16_t *dy, uint16_t *d
     for (size_t i = 0; i < n; ++i) dx[i] = kto_bwd_bf16(op, a[i], dy[i], TE, Tr, Tb);
 }
 
+void kto_bwd_map_f32_p(int op, const uint32_t *a, const uint32_t *dy, uint32_t *dx, size_t n,
+                       const int *TE, const int *Tr, const int *Tb, int pb)
+{
+    for (size_t i = 0; i < n; ++i) dx[i] = bwd_f32_pb(op, a[i], dy[i], TE, Tr, Tb, pb);
+}
+
 void kto_bwd_map_f32(int op, const uint32_t *a, const uint32_t *dy, uint32_t *dx, size_t n,
                      const int *TE, const int *Tr, const int *Tb)
 {
-    for (size_t i = 0; i < n; ++i) dx[i] = kto_bwd_f32(op, a[i], dy[i], TE, Tr, Tb);
+    kto_bwd_map_f32_p(op, a, dy, dx, n, TE, Tr, Tb, 7);
 }
 
 /* ------------------------------------------------------------------ */
@@ -400,18 +445,26 @@ void kto_map_bf16(int op, const uint16_t *x, uint16_t *y, size_t n,
     }
 }
 
-void kto_map_f32(int op, const uint32_t *x, uint32_t *y, size_t n,
-                 const int *TE, const int *Tr, const int *Tb)
+/* pb: unit of b_t, 7 (Table 1's tables, reading A8) or 23 (re-optimised   */
+/* F32 tables); op 4 (via BF16) needs a BF16 table (pb = 7).               */
+void kto_map_f32_p(int op, const uint32_t *x, uint32_t *y, size_t n,
+                   const int *TE, const int *Tr, const int *Tb, int pb)
 {
     for (size_t i = 0; i < n; ++i) {
         switch (op) {
-        case 0: y[i] = kto_ktanh_f32(x[i], TE, Tr, Tb); break;
-        case 1: y[i] = kto_ksigmoid_f32(x[i], TE, Tr, Tb); break;
-        case 2: y[i] = kto_kswish_f32(x[i], TE, Tr, Tb); break;
+        case 0: y[i] = ktanh_f32_pb(x[i], TE, Tr, Tb, pb); break;
+        case 1: y[i] = ksigmoid_f32_pb(x[i], TE, Tr, Tb, pb); break;
+        case 2: y[i] = kswish_f32_pb(x[i], TE, Tr, Tb, pb); break;
         case 4: y[i] = kto_ktanh_f32_via_bf16(x[i], TE, Tr, Tb); break;
-        default: y[i] = kto_kgelu_f32(x[i], TE, Tr, Tb); break;
+        default: y[i] = kgelu_f32_pb(x[i], TE, Tr, Tb, pb); break;
         }
     }
+}
+
+void kto_map_f32(int op, const uint32_t *x, uint32_t *y, size_t n,
+                 const int *TE, const int *Tr, const int *Tb)
+{
+    kto_map_f32_p(op, x, y, n, TE, Tr, Tb, 7);
 }
 
 /* Strided gather variant for sampled full-size checks: y[j] = f(x[idx[j]]). */
@@ -477,94 +530,130 @@ void kto_bounds(int r, int v, int *bmin, int *bmax)
     *bmin = -v * (int)floor(ldexp(1.0, p - s - r));
 }
 
-/* Eq. 3 / b_max with s index bits. */
+/* Eq. 3 / b_max with s index bits and p mantissa bits: */
+/*   b_max = 2^p - 1 - floor(((v+1) 2^(p-s) - 1) / 2^r)                     */
+/*   b_min = -v floor(2^(p-s-r))            (0 when r > p - s)              */
+void kto_bounds_sp(int r, int v, int s_bits, int p, int *bmin, int *bmax)
+{
+    *bmax = (1 << p) - 1 - (int)((((int64_t)(v + 1) << (p - s_bits)) - 1) >> r);
+    *bmin = r <= p - s_bits ? -v * (1 << (p - s_bits - r)) : 0;
+}
+
 void kto_bounds_s(int r, int v, int s_bits, int *bmin, int *bmax)
 {
-    const int p = 7;
-    *bmax = (1 << p) - 1 - (int)floor((double)((v + 1) * (1 << (p - s_bits)) - 1) / ldexp(1.0, r));
-    *bmin = -v * (int)floor(ldexp(1.0, p - s_bits - r));
+    kto_bounds_sp(r, v, s_bits, 7, bmin, bmax);
+}
+
+/* RNE of y > 0 to the p-bit format (p = 7: BFloat16, p = 23: Float32),    */
+/* returned as biased exponent and mantissa fields.                        */
+static void rne_fields(double y, int p, int *E, int *M)
+{
+    uint32_t u;
+    if (p == 7) u = (uint32_t)kto_bf16_encode_rne(y) << 16;
+    else u = bits_from_f32((float)y);                       /* C cast: RNE */
+    *E = (int)((u >> 23) & 0xFF);
+    *M = (int)((u & 0x7FFFFF) >> (23 - p));
+}
+
+/* floor(a / b) for b > 0 */
+static __int128 floor_div(__int128 a, __int128 b)
+{
+    __int128 q = a / b;
+    if ((a % b != 0) && (a < 0)) q -= 1;
+    return q;
 }
 
 /* ------------------------------------------------------------------ */
-/* Sec. 2.4 optimizer, Steps 1-3, reading R*:           */
+/* Sec. 2.4 optimizer, Steps 1-3, reading R*, for s     */
+/* mantissa index bits and inputs / outputs with p mantissa bits (p = 7:   */
+/* BFloat16, the paper's case; p = 23: Float32 tables re-optimised for the */
+/* native F32 path, SURVEY.md NEXT-3 -- the paper's text is written for a  */
+/* general p: "p = 7 in case of BFloat16"):              */
+/*  inputs: every positive x = 2^(E-127)(1 + M/2^p), T1 <= x <= T2, whose  */
+/*     index ((E & 3) << s) | (M >> (p - s)) is t.                          */
 /*  Step 1: y_i = tanh(x_i) in binary64, (E_i, M_i) =   */
-/*     fields of RNE_bf16(y_i) (reading A12).                              */
+/*     fields of RNE_p(y_i) (reading A12).                                 */
 /*  Step 2: for each candidate E in {min(E_i, 126)}     */
 /*     (reading A15), M^_j = M_j if E = E_j, 0 if E > E_j, 2^q - 1 if      */
-/*     E < E_j; pick the E minimising sum (y_i - y^_i)^2 against the       */
-/*     unrounded y_i; ties -> smaller E.                                   */
-/*  Step 3 (Eq. 2): for r = 0..r_max (= p = 7):          */
+/*     E < E_j (q = p); pick the E minimising sum (y_i - y^_i)^2 against   */
+/*     the unrounded y_i; ties -> smaller E.                               */
+/*  Step 3 (Eq. 2): for r = 0..r_max (= p):               */
 /*     b* = mean(M^_i - m_i / 2^r) (real division as printed, A13),        */
 /*     b = floor(b* + 1/2) (A14), clamped to [b_min, b_max]; score         */
 /*     sum (M^_i - ((m_i >> r) + b))^2; keep the minimum, ties -> smaller r */
 /*     (A17).  bmin_zero != 0 is the Sec. 3.1 ablation.      */
-/* Returns the per-interval minimum score in sse_out (may be NULL).         */
+/* b* and the scores are computed exactly in 128-bit integers.  Returns    */
+/* the per-interval minimum score in sse_out (may be NULL); returns 0, or  */
+/* -1 for an unsupported (s, p).                                           */
 /* ------------------------------------------------------------------ */
-void kto_build_lut_s(int s_bits, int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
+int kto_build_lut_sp(int s_bits, int p, int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
 {
-    const int q = 7;
-    const int nent = 4 << s_bits, per = 1 << (7 - s_bits);
+    if ((p != 7 && p != 23) || s_bits < 1 || s_bits > 5) return -1;
+    const int q = p;
+    const int nent = 4 << s_bits, per = 1 << (p - s_bits);
+    double *xs = malloc(sizeof(double) * per), *ys = malloc(sizeof(double) * per);
+    int *ms = malloc(sizeof(int) * per), *Ei = malloc(sizeof(int) * per);
+    int *Mi = malloc(sizeof(int) * per), *Mhat = malloc(sizeof(int) * per);
+    int *Mhat_best = malloc(sizeof(int) * per);
     for (int t = 0; t < nent; ++t) {
-        /* the positive BF16 inputs of interval t with T1 <= x <= T2 */
-        double xs[16], ys[16];
-        int ms[16], Ei[16], Mi[16], cnt = 0;
-        (void)per;
-        for (int w = 0; w < 0x7F80; ++w) {
-            double xv = kto_bf16_decode((uint16_t)w);
-            if (xv < T1 || xv > T2) continue;
-            int E = (w >> 7) & 0xFF, M = w & 0x7F;
-            if ((((E & 3) << s_bits) | (M >> (7 - s_bits))) != t) continue;
-            xs[cnt] = xv;
-            ms[cnt] = M;
-            cnt++;
+        int cnt = 0;
+        for (int E = 125; E <= 128; ++E) {          /* T1 = 2^-2 <= x <= T2 < 2^2 */
+            if ((E & 3) != (t >> s_bits)) continue;
+            for (int j = 0; j < per; ++j) {
+                int M = ((t & ((1 << s_bits) - 1)) << (p - s_bits)) | j;
+                double xv = ldexp(1.0 + ldexp((double)M, -p), E - 127);
+                if (xv < T1 || xv > T2) continue;
+                xs[cnt] = xv;
+                ms[cnt] = M;
+                cnt++;
+            }
         }
+        if (cnt == 0) { TE[t] = 126; Tr[t] = 0; Tb[t] = 0; if (sse_out) sse_out[t] = 0; continue; }
         /* Step 1 */
         for (int i = 0; i < cnt; ++i) {
             ys[i] = tanh(xs[i]);
-            uint16_t yb = kto_bf16_encode_rne(ys[i]);
-            Ei[i] = (yb >> 7) & 0xFF;
-            Mi[i] = yb & 0x7F;
+            rne_fields(ys[i], p, &Ei[i], &Mi[i]);
         }
-        /* Step 2 */
-        int bestE = -1;
+        /* Step 2 (each distinct candidate once; a repeat scores the same) */
+        int bestE = -1, tried[4] = {-1, -1, -1, -1}, ntried = 0;
         double bestSSE = INFINITY;
-        int Mhat_best[16];
-        if (cnt == 0) { TE[t] = 126; Tr[t] = 0; Tb[t] = 0; if (sse_out) sse_out[t] = 0; continue; }
         for (int c = 0; c < cnt; ++c) {
             int E = Ei[c] < 126 ? Ei[c] : 126;
+            int seen = 0;
+            for (int k = 0; k < ntried; ++k) seen |= tried[k] == E;
+            if (seen) continue;
+            if (ntried < 4) tried[ntried++] = E;
             double sse = 0.0;
-            int Mhat[16];
             for (int j = 0; j < cnt; ++j) {
                 if (E == Ei[j]) Mhat[j] = Mi[j];
                 else if (E > Ei[j]) Mhat[j] = 0;
                 else Mhat[j] = (1 << q) - 1;
-                double yhat = ldexp(1.0 + Mhat[j] / 128.0, E - 127);
+                double yhat = ldexp(1.0 + ldexp((double)Mhat[j], -q), E - 127);
                 sse += (ys[j] - yhat) * (ys[j] - yhat);
             }
             if (sse < bestSSE || (sse == bestSSE && E < bestE)) {
                 bestSSE = sse;
                 bestE = E;
-                memcpy(Mhat_best, Mhat, sizeof(Mhat));
+                memcpy(Mhat_best, Mhat, sizeof(int) * cnt);
             }
         }
         /* Step 3 */
         int v = t & ((1 << s_bits) - 1);
         int bestR = -1, bestB = 0;
-        long bestScore = -1;
-        for (int r = 0; r <= 7; ++r) {
-            double bstar = 0.0;
-            for (int j = 0; j < cnt; ++j) bstar += Mhat_best[j] - ms[j] / ldexp(1.0, r);
-            bstar /= cnt;
-            int b = (int)floor(bstar + 0.5);
+        __int128 bestScore = -1;
+        for (int r = 0; r <= p; ++r) {
+            __int128 S = 0;                          /* cnt 2^r b* = sum(M^ 2^r - m) */
+            for (int j = 0; j < cnt; ++j) S += ((__int128)Mhat_best[j] << r) - ms[j];
+            int b = (int)floor_div(2 * S + ((__int128)cnt << r), (__int128)cnt << (r + 1));
             int bmin, bmax;
-            kto_bounds_s(r, v, s_bits, &bmin, &bmax);
+            kto_bounds_sp(r, v, s_bits, p, &bmin, &bmax);
             if (bmin_zero) bmin = 0;
             if (b < bmin) b = bmin;
             if (b > bmax) b = bmax;
-            long score = 0;
+            __int128 score = 0;
             for (int j = 0; j < cnt; ++j) {
-                long d = Mhat_best[j] - ((ms[j] >> r) + b);
-                score += d * d;
+                int64_t d = (int64_t)Mhat_best[j] - ((ms[j] >> r) + b);
+                score += (__int128)(d * d);
             }
             if (bestScore < 0 || score < bestScore) {
                 bestScore = score;
@@ -577,6 +666,13 @@ void kto_build_lut_s(int s_bits, int bmin_zero, int *TE, int *Tr, int *Tb, doubl
         Tb[t] = bestB;
         if (sse_out) sse_out[t] = (double)bestScore;
     }
+    free(xs); free(ys); free(ms); free(Ei); free(Mi); free(Mhat); free(Mhat_best);
+    return 0;
+}
+
+void kto_build_lut_s(int s_bits, int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
+{
+    kto_build_lut_sp(s_bits, 7, bmin_zero, TE, Tr, Tb, sse_out);
 }
 
 void kto_build_lut(int bmin_zero, int *TE, int *Tr, int *Tb, double *sse_out)
