@@ -174,6 +174,9 @@ class Step:
             apx = kt.Apx(kind, int(p), int(q))
             call = kt.kt_apx_tanh_bf16 if self.cfg.elem_bytes == 2 else kt.kt_apx_tanh_f32
             return lambda x, y: call(x, apx, out=y)
+        if op == "ktanh_f32:p23":             # F32-native table re-optimised at p = 23 (NEXT-3)
+            h = kt.Lut.optimized(23)
+            return lambda x, y: kt.ktanh_f32(x, out=y, lut=h)
         if op == "lstm":
             return lambda x, y: kt.klstm_gates_bf16(x, WL.LSTM_HIDDEN, 2, out=y)
         return lambda x, y: getattr(kt, op)(x, out=y)
@@ -424,7 +427,8 @@ KERNEL_NAME = {"ktanh_bf16": "k_map<0, 0, true>", "ktanh_f32": "k_map<0, 1, true
                "kgelu_bf16": "k_map<3, 0, true>", "kswish_bf16": "k_map<2, 0, true>",
                "lstm": "k_lstm<true>"}
 
-EXTRA = [("c2_bf16_2p24", "ktanh64_bf16"), ("c3_f32_2p28", "ktanh_f32"), ("c3_f32_2p28", "ktanh_f32_via_bf16"), ("c4_lstm_gates", "lstm"),
+EXTRA = [("c2_bf16_2p24", "ktanh64_bf16"), ("c3_f32_2p28", "ktanh_f32"), ("c3_f32_2p28", "ktanh_f32:p23"),
+         ("c3_f32_2p28", "ktanh_f32_via_bf16"), ("c4_lstm_gates", "lstm"),
          ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16"),
          ("c5_ffn_2p30", "kgelu_swish_bf16"), ("c5_ffn_2p30", "kgelu_bwd_bf16"),
          ("c4_lstm_gates", "lstm_cell")]

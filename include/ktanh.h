@@ -90,7 +90,34 @@ KT_API kt_status kt_lut_create(const int32_t E[32], const int32_t r[32], const i
 /* Handle for the paper's Table 1. */
 KT_API kt_status kt_lut_create_paper(kt_lut *out);
 
-/* Copy the handle's tables back out (host arrays of 32). */
+/* F32-native table re-optimised at p = 23 (the Sec. 2.4
+ * optimizer run with p = 23, "p = 7 in case of BFloat16").
+ * Same index t (= ((E & 3) << 3) | (M23 >> 20)), thresholds and Alg. 1, but
+ * b_t is in units of 2^-23: line 8 is M_o = (M23 >> r_t) + b_t.  Validation
+ * (KT_ERR_LUT): 0 <= r_t <= 23, 1 <= E_t <= 127, 0 <= M_o < 2^23 for every
+ * reachable M23, E_t == 127 only with M_o == 0.  The handle serves the F32
+ * calls only (ktanh/ksigmoid/kswish/kgelu_f32, their backward passes,
+ * kgelu_swish_f32, kt_apply / kt_apply_host with KT_F32); every call that
+ * reads BF16 data (incl. ktanh_f32_via_bf16, the LSTM and GEMM calls) returns
+ * KT_ERR_LUT for it.  Ownership as kt_lut_create. */
+KT_API kt_status kt_lut_create_f32(const int32_t E[32], const int32_t r[32], const int32_t b[32],
+                                   kt_lut *out);
+
+/* Build a table with the Sec. 2.4 optimizer (Steps 1-3,
+ * Eq. 2-3) from tanh itself, readings A12-A17 of DESIGN.md §3: p = 7 gives a
+ * BF16 table (the paper's "R*" table: it differs from the printed Table 1 in
+ * 6 of 32 rows) as kt_lut_create would; p = 23 gives the
+ * F32-native table as kt_lut_create_f32 would.  bmin_zero != 0 is the Sec.
+ * 3.1 ablation (b_min = 0).  Host-only, deterministic; p = 23
+ * takes well under a second on a multi-core host (intervals run on host
+ * threads).  KT_ERR_ARG for another p. */
+KT_API kt_status kt_lut_create_optimized(int32_t p, int32_t bmin_zero, kt_lut *out);
+
+/* Unit of the handle's b: *p = 7 (kt_lut_create / _paper) or 23 (kt_lut_create_f32). */
+KT_API kt_status kt_lut_mantissa_bits(kt_lut lut, int32_t *p);
+
+/* Copy the handle's tables back out (host arrays of 32; b in the
+ * handle's unit, see kt_lut_mantissa_bits). */
 KT_API kt_status kt_lut_get(kt_lut lut, int32_t E[32], int32_t r[32], int32_t b[32]);
 
 /* Release a handle; NULL is a no-op. */
@@ -105,6 +132,10 @@ typedef struct kt_lut64_s *kt_lut64;
 KT_API kt_status kt_lut64_create(const int32_t E[64], const int32_t r[64], const int32_t b[64],
                                  kt_lut64 *out);
 KT_API kt_status kt_lut64_get(kt_lut64 lut, int32_t E[64], int32_t r[64], int32_t b[64]);
+
+/* 64-interval table from the Sec. 2.4 optimizer with 4 mantissa index bits
+ * (as kt_lut_create_optimized with p = 7). */
+KT_API kt_status kt_lut64_create_optimized(int32_t bmin_zero, kt_lut64 *out);
 KT_API void kt_lut64_destroy(kt_lut64 lut);   /* NULL-safe */
 
 /* ---------------------------------------------------------------------- */

@@ -39,6 +39,8 @@ MAP_CALLS = ("ktanh_bf16", "ktanh_f32", "ksigmoid_bf16", "ksigmoid_f32",
 BWD_CALLS = ("ktanh_bwd_bf16", "ktanh_bwd_f32", "ksigmoid_bwd_bf16", "ksigmoid_bwd_f32")
 BWD_LUT_CALLS = ("kswish_bwd_bf16", "kswish_bwd_f32", "kgelu_bwd_bf16", "kgelu_bwd_f32")
 EXPORTS = MAP_CALLS + BWD_CALLS + BWD_LUT_CALLS + ("kt_apply_bwd", "kt_lut_create", "kt_lut_create_paper", "kt_lut_get", "kt_lut_destroy",
+                       "kt_lut_create_f32", "kt_lut_mantissa_bits", "kt_lut_create_optimized",
+                       "kt_lut64_create_optimized",
                        "klstm_gates_bf16", "klstm_cell_bf16", "kgemm_bf16", "kt_apply", "kt_apply_host", "kt_shard_range",
                        "kt_status_string", "kt_last_error", "kt_abi_version", "kt_launch_count",
                        "kt_apx_create", "kt_apx_coeffs", "kt_apx_destroy", "kt_apx_tanh_bf16",
@@ -62,6 +64,14 @@ _lib.kt_apply_bwd.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _sz, _v
 _lib.kt_apply_bwd.restype = ctypes.c_int
 _lib.kt_lut_create.argtypes = [_c_i32p, _c_i32p, _c_i32p, ctypes.POINTER(_vp)]
 _lib.kt_lut_create.restype = ctypes.c_int
+_lib.kt_lut_create_f32.argtypes = [_c_i32p, _c_i32p, _c_i32p, ctypes.POINTER(_vp)]
+_lib.kt_lut_create_f32.restype = ctypes.c_int
+_lib.kt_lut_mantissa_bits.argtypes = [_vp, ctypes.POINTER(ctypes.c_int32)]
+_lib.kt_lut_mantissa_bits.restype = ctypes.c_int
+_lib.kt_lut_create_optimized.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp)]
+_lib.kt_lut_create_optimized.restype = ctypes.c_int
+_lib.kt_lut64_create_optimized.argtypes = [ctypes.c_int32, ctypes.POINTER(_vp)]
+_lib.kt_lut64_create_optimized.restype = ctypes.c_int
 _lib.kt_lut_create_paper.argtypes = [ctypes.POINTER(_vp)]
 _lib.kt_lut_create_paper.restype = ctypes.c_int
 _lib.kt_lut_get.argtypes = [_vp, _c_i32p, _c_i32p, _c_i32p]
@@ -169,10 +179,35 @@ class Lut:
         _check(_lib.kt_lut_create(arr[0], arr[1], arr[2], ctypes.byref(h)), "kt_lut_create")
         return cls(h.value)
 
+    @classmethod
+    def optimized(cls, p: int = 7, bmin_zero: bool = False) -> "Lut":
+        """Sec. 2.4 optimizer in the library: p = 7 (BF16) or 23 (F32-native)."""
+        h = _vp()
+        _check(_lib.kt_lut_create_optimized(int(p), int(bmin_zero), ctypes.byref(h)),
+               "kt_lut_create_optimized")
+        return cls(h.value)
+
+    @classmethod
+    def from_tables_f32(cls, E, r, b) -> "Lut":
+        """F32-only table with b in 2^-23 units (re-optimised at p = 23, NEXT-3)."""
+        if any(len(a) != 32 for a in (E, r, b)):
+            raise ValueError("tables must have 32 entries")
+        arr = [(ctypes.c_int32 * 32)(*[int(v) for v in a]) for a in (E, r, b)]
+        h = _vp()
+        _check(_lib.kt_lut_create_f32(arr[0], arr[1], arr[2], ctypes.byref(h)), "kt_lut_create_f32")
+        return cls(h.value)
+
     def tables(self):
         E, r, b = ((ctypes.c_int32 * 32)() for _ in range(3))
         _check(_lib.kt_lut_get(self._h, E, r, b), "kt_lut_get")
         return list(E), list(r), list(b)
+
+    @property
+    def p(self) -> int:
+        """Unit of b: 7 (BF16 tables) or 23 (F32-only tables)."""
+        v = ctypes.c_int32()
+        _check(_lib.kt_lut_mantissa_bits(self._h, ctypes.byref(v)), "kt_lut_mantissa_bits")
+        return v.value
 
     @property
     def handle(self):
@@ -576,6 +611,16 @@ class Lut64:
         h = _vp()
         _check(_lib.kt_lut64_create(arr[0], arr[1], arr[2], ctypes.byref(h)), "kt_lut64_create")
         self._h = h
+
+    @classmethod
+    def optimized(cls, bmin_zero: bool = False) -> "Lut64":
+        """Sec. 2.4 optimizer with 4 mantissa index bits (64 intervals)."""
+        self = cls.__new__(cls)
+        h = _vp()
+        _check(_lib.kt_lut64_create_optimized(int(bmin_zero), ctypes.byref(h)),
+               "kt_lut64_create_optimized")
+        self._h = h
+        return self
 
     def tables(self):
         E, r, b = ((ctypes.c_int32 * 64)() for _ in range(3))

@@ -20,6 +20,7 @@ uint64_t launch_count();
 
 struct kt_lut_s {
   int32_t E[32], r[32], b[32];
+  int32_t p = 7;            // unit of b: 2^-7 (BF16 tables) or 2^-23 (kt_lut_create_f32)
   kt::LutWords words;
 };
 
@@ -123,6 +124,44 @@ kt_status validate_and_pack(const int32_t *E, const int32_t *r, const int32_t *b
   return KT_OK;
 }
 
+// F32-native table re-optimised at p = 23: b in units of
+// 2^-23, r in [0, 23]; Alg. 1 line 8 on F32 is M_o = (M23 >> r) + b.  Only
+// the F32 words exist (C_t of kt_internal.h with b_t 2^(p-7) -> b_t).
+kt_status validate_and_pack_f32(const int32_t *E, const int32_t *r, const int32_t *b, kt_lut_s *L) {
+  for (int t = 0; t < 32; ++t) {
+    if (r[t] < 0 || r[t] > 23) return fail(KT_ERR_LUT, "r[%d] = %d outside [0, 23]", t, r[t]);
+    if (E[t] < 1 || E[t] > 127) return fail(KT_ERR_LUT, "E[%d] = %d outside [1, 127]", t, E[t]);
+    int lo, hi;
+    reach(t, &lo, &hi);
+    const int64_t lo23 = (int64_t)lo << 16;
+    const int64_t hi23 = (t == 7) ? lo23 : (((int64_t)hi << 16) | 0xFFFF);
+    const int64_t mlo = (lo23 >> r[t]) + b[t], mhi = (hi23 >> r[t]) + b[t];   // monotone in M23
+    if (mlo < 0 || mhi > 0x7FFFFF)
+      return fail(KT_ERR_LUT, "entry %d: M_o in [%lld, %lld] leaves [0, 2^23 - 1]", t, (long long)mlo,
+                  (long long)mhi);
+    if (E[t] == 127 && mhi != 0)
+      return fail(KT_ERR_LUT, "entry %d: E=127 with M_o != 0 gives |y| > 1", t);
+  }
+  L->p = 23;
+  L->words = kt::LutWords{};
+  for (int t = 0; t < 32; ++t) {
+    L->E[t] = E[t];
+    L->r[t] = r[t];
+    L->b[t] = b[t];
+    L->words.f32K[t] = 1u << (31 - r[t]);
+    const int64_t c32 = ((int64_t)E[t] << 23) + (int64_t)b[t] - ((int64_t)e_in(t) << (23 - r[t]));
+    L->words.f32C[t] = (uint32_t)(c32 & 0xFFFFFFFFll);
+  }
+  return KT_OK;
+}
+
+// Calls that touch BF16 data need the BF16 words: a p = 23 table has none.
+kt_status need_bf16(kt_lut lut) {
+  if (lut && lut->p != 7)
+    return fail(KT_ERR_LUT, "table from kt_lut_create_f32 (b in 2^-23 units) serves F32 calls only");
+  return KT_OK;
+}
+
 // ---- device info ----------------------------------------------------------
 constexpr int kMaxDev = 64;
 int g_sm_count[kMaxDev];  // 0 = unknown
@@ -178,6 +217,10 @@ kt_status run_map(int op, int fmt, const void *x, void *y, size_t n, kt_lut lut,
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
   if (op < 0 || op > 4 || fmt < 0 || fmt > 1 || (op == 4 && fmt != kt::FMT_F32))
     return fail(KT_ERR_ARG, "bad op/dtype");
+  if (fmt == kt::FMT_BF16 || op == 4) {
+    kt_status s = need_bf16(lut);
+    if (s != KT_OK) return s;
+  }
   if (n == 0) return KT_OK;
   const size_t es = fmt == kt::FMT_BF16 ? 2 : 4;
   kt::LaunchInfo li;
@@ -198,6 +241,10 @@ kt_status run_bwd(int op, int fmt, const void *a, const void *dy, void *dx, size
   if (op < 0 || op > 3 || fmt < 0 || fmt > 1) return fail(KT_ERR_ARG, "bad op/dtype");
   if ((op == kt::OP_SWISH || op == kt::OP_GELU) && !lut)
     return fail(KT_ERR_ARG, "lut is NULL (needed to recompute K-TanH)");
+  if (fmt == kt::FMT_BF16) {
+    kt_status s = need_bf16(lut);
+    if (s != KT_OK) return s;
+  }
   if (n == 0) return KT_OK;
   const size_t es = fmt == kt::FMT_BF16 ? 2 : 4;
   if (!a || !dy || !dx) return fail(KT_ERR_ARG, "NULL pointer with n = %zu", n);
@@ -283,6 +330,32 @@ KT_API kt_status kt_lut_create(const int32_t E[32], const int32_t r[32], const i
   return KT_OK;
 }
 
+KT_API kt_status kt_lut_create_f32(const int32_t E[32], const int32_t r[32], const int32_t b[32],
+                                   kt_lut *out) {
+  if (!E || !r || !b || !out) return fail(KT_ERR_ARG, "NULL argument");
+  kt_lut_s tmp;
+  kt_status s = validate_and_pack_f32(E, r, b, &tmp);
+  if (s != KT_OK) return s;
+  kt_lut_s *L = new (std::nothrow) kt_lut_s(tmp);
+  if (!L) return fail(KT_ERR_ARG, "out of host memory");
+  *out = L;
+  return KT_OK;
+}
+
+KT_API kt_status kt_lut_create_optimized(int32_t p, int32_t bmin_zero, kt_lut *out) {
+  if (!out) return fail(KT_ERR_ARG, "NULL argument");
+  if (p != 7 && p != 23) return fail(KT_ERR_ARG, "p = %d: only 7 (BF16) and 23 (F32) tables", p);
+  int32_t E[32], r[32], b[32];
+  if (!kt::optimize_table(3, p, bmin_zero != 0, E, r, b)) return fail(KT_ERR_ARG, "optimizer failed");
+  return p == 7 ? kt_lut_create(E, r, b, out) : kt_lut_create_f32(E, r, b, out);
+}
+
+KT_API kt_status kt_lut_mantissa_bits(kt_lut lut, int32_t *p) {
+  if (!lut || !p) return fail(KT_ERR_ARG, "NULL argument");
+  *p = lut->p;
+  return KT_OK;
+}
+
 KT_API kt_status kt_lut_create_paper(kt_lut *out) {
   return kt_lut_create(kPaperE, kPaperR, kPaperB, out);
 }
@@ -330,6 +403,13 @@ KT_API kt_status kt_lut64_create(const int32_t E[64], const int32_t r[64], const
   if (!L) return fail(KT_ERR_ARG, "out of host memory");
   *out = L;
   return KT_OK;
+}
+
+KT_API kt_status kt_lut64_create_optimized(int32_t bmin_zero, kt_lut64 *out) {
+  if (!out) return fail(KT_ERR_ARG, "NULL argument");
+  int32_t E[64], r[64], b[64];
+  if (!kt::optimize_table(4, 7, bmin_zero != 0, E, r, b)) return fail(KT_ERR_ARG, "optimizer failed");
+  return kt_lut64_create(E, r, b, out);
 }
 
 KT_API kt_status kt_lut64_get(kt_lut64 lut, int32_t E[64], int32_t r[64], int32_t b[64]) {
@@ -391,6 +471,10 @@ KT_API kt_status kt_apply(kt_op op, kt_dtype dtype, const void *x, void *y, size
 static kt_status run_dual(int fmt, const void *x, void *yg, void *ys, size_t n, kt_lut lut,
                           void *stream) {
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (fmt == kt::FMT_BF16) {
+    kt_status s = need_bf16(lut);
+    if (s != KT_OK) return s;
+  }
   if (n == 0) return KT_OK;
   const size_t es = fmt == kt::FMT_BF16 ? 2 : 4;
   if (!x || !yg || !ys) return fail(KT_ERR_ARG, "NULL pointer with n = %zu", n);
@@ -466,6 +550,8 @@ KT_API kt_status kt_alu_probe(kt_dtype dtype, kt_lut lut, kt_apx apx, const void
                               int iters, double *cycles_net, double *cycles_gross) {
   if ((!lut) == (!apx)) return fail(KT_ERR_ARG, "pass exactly one of lut, apx");
   if ((int)dtype < 0 || (int)dtype > 1) return fail(KT_ERR_ARG, "bad dtype");
+  if (dtype == KT_BF16)
+    if (kt_status sb = need_bf16(lut)) return sb;
   if (!sample_host || !cycles_net || !cycles_gross || iters < 1)
     return fail(KT_ERR_ARG, "NULL argument or iters < 1");
   kt::LaunchInfo li;
@@ -519,6 +605,7 @@ KT_API kt_status kt_apply_bwd(kt_op op, kt_dtype dtype, const void *a, const voi
 KT_API kt_status klstm_gates_bf16(const uint16_t *x, uint16_t *y, size_t rows, size_t hidden,
                                   int tanh_quarter, kt_lut lut, void *stream) {
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (kt_status sb = need_bf16(lut)) return sb;
   if (hidden == 0) return fail(KT_ERR_ARG, "hidden == 0");
   if (tanh_quarter < 0 || tanh_quarter > 3) return fail(KT_ERR_ARG, "tanh_quarter not in 0..3");
   if (rows > SIZE_MAX / 4 / hidden) return fail(KT_ERR_ARG, "size overflow");
@@ -537,6 +624,7 @@ KT_API kt_status klstm_cell_bf16(const uint16_t *gates, const float *c_prev, flo
                                  uint16_t *h_next, size_t rows, size_t hidden, kt_lut lut,
                                  void *stream) {
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (kt_status sb = need_bf16(lut)) return sb;
   if (hidden == 0) return fail(KT_ERR_ARG, "hidden == 0");
   if (rows > SIZE_MAX / 4 / hidden) return fail(KT_ERR_ARG, "size overflow");
   const size_t n = rows * hidden;
@@ -566,6 +654,8 @@ static kt_status run_gemm(int epilogue, const uint16_t *A, const uint16_t *B, ui
                           size_t N, size_t K, kt_lut lut, void *stream, uint32_t lstm_hidden,
                           uint32_t lstm_tq) {
   if (epilogue >= 0 && !lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (epilogue >= 0)
+    if (kt_status sb = need_bf16(lut)) return sb;
   if (M == 0 || N == 0) return KT_OK;
   if (M % 128 || N % 256 || K % 64 || K == 0)
     return fail(KT_ERR_ARG, "kgemm needs M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (K > 0)");
@@ -609,6 +699,7 @@ KT_API kt_status kgemm_lstm_cell_bf16(const uint16_t *A, const uint16_t *B, cons
                                       float *c_next, uint16_t *h_next, size_t M, size_t hidden,
                                       size_t K, kt_lut lut, void *stream) {
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
+  if (kt_status sb = need_bf16(lut)) return sb;
   if (M == 0 || hidden == 0) return KT_OK;
   if (M % 128 || hidden % 64 || K % 64 || K == 0)
     return fail(KT_ERR_ARG, "needs M %% 128 == 0, hidden %% 64 == 0, K %% 64 == 0 (K > 0)");
@@ -680,6 +771,9 @@ KT_API kt_status kt_apply_host_ex(kt_op op, kt_dtype dtype, const void *x_host, 
   if (!lut) return fail(KT_ERR_ARG, "lut is NULL");
   if ((int)op < 0 || (int)op > 3 || (int)dtype < 0 || (int)dtype > 1)
     return fail(KT_ERR_ARG, "bad op/dtype");
+  if (dtype == KT_BF16)
+    if (kt_status sb = need_bf16(lut)) return sb;
+
   if (n == 0) return KT_OK;
   if (!x_host || !y_host) return fail(KT_ERR_ARG, "NULL pointer");
   const size_t es = dtype == KT_BF16 ? 2 : 4;

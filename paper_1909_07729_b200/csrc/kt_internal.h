@@ -90,6 +90,10 @@ cudaError_t launch_gemm_cell(const uint16_t *A, const uint16_t *B, const float *
                              uint16_t *h_next, size_t M, size_t H, size_t K, const LutWords &lut,
                              cudaStream_t s, int sms);
 
+// Sec. 2.4 optimizer (kt_tables.cu): 4 << s entries for s mantissa index bits,
+// p = 7 (BF16) or 23 (F32-native); false for unsupported (s, p).
+bool optimize_table(int s, int p, bool bmin_zero, int32_t *E, int32_t *r, int32_t *b);
+
 void count_launch();
 bool pdl_enabled();        // KT_PDL != 0
 bool prefetch_enabled();   // KT_PREFETCH != 0 (and PDL on)

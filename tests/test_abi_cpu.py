@@ -298,3 +298,83 @@ def test_lut_validation_matches_the_rule(kt, data):
         assert e.status == kt.KT_ERR_LUT
         accepted = False
     assert accepted == ok, (E, r, b)
+
+
+# ---- F32-native tables re-optimised at p = 23 -----------
+
+def test_lut_f32_accepts_p23_optimizer_table(kt):
+    L, _ = O.build_lut_sp(3, 23)
+    h = kt.Lut.from_tables_f32(L.E, L.r, L.b)
+    assert h.p == 23 and kt.Lut.paper().p == 7
+    assert h.tables() == (list(L.E), list(L.r), list(L.b))
+    T = O.table1()                           # Table 1 lifted to 2^-23 units is valid too
+    kt.Lut.from_tables_f32(T.E, T.r, [int(v) * 65536 for v in T.b])
+
+
+def test_lut_f32_validation_bounds(kt):
+    """b within the p = 23 bounds (PAPER.md:210-219 with p = 23) accepted, b_max + 1
+    and b_min - 1 rejected; r outside [0, 23] rejected."""
+    L, _ = O.build_lut_sp(3, 23)
+    rng = np.random.default_rng(1)
+    for _ in range(100):
+        E, r, b = L.E.copy(), L.r.copy(), L.b.copy()
+        t = int(rng.integers(0, 32))
+        if t == 7:
+            continue
+        r[t] = int(rng.integers(0, 24))
+        lo, hi = O.bounds_sp(int(r[t]), t & 7, 3, 23)
+        b[t] = int(rng.integers(lo, hi + 1))
+        kt.Lut.from_tables_f32(E, r, b)
+        # b_min = -v floor(2^(p-s-r)) is tight only for r <= p - s = 20
+        for bad in ((hi + 1, lo - 1) if r[t] <= 20 else (hi + 1,)):
+            b[t] = bad
+            with pytest.raises(kt.KTanhError) as ei:
+                kt.Lut.from_tables_f32(E, r, b)
+            assert ei.value.status == kt.KT_ERR_LUT
+    E, r, b = L.E.copy(), L.r.copy(), L.b.copy()
+    r[3] = 24
+    with pytest.raises(kt.KTanhError):
+        kt.Lut.from_tables_f32(E, r, b)
+    r[3], E[3] = L.r[3], 127                  # E = 127 needs M_o == 0
+    with pytest.raises(kt.KTanhError):
+        kt.Lut.from_tables_f32(E, r, b)
+
+
+def test_lut_f32_rejected_by_bf16_calls(kt):
+    """A p = 23 handle has no BF16 words: every BF16 call returns KT_ERR_LUT
+    before touching the device; F32 calls accept it (n == 0: no launch)."""
+    L, _ = O.build_lut_sp(3, 23)
+    h = kt.Lut.from_tables_f32(L.E, L.r, L.b).handle
+    lib = kt._lib
+    for name in kt.MAP_CALLS:
+        want = kt.KT_ERR_LUT if ("bf16" in name) else kt.KT_OK
+        assert getattr(lib, name)(None, None, 0, h, None) == want, name
+    assert lib.kt_apply(0, 0, None, None, 0, h, None) == kt.KT_ERR_LUT
+    assert lib.kt_apply(0, 1, None, None, 0, h, None) == kt.KT_OK
+    assert lib.kswish_bwd_bf16(None, None, None, 0, h, None) == kt.KT_ERR_LUT
+    assert lib.kswish_bwd_f32(None, None, None, 0, h, None) == kt.KT_OK
+    assert lib.kgelu_swish_bf16(None, None, None, 0, h, None) == kt.KT_ERR_LUT
+    assert lib.kgelu_swish_f32(None, None, None, 0, h, None) == kt.KT_OK
+    assert lib.klstm_gates_bf16(None, None, 0, 16, 2, h, None) == kt.KT_ERR_LUT
+    assert lib.klstm_cell_bf16(None, None, None, None, 0, 16, h, None) == kt.KT_ERR_LUT
+    assert lib.kgemm_bf16(None, None, None, 0, 0, 0, 3, h, None) == kt.KT_ERR_LUT
+    assert lib.kgemm_bf16(None, None, None, 0, 0, 0, -1, h, None) == kt.KT_OK
+    assert lib.kgemm_lstm_cell_bf16(None, None, None, None, None, 0, 0, 0, h, None) == kt.KT_ERR_LUT
+    assert "kt_lut_create_f32" in lib.kt_last_error().decode()
+
+
+def test_library_optimizer_matches_oracle(kt):
+    """kt_lut_create_optimized (product, kt_tables.cu) and the oracle's
+    kto_build_lut_sp are separate implementations of Sec. 2.4: identical tables
+    for p = 7 (both b_min readings), p = 23, and the 64-interval p = 7 table."""
+    for bz in (False, True):
+        L, _ = O.build_lut_sp(3, 7, bz)
+        h = kt.Lut.optimized(7, bz)
+        assert h.p == 7 and h.tables() == (list(L.E), list(L.r), list(L.b))
+        L64, _ = O.build_lut_sp(4, 7, bz)
+        assert kt.Lut64.optimized(bz).tables() == (list(L64.E), list(L64.r), list(L64.b))
+    L, _ = O.build_lut_sp(3, 23)
+    h = kt.Lut.optimized(23)
+    assert h.p == 23 and h.tables() == (list(L.E), list(L.r), list(L.b))
+    with pytest.raises(kt.KTanhError):
+        kt.Lut.optimized(10)

@@ -30,13 +30,13 @@ def kt():
     return kt
 
 
-def _oracle_parallel(op, bits, pool, nthreads):
+def _oracle_parallel(op, bits, pool, nthreads, lut=None):
     out = np.empty_like(bits)
     step = (bits.size + nthreads - 1) // nthreads
 
     def work(k):
         s = k * step
-        out[s:s + step] = O.map_f32(op, bits[s:s + step])
+        out[s:s + step] = O.map_f32(op, bits[s:s + step], lut)
     list(pool.map(work, range(nthreads)))
     return out
 
@@ -45,10 +45,17 @@ def _oracle_parallel(op, bits, pool, nthreads):
 @pytest.mark.parametrize("op,call,nan_by_class", [
     ("tanh", "ktanh_f32", False),
     ("sigmoid", "ksigmoid_f32", True),
-    ("tanh_via_bf16", "ktanh_f32_via_bf16", True)])
+    ("tanh_via_bf16", "ktanh_f32_via_bf16", True),
+    ("tanh", "ktanh_f32:p23", False)])
 def test_exhaustive_f32(kt, op, call, nan_by_class):
     """Every one of the 2^32 F32 bit patterns, bit-exact (NaN by class where
-    the GPU's arithmetic canonicalises the payload)."""
+    the GPU's arithmetic canonicalises the payload).  ":p23": with the F32
+    table re-optimised at p = 23 (kt_lut_create_f32, NEXT-3)."""
+    lut = hlut = None
+    if call.endswith(":p23"):
+        call = call[:-4]
+        lut = O.build_lut_sp(3, 23)[0]
+        hlut = kt.Lut.from_tables_f32(lut.E, lut.r, lut.b)
     fn = getattr(kt, call)
     nthreads = max(1, os.cpu_count() or 1)
     x = torch.empty(CHUNK, dtype=torch.float32, device="cuda")
@@ -57,9 +64,9 @@ def test_exhaustive_f32(kt, op, call, nan_by_class):
         for c in range(1 << 32 >> 28):
             bits = np.arange(c * CHUNK, (c + 1) * CHUNK, dtype=np.uint64).astype(np.uint32)
             x.copy_(torch.from_numpy(bits.view(np.int32)).view(torch.float32))
-            fn(x, out=y)
+            fn(x, out=y, lut=hlut)
             got = y.view(torch.int32).cpu().numpy().view(np.uint32)
-            want = _oracle_parallel(op, bits, pool, nthreads)
+            want = _oracle_parallel(op, bits, pool, nthreads, lut)
             assert_bitexact(got, want, 32, nan_by_class=nan_by_class, ctx=f"{op} chunk {c}")
 
 
