@@ -177,6 +177,12 @@ class Step:
         if op == "ktanh_f32:p23":             # F32-native table re-optimised at p = 23 (NEXT-3)
             h = kt.Lut.optimized(23)
             return lambda x, y: kt.ktanh_f32(x, out=y, lut=h)
+        if op.startswith("torch:"):           # library comparators (NEXT-4 context rows)
+            name = op[6:]
+            if name == "tanh":
+                return lambda x, y: torch.tanh(x, out=y)
+            approx = "tanh" if name == "gelu_tanh" else "none"
+            return lambda x, y: torch.ops.aten.gelu.out(x, approximate=approx, out=y)
         if op == "lstm":
             return lambda x, y: kt.klstm_gates_bf16(x, WL.LSTM_HIDDEN, 2, out=y)
         return lambda x, y: getattr(kt, op)(x, out=y)
@@ -475,7 +481,8 @@ def run_reference(args):
 TABLE2_MAPS = [("ktanh", None), ("sfu", "apx:sfu:0:0"), ("libm", "apx:libm:0:0"),
                ("pade_3_2", "apx:pade:3:2"), ("pade_7_8", "apx:pade:7:8"),
                ("minimax_2", "apx:minimax:2:0"), ("minimax_3", "apx:minimax:3:0"),
-               ("taylor_2", "apx:taylor:2:0"), ("taylor_3", "apx:taylor:3:0")]
+               ("taylor_2", "apx:taylor:2:0"), ("taylor_3", "apx:taylor:3:0"),
+               ("torch_tanh", "torch:tanh")]            # library (ATen) kernel, context
 
 
 def lstm_gemm_line(kt, K, W, world, device, rank):
@@ -547,6 +554,10 @@ def table2_b200(kt, K, W, world, device, rank, peak):
             y = kt.ktanh_bf16(xall)
             cyc, _ = kt.alu_probe("bf16", sample, lut=kt.paper_lut())
             st = Step(kt, "c2_bf16_2p24", "ktanh_bf16", device, rank)
+        elif op.startswith("torch:"):
+            y = torch.tanh(xall)
+            cyc = None
+            st = Step(kt, "c2_bf16_2p24", op, device, rank)
         else:
             _, kind, p, q = op.split(":")
             A = kt.Apx(kind, int(p), int(q))
@@ -564,12 +575,37 @@ def table2_b200(kt, K, W, world, device, rank, peak):
         rows[name] = {"max_abs_err": float(err.max()), "max_rel_err_pct": round(float(rel.max()) * 100, 4),
                       "gelem_s": round(st.n * world / (m_ / 1e3) / 1e9, 2),
                       "hbm_gbs_per_gpu": round(gbs, 1), "frac_of_measured": round(gbs / peak, 4),
-                      "sm_cycles_per_elem_per_sm": round(cyc, 4)}
+                      "sm_cycles_per_elem_per_sm": None if cyc is None else round(cyc, 4)}
+        del st
+        torch.cuda.empty_cache()
+    # GELU: K-GELU vs ATen's BF16 GELU (tanh form and erf form),
+    # accuracy against the exact x Phi(x) in binary64 over every finite BF16 input
+    import math
+    ref_g = np.zeros_like(xv)
+    ref_g[fin] = np.array([v * 0.5 * (1.0 + math.erf(v / math.sqrt(2.0))) for v in xv[fin]])
+    grows = {}
+    for name, op, fn in (("kgelu", "kgelu_bf16", lambda t: kt.kgelu_bf16(t)),
+                         ("torch_gelu_tanh", "torch:gelu_tanh",
+                          lambda t: torch.nn.functional.gelu(t, approximate="tanh")),
+                         ("torch_gelu_erf", "torch:gelu_erf", lambda t: torch.nn.functional.gelu(t))):
+        yb = fn(xall).view(torch.int16).cpu().numpy().view(np.uint16)
+        yv = (yb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        ok = fin & np.isfinite(ref_g)
+        err = np.abs(yv[ok] - ref_g[ok])
+        st = Step(kt, "c2_bf16_2p24", op, device, rank)
+        wts, _, _ = time_windows(st, K, W, world, device, None, min_total_s=0.3, max_windows=400)
+        m_ = statistics.median(wts) / K
+        gbs = st.bytes_per_step / (m_ / 1e3) / 1e9
+        grows[name] = {"max_abs_err_vs_exact_gelu": float(err.max()),
+                       "max_abs_err_abs_x_le_4": float(np.abs(yv - ref_g)[fin & (np.abs(xv) <= 4)].max()),
+                       "gelem_s": round(st.n * world / (m_ / 1e3) / 1e9, 2),
+                       "hbm_gbs_per_gpu": round(gbs, 1), "frac_of_measured": round(gbs / peak, 4)}
         del st
         torch.cuda.empty_cache()
     return {"workload": "accuracy: all finite BF16 inputs; throughput: c2_bf16_2p24 (BF16 in/out)",
             "note": "paper Table 2 (Intel CLX AVX512, cycles per TanH per core) is context only; "
-                    "readings R-CMP-* in DESIGN.md", "rows": rows}
+                    "readings R-CMP-* in DESIGN.md; torch_* rows are ATen library kernels",
+            "rows": rows, "gelu_rows": grows}
 
 
 def main():
