@@ -157,6 +157,45 @@ def launch_count() -> int:
     return int(_lib.kt_launch_count())
 
 
+# ---- parameter-table serialization (SURVEY.md §8(b) "a JSON table format") --
+# {format, exp_lsb_bits, man_msb_bits, b_unit_bits, t1_bits, t2_bits, E, r, b,
+#  provenance}; fixed key order and formatting, so equal tables give
+# byte-identical text.  Host-side marshalling only: the handle is created
+# (and validated) by the C ABI.
+
+def _table_json(fmt, s_bits, b_unit, E, r, b, provenance):
+    import json
+    t1, t2 = ("0x3E80", "0x4070") if fmt == "bfloat16" else ("0x3E800000", "0x40700000")
+    doc = {"format": fmt, "exp_lsb_bits": 2, "man_msb_bits": s_bits, "b_unit_bits": b_unit,
+           "t1_bits": t1, "t2_bits": t2, "E": [int(v) for v in E], "r": [int(v) for v in r],
+           "b": [int(v) for v in b], "provenance": str(provenance)}
+    return json.dumps(doc, indent=None, separators=(", ", ": ")) + "\n"
+
+
+def _table_dump(s_bits, E, r, b):
+    """Table 1's layout: index bit string, E_t, r_t, b_t."""
+    nb = 2 + s_bits
+    return "".join(f"{t:0{nb}b} {E[t]:4d} {r[t]:3d} {b[t]:9d}\n" for t in range(len(E)))
+
+
+def lut_from_json(text: str):
+    """Lut (32 entries; format bfloat16 with b_unit_bits 7, or float32 with
+    b_unit_bits 23) or Lut64 (man_msb_bits 4) from the JSON table format."""
+    import json
+    d = json.loads(text)
+    fmt, s_bits, unit = d["format"], int(d["man_msb_bits"]), int(d.get("b_unit_bits", 7))
+    if int(d.get("exp_lsb_bits", 2)) != 2:
+        raise ValueError("exp_lsb_bits must be 2 (Alg. 1 line 6)")
+    E, r, b = d["E"], d["r"], d["b"]
+    if fmt == "bfloat16" and unit == 7 and s_bits == 3:
+        return Lut.from_tables(E, r, b)
+    if fmt == "bfloat16" and unit == 7 and s_bits == 4:
+        return Lut64(E, r, b)
+    if fmt == "float32" and unit == 23 and s_bits == 3:
+        return Lut.from_tables_f32(E, r, b)
+    raise ValueError(f"unsupported table: format={fmt} man_msb_bits={s_bits} b_unit_bits={unit}")
+
+
 class Lut:
     """Immutable parameter-table handle (T_E, T_r, T_b), Alg. 1 line 1."""
 
@@ -201,6 +240,13 @@ class Lut:
         E, r, b = ((ctypes.c_int32 * 32)() for _ in range(3))
         _check(_lib.kt_lut_get(self._h, E, r, b), "kt_lut_get")
         return list(E), list(r), list(b)
+
+    def to_json(self, provenance: str = "") -> str:
+        fmt = "bfloat16" if self.p == 7 else "float32"
+        return _table_json(fmt, 3, self.p, *self.tables(), provenance)
+
+    def dump(self) -> str:
+        return _table_dump(3, *self.tables())
 
     @property
     def p(self) -> int:
@@ -626,6 +672,12 @@ class Lut64:
         E, r, b = ((ctypes.c_int32 * 64)() for _ in range(3))
         _check(_lib.kt_lut64_get(self._h, E, r, b), "kt_lut64_get")
         return list(E), list(r), list(b)
+
+    def to_json(self, provenance: str = "") -> str:
+        return _table_json("bfloat16", 4, 7, *self.tables(), provenance)
+
+    def dump(self) -> str:
+        return _table_dump(4, *self.tables())
 
     @property
     def handle(self):

@@ -378,3 +378,34 @@ def test_library_optimizer_matches_oracle(kt):
     assert h.p == 23 and h.tables() == (list(L.E), list(L.r), list(L.b))
     with pytest.raises(kt.KTanhError):
         kt.Lut.optimized(10)
+
+
+def test_table_json_roundtrip(kt):
+    """JSON table format (fields of SPEC.md:183): round trip for
+    BF16, F32 (p = 23) and 64-interval tables; byte-identical text for equal
+    tables; the text dump row 11000 of Table 1 reads (126, 0, 65)."""
+    import json
+    P = kt.Lut.paper()
+    j = P.to_json("Table 1, PAPER.md:225-252")
+    d = json.loads(j)
+    assert d["format"] == "bfloat16" and d["man_msb_bits"] == 3 and d["t1_bits"] == "0x3E80"
+    assert kt.lut_from_json(j).tables() == P.tables()
+    assert kt.lut_from_json(j).to_json("Table 1, PAPER.md:225-252") == j
+    row = [ln for ln in P.dump().splitlines() if ln.startswith("11000 ")][0].split()
+    assert row[1:] == ["126", "0", "65"]
+    F = kt.Lut.optimized(23)
+    jf = F.to_json()
+    assert json.loads(jf)["format"] == "float32" and json.loads(jf)["b_unit_bits"] == 23
+    G = kt.lut_from_json(jf)
+    assert G.p == 23 and G.tables() == F.tables()
+    L64 = kt.Lut64.optimized()
+    j64 = L64.to_json()
+    assert kt.lut_from_json(j64).tables() == L64.tables() and len(L64.dump().splitlines()) == 64
+    bad = json.loads(j)
+    bad["r"][3] = 9
+    with pytest.raises(kt.KTanhError):
+        kt.lut_from_json(json.dumps(bad))
+    bad = json.loads(j)
+    bad["man_msb_bits"] = 5
+    with pytest.raises(ValueError):
+        kt.lut_from_json(json.dumps(bad))
