@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <mutex>
 #include <new>
 #include <string>
@@ -151,6 +152,17 @@ kt_status validate_and_pack_f32(const int32_t *E, const int32_t *r, const int32_
     L->words.f32K[t] = 1u << (31 - r[t]);
     const int64_t c32 = ((int64_t)E[t] << 23) + (int64_t)b[t] - ((int64_t)e_in(t) << (23 - r[t]));
     L->words.f32C[t] = (uint32_t)(c32 & 0xFFFFFFFFll);
+  }
+  return KT_OK;
+}
+
+// The host optimizer allocates and starts threads: no C++ exception may
+// cross the C ABI.
+kt_status run_optimizer(int s, int p, int32_t bmin_zero, int32_t *E, int32_t *r, int32_t *b) {
+  try {
+    if (!kt::optimize_table(s, p, bmin_zero != 0, E, r, b)) return fail(KT_ERR_ARG, "optimizer failed");
+  } catch (const std::exception &ex) {
+    return fail(KT_ERR_ARG, "optimizer: %s", ex.what());
   }
   return KT_OK;
 }
@@ -346,7 +358,7 @@ KT_API kt_status kt_lut_create_optimized(int32_t p, int32_t bmin_zero, kt_lut *o
   if (!out) return fail(KT_ERR_ARG, "NULL argument");
   if (p != 7 && p != 23) return fail(KT_ERR_ARG, "p = %d: only 7 (BF16) and 23 (F32) tables", p);
   int32_t E[32], r[32], b[32];
-  if (!kt::optimize_table(3, p, bmin_zero != 0, E, r, b)) return fail(KT_ERR_ARG, "optimizer failed");
+  if (kt_status so = run_optimizer(3, p, bmin_zero, E, r, b)) return so;
   return p == 7 ? kt_lut_create(E, r, b, out) : kt_lut_create_f32(E, r, b, out);
 }
 
@@ -408,7 +420,7 @@ KT_API kt_status kt_lut64_create(const int32_t E[64], const int32_t r[64], const
 KT_API kt_status kt_lut64_create_optimized(int32_t bmin_zero, kt_lut64 *out) {
   if (!out) return fail(KT_ERR_ARG, "NULL argument");
   int32_t E[64], r[64], b[64];
-  if (!kt::optimize_table(4, 7, bmin_zero != 0, E, r, b)) return fail(KT_ERR_ARG, "optimizer failed");
+  if (kt_status so = run_optimizer(4, 7, bmin_zero, E, r, b)) return so;
   return kt_lut64_create(E, r, b, out);
 }
 
