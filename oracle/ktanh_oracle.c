@@ -266,11 +266,12 @@ uint32_t kto_ktanh_f32_via_bf16(uint32_t x, const int *TE, const int *Tr, const 
 /* GELU argument, decision precision binary32 (reading R-GELU-ARG):       */
 /*   C0 = f32(sqrt(2/pi)), C1 = f32(sqrt(2/pi) * a)                        */
 /*   u  = x * fma(C1, x*x, C0)        == sqrt(2/pi)(x + a x^3) in exact math */
+static const double GELU_A = 0.044715;
+
 static float gelu_arg_f32(float x)
 {
-    const double a = 0.044715;
     const float C0 = (float)sqrt(2.0 / M_PI);
-    const float C1 = (float)(sqrt(2.0 / M_PI) * a);
+    const float C1 = (float)(sqrt(2.0 / M_PI) * GELU_A);
     float x2 = x * x;
     float p = fmaf(C1, x2, C0);
     float u = x * p;
@@ -279,9 +280,8 @@ static float gelu_arg_f32(float x)
 
 uint32_t kto_gelu_consts(int which)   /* for the pin tests: bit patterns of C0, C1 */
 {
-    const double a = 0.044715;
     float C0 = (float)sqrt(2.0 / M_PI);
-    float C1 = (float)(sqrt(2.0 / M_PI) * a);
+    float C1 = (float)(sqrt(2.0 / M_PI) * GELU_A);
     return which == 0 ? bits_from_f32(C0) : bits_from_f32(C1);
 }
 
@@ -370,7 +370,7 @@ uint32_t kto_kgelu_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
 /* ------------------------------------------------------------------ */
 static double bwd_factor(int op, double a, double tv)
 {
-    const double c = sqrt(2.0 / M_PI), ga = 0.044715;
+    const double c = sqrt(2.0 / M_PI), ga = GELU_A;
     switch (op) {
     case 0: return 1.0 - a * a;
     case 1: return a * (1.0 - a);

@@ -320,3 +320,41 @@ def test_error_bounds_and_ordering():
     assert err[("pade", 7, 8)] < ktanh
     paper = {r[0]: r for r in read_golden("table2_comparators.txt")}
     assert float(paper["pade_7_8"][1]) < float(paper["ktanh_bf16"][1])
+
+
+@pytest.mark.parametrize("deg", [2, 3])
+def test_piecewise_layout_last_piece_and_saturation(deg):
+    """Reading R-CMP-LAYOUT: 16 pieces of width 1/2 cover [0, 8) and |x| >= 8
+    saturates.  On the last piece [7.5, 8) the minimax map is within its own
+    levelled error of tanh (binary64) -- not the constant 1 -- and from 8 on
+    it is exactly 1."""
+    A = O.Apx("minimax", deg)
+    _, E15, _ = O.minimax_piece(deg, 15)
+    xs = np.linspace(7.5, 8.0, 257)[:-1]
+    err = max(abs(A.eval(x) - math.tanh(x)) for x in xs)
+    assert err <= E15 * (1 + 1e-6) + 1e-15
+    assert all(A.eval(x) == 1.0 for x in (8.0, 8.5, 100.0))
+    T = O.Apx("taylor", deg)
+    assert max(abs(T.eval(x) - math.tanh(x)) for x in xs) < 1e-7 < 1.0 - math.tanh(7.5)
+
+
+@pytest.mark.parametrize("j,pq", [(3, (3, 2)), (8, (7, 8))])
+def test_pade_eval_is_the_lambert_convergent(j, pq):
+    """The comparator's evaluated map (not only its coefficients) is the Lambert
+    convergent below its saturation point, and exactly 1 from X_p on."""
+    A = O.Apx("pade", *pq)
+    X = A.xsat
+    for x in np.linspace(0.01, X * 0.999, 97):
+        assert A.eval(x) == pytest.approx(min(lambert_cf(j, x), 1.0), rel=1e-13, abs=1e-15)
+    assert A.eval(X * 1.001) == 1.0 and A.eval(50.0) == 1.0
+
+
+@pytest.mark.parametrize("deg", [2, 3])
+def test_taylor_pieces_interpolate_at_their_centres(deg):
+    """A Taylor polynomial equals the function at its expansion point: piece k
+    (k >= 1) is expanded about k/2 + 1/4 (reading R-CMP-LAYOUT), piece 0 about 0."""
+    T = O.Apx("taylor", deg)
+    for k in range(1, 16):
+        c = k / 2 + 0.25
+        assert T.eval(c) == pytest.approx(math.tanh(c), rel=1e-15, abs=1e-16), k
+    assert T.eval(0.0) == 0.0

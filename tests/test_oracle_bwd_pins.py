@@ -110,3 +110,19 @@ def test_f32_bwd_consistent_with_bf16_on_bf16_inputs():
         # sensitivity to t is <= 1/2 + |x| u'(x)
         sens = 0.5 + np.abs(xv) * (1 + 0.14 * xv ** 2)
         assert np.all(np.abs(g16 - g32) <= sens * 2 ** -7 + np.abs(g32) * 2 ** -8 + 1e-9), op
+
+
+def test_gelu_bwd_f32_bypass_transcription():
+    """Transcription check of R-BWD for GELU on F32 where K-TanH is the identity
+    (|u| < T1, Alg. 1 line 3), so t = u with no table involved:
+    g = (1 + u)/2 + (x/2)(1 - u^2) sqrt(2/pi)(1 + 3 a x^2), u from the golden a."""
+    a = float(read_golden("gelu_a.txt")[0][1])
+    c = math.sqrt(2 / math.pi)
+    x = np.linspace(-0.3, 0.3, 4001).astype(np.float32)
+    x = x[np.abs(c * (x + a * x.astype(np.float64) ** 3)) < 0.249]
+    g = O.bwd_f32("gelu", x.view(np.uint32), np.ones(x.size, np.float32).view(np.uint32))
+    g = g.view(np.float32).astype(np.float64)
+    xd = x.astype(np.float64)
+    u = c * (xd + a * xd ** 3)
+    want = 0.5 * (1 + u) + 0.5 * xd * (1 - u * u) * c * (1 + 3 * a * xd ** 2)
+    assert np.max(np.abs(g - want)) < 1e-6

@@ -152,3 +152,36 @@ def test_p23_dominates_lifted_rows(region, p23):
         sse[name] = np.bincount(t, weights=(y - ref) ** 2, minlength=32)
     for k in ks:
         assert sse["p23"][k] <= min(sse["t1"][k], sse["p7"][k]) * (1 + 1e-9) + 1e-18, k
+
+
+def _sumsq_exact(d):
+    """sum(d^2) for |d| < 2^31 without int64 overflow: split d = h 2^16 + l."""
+    h, l = d >> 16, d & 0xFFFF
+    return (int((h * h).sum()) << 32) + (int((h * l).sum()) << 17) + int((l * l).sum())
+
+
+def test_p23_rows_rederived_with_numpy_rounding(region, p23):
+    """Cross-check of Steps 1 and 3 on the non-clipping intervals: targets from
+    numpy's own RNE to F32, b_r = floor(mean(M^ - m/2^r) + 1/2) (A13, A14) in
+    exact integer arithmetic, clamped to Eq. 3, r = argmin of the integer
+    score with ties -> smaller r (A17): the oracle's (r, b) exactly."""
+    x, xv, ref, t, M = region
+    L, _ = p23
+    yb = ref.astype(np.float32).view(np.uint32)
+    for k in _no_clip_intervals(L, region):
+        m = t == k
+        Mh = (yb[m] & 0x7FFFFF).astype(np.int64)
+        mi = M[m].astype(np.int64)
+        cnt = int(mi.size)
+        sum_mh, sum_m = int(Mh.sum()), int(mi.sum())
+        best = None
+        for r in range(24):
+            S = (sum_mh << r) - sum_m                       # cnt 2^r b*, exact
+            b = (2 * S + (cnt << r)) // (cnt << (r + 1))     # floor(b* + 1/2)
+            lo, hi = O.bounds_sp(r, k & 7, 3, 23)
+            b = min(max(b, lo), hi)
+            d = Mh - (mi >> r) - b
+            score = _sumsq_exact(d)
+            if best is None or score < best[0]:
+                best = (score, r, b)
+        assert (int(L.r[k]), int(L.b[k])) == best[1:], k

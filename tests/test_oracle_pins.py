@@ -476,3 +476,73 @@ def test_via_bf16_error_bound_and_invariants():
     ys = O.map_f32("tanh_via_bf16", sp)
     assert (ys[0] & 0x7FFFFFFF) > 0x7F800000
     assert list(ys[1:]) == [0x3F800000, 0xBF800000, 0x3F800000, 0xBF800000, 0, 0x80000000]
+
+
+# --------------------------------------------------------------------------
+# Fused LSTM cell (reading R-LSTM-CELL): closed forms at saturated gates
+# --------------------------------------------------------------------------
+P_INF, N_INF = 0x7F80, 0xFF80          # K-Sigmoid(+inf) = 1, K-Sigmoid(-inf) = 0 (Alg. 1 line 4)
+
+
+def _cell(gi, gf, gg, go, c):
+    H = gi.size
+    gates = np.concatenate([gi, gf, gg, go]).astype(np.uint16)
+    return O.lstm_cell_bf16(gates, c.astype(np.float32).view(np.uint32), H)
+
+
+def test_lstm_cell_input_path_closed_form():
+    """i = 1, f = 0: c' = g exactly (the i g term alone); o = 1 and |g| < T1:
+    h' = g (K-TanH bypass, BF16-exact value)."""
+    rng = np.random.default_rng(21)
+    H = 4096
+    gg = rng.integers(0, 65536, H).astype(np.uint16)
+    gg = gg[np.isfinite(O.bf16_to_f64(gg))]
+    H = gg.size
+    one, zero = np.full(H, P_INF, np.uint16), np.full(H, N_INF, np.uint16)
+    c = (rng.standard_normal(H) * 3).astype(np.float32)
+    cn, hn = _cell(one, zero, gg, one, c)
+    g = O.map_bf16("tanh", gg)
+    assert np.array_equal(cn.view(np.float32), O.bf16_to_f64(g).astype(np.float32))
+    small = np.abs(O.bf16_to_f64(g)) < 0.25
+    assert small.sum() > 100 and np.array_equal(hn[small], g[small])
+
+
+def test_lstm_cell_forget_path_closed_form():
+    """i = 0, f = 1: c' = c exactly (the f c term alone); o = 1: h' = +-1 for
+    |c| > T2, RN_bf16(c) for |c| < T1 (Alg. 1 lines 3-4 on F32)."""
+    rng = np.random.default_rng(22)
+    H = 8192
+    c = (rng.standard_normal(H) * 4).astype(np.float32)
+    gg = rng.integers(0, 65536, H).astype(np.uint16)
+    gg[~np.isfinite(O.bf16_to_f64(gg))] = 0
+    one, zero = np.full(H, P_INF, np.uint16), np.full(H, N_INF, np.uint16)
+    cn, hn = _cell(zero, one, gg, one, c)
+    assert np.array_equal(cn, c.view(np.uint32))
+    h = O.bf16_to_f64(hn)
+    big, small = np.abs(c) > 3.75, np.abs(c) < 0.25
+    assert big.sum() > 100 and small.sum() > 100
+    assert np.array_equal(h[big], np.sign(c[big]).astype(np.float64))
+    want = np.array([O.bf16_encode_rne(float(v)) for v in c[small]], np.uint16)
+    assert np.array_equal(hn[small], want)
+
+
+def test_lstm_cell_output_gate_zero_and_bounds():
+    """o = 0: h' = +-0; generic gates: c' is f c + i g rounded once to F32 and
+    |h'| <= 1 with h' within the K-TanH error bound of o tanh(c')."""
+    rng = np.random.default_rng(23)
+    H = 8192
+    gi, gf, gg, go = (rng.standard_normal((4, H)) * 3).astype(np.float32)
+    b16 = lambda v: np.array([O.bf16_encode_rne(float(t)) for t in v], np.uint16)
+    gi, gf, gg, go = b16(gi), b16(gf), b16(gg), b16(go)
+    c = (rng.standard_normal(H) * 2).astype(np.float32)
+    _, h0 = _cell(gi, gf, gg, np.full(H, N_INF, np.uint16), c)
+    assert np.all((h0 & 0x7FFF) == 0)
+    cn, hn = _cell(gi, gf, gg, go, c)
+    i, f, o = (O.bf16_to_f64(O.map_bf16("sigmoid", v)) for v in (gi, gf, go))
+    g = O.bf16_to_f64(O.map_bf16("tanh", gg))
+    exact = f * c.astype(np.float64) + i * g
+    cnv = cn.view(np.float32).astype(np.float64)
+    assert np.all(np.abs(cnv - exact) <= np.spacing(np.abs(exact).astype(np.float32)).astype(np.float64) / 2)
+    h = O.bf16_to_f64(hn)
+    assert np.all(np.abs(h) <= 1.0)
+    assert np.all(np.abs(h - o * np.tanh(cnv)) <= 1.67e-2 + 2.0 ** -8)
