@@ -1,0 +1,116 @@
+"""Mutation check of the GPU parity tests: one plausible mistake at a time in
+a scratch copy of the CUDA sources, built into its own libktanh.so; the GPU
+parity tests, run against each mutant through KT_LIB, must fail.
+
+  python tools/kernel_mutants.py build [-j 4]   # here (nvcc cross-compiles): abtmp/mut_*.so
+  python tools/kernel_mutants.py run            # on the GPU box: one line per mutant
+"""
+import argparse
+import glob
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "abtmp")
+D = "kt_device.cuh"
+KK = "kt_kernels.cu"
+G = "kt_gemm.cu"
+# (name, file under csrc/, original text, mutated text, tests that must catch it)
+PARITY = "tests/test_gpu_parity.py"
+MUTANTS = [
+    ("bf16 T1 threshold", D, "constexpr uint32_t kT1x2 = 0x3E803E80u;",
+     "constexpr uint32_t kT1x2 = 0x3E813E81u;", PARITY),
+    ("f32 saturate at T2", D, "uint32_t y = (u2 > (kT2f << 1)) ? 0x3F800000u : ym;",
+     "uint32_t y = (u2 >= (kT2f << 1)) ? 0x3F800000u : ym;", PARITY),
+    ("sigmoid outer constant", D, "  return hfma2_bf16(t, kHalfx2, kHalfx2);",
+     "  return hfma2_bf16(t, kHalfx2, 0x3F013F01u);", PARITY),
+    ("gelu C1 one ulp", D, "constexpr uint32_t kGeluC1Bits = 0x3D122279u;",
+     "constexpr uint32_t kGeluC1Bits = 0x3D12227Au;", PARITY),
+    ("gelu bwd C3", D, "constexpr uint32_t kGeluC3Bits = 0x3DDB33B6u;",
+     "constexpr uint32_t kGeluC3Bits = 0x3DDB43B6u;", "tests/test_gpu_bwd.py"),
+    ("ragged tail off by one", KK, "scalar_span<OP, FMT>(x + toff, y + toff, tail, L);",
+     "scalar_span<OP, FMT>(x + toff, y + toff, tail ? tail - 1 : 0, L);", PARITY),
+    ("lstm cell double rounding", D, "return pack_bf16x2(mul_rodd(ov.y, th), mul_rodd(ov.x, tl));",
+     "return pack_bf16x2(ov.y * th, ov.x * tl);", PARITY),
+    ("via-bf16 rounding", D, "const uint32_t b = pack_bf16x2(0.0f, __uint_as_float(u));",
+     "const uint32_t b = u >> 16;", PARITY),
+    ("64-entry half select", D, "const uint32_t Ll = (x & 0x100u) ? l1 : l0;",
+     "const uint32_t Ll = (x & 0x80u) ? l1 : l0;", PARITY),
+    ("gemm epilogue column order", G,
+     "o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);",
+     "o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), lw);",
+     "tests/test_gpu_gemm.py"),
+    ("gemm cell gate order", G,
+     "const uint32_t gf = pack_bf16x2(__uint_as_float(r[32 + 2 * k + 1]), __uint_as_float(r[32 + 2 * k]));",
+     "const uint32_t gf = pack_bf16x2(__uint_as_float(r[96 + 2 * k + 1]), __uint_as_float(r[96 + 2 * k]));",
+     "tests/test_gpu_gemm.py"),
+]
+
+
+def slug(name):
+    return "".join(c if c.isalnum() else "_" for c in name)
+
+
+def build_one(m):
+    name, f, old, new, _ = m
+    sys.path.insert(0, os.path.join(ROOT, "paper_1909_07729_b200"))
+    import build as B
+    d = tempfile.mkdtemp(prefix="kt_kmut_")
+    try:
+        csrc = os.path.join(d, "csrc")
+        shutil.copytree(B.CSRC, csrc)
+        p = os.path.join(csrc, f)
+        s = open(p).read()
+        if s.count(old) != 1:
+            return name, f"NOT APPLIED ({s.count(old)} matches)"
+        open(p, "w").write(s.replace(old, new))
+        out = os.path.join(OUT, f"mut_{slug(name)}.so")
+        flags = [x for x in B.NVCC_FLAGS if x not in ("-Xptxas", "-v")]
+        cmd = ["nvcc"] + flags + ["-I", B.INCLUDE, "-I", csrc, "-o", out] + \
+            sorted(glob.glob(os.path.join(csrc, "*.cu")))
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return name, "built" if r.returncode == 0 else "BUILD FAILED: " + r.stderr[-300:]
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+
+
+def run_one(m):
+    name, _, _, _, tests = m
+    so = os.path.join(OUT, f"mut_{slug(name)}.so")
+    if not os.path.exists(so):
+        return name, "MISSING .so"
+    env = dict(os.environ, KT_LIB=so)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                        tests], cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
+    if r.returncode == 0:
+        return name, "SURVIVED"
+    failed = [ln for ln in r.stdout.splitlines() if ln.startswith("FAILED") or ln.startswith("ERROR")]
+    return name, "killed by " + (failed[0].split(" - ")[0] if failed else f"rc={r.returncode}")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", choices=["build", "run"])
+    ap.add_argument("-j", type=int, default=4)
+    args = ap.parse_args()
+    os.makedirs(OUT, exist_ok=True)
+    if args.mode == "build":
+        with ThreadPoolExecutor(args.j) as ex:
+            res = list(ex.map(build_one, MUTANTS))
+    else:
+        res = [run_one(m) for m in MUTANTS]
+    bad = 0
+    for name, verdict in res:
+        print(f"{name:30s} {verdict}", flush=True)
+        bad += args.mode == "run" and not verdict.startswith("killed")
+    if args.mode == "run":
+        print(f"{len(res) - bad}/{len(res)} mutants killed")
+    return 1 if bad else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
