@@ -429,6 +429,11 @@ def load_traffic(tag_substr):
     return None, None
 
 
+# --config: workload, library call, oracle / host-path op of the headline line
+HEADS = {"c1": ("c1_exhaustive_bf16", "ktanh_bf16", "tanh"), "c2": ("c2_bf16_2p24", "ktanh_bf16", "tanh"),
+         "c3": ("c3_f32_2p28", "ktanh_f32", "tanh"), "c4": ("c4_lstm_gates", "lstm", "lstm"),
+         "c5": ("c5_ffn_2p30", "kgelu_bf16", "gelu")}
+
 KERNEL_NAME = {"ktanh_bf16": "k_map<0, 0, true>", "ktanh_f32": "k_map<0, 1, true>",
                "kgelu_bf16": "k_map<3, 0, true>", "kswish_bf16": "k_map<2, 0, true>",
                "lstm": "k_lstm<true>"}
@@ -444,19 +449,28 @@ def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
         return 0
-    cfg = WL.CONFIGS["c2_bf16_2p24"]
+    key, _, op = HEADS[args.config]
+    cfg = WL.CONFIGS[key]
     import oracle as O
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     x = WL.make_input(cfg, device=dev)
-    m = 1 << 22                                   # bounded sample per step
-    xb = x.reshape(-1)[:m].view(torch.int16).cpu().numpy().view(np.uint16)
+    m = min(x.numel(), 1 << 22)                   # bounded sample per step
+    if op == "lstm":
+        m -= m % (4 * WL.LSTM_HIDDEN)             # whole gate rows
+    if cfg.dtype == torch.bfloat16:
+        xb = x.reshape(-1)[:m].view(torch.int16).cpu().numpy().view(np.uint16)
+        f = (lambda: O.lstm_gates_bf16(xb, WL.LSTM_HIDDEN, 2)) if op == "lstm" else \
+            (lambda: O.map_bf16(op, xb))
+    else:
+        xb = x.reshape(-1)[:m].view(torch.int32).cpu().numpy().view(np.uint32)
+        f = lambda: O.map_f32(op, xb)
     del x
     for _ in range(args.warmup):
-        O.map_bf16("tanh", xb)
+        f()
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        O.map_bf16("tanh", xb)
+        f()
         ts.append(time.perf_counter() - t0)
     sec = sum(ts) / len(ts)
     val = m / sec / 1e9
@@ -465,9 +479,10 @@ def run_reference(args):
         "metric": "K-TanH Gelem/s and achieved HBM GB/s vs ~8 TB/s peak at 1/2/4/8 B200",
         "value": round(val, 6), "unit": "Gelem/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "u16" if cfg.dtype == torch.bfloat16 else "u32", "data": "synthetic",
         "config": {"workload": cfg.key, "desc": cfg.desc, "elements_per_step": m,
-                   "note": "each step = a bounded sample (first 2^22 elements) of the workload"},
+                   "note": f"each step = a bounded sample (first {m} elements) of the workload"},
         "cpu_baseline": {"value": round(val, 6), "unit": "Gelem/s", "cores": 1, "kind": "oracle",
                          "sample": f"first {m} elements of {cfg.key}, {args.steps} timed steps",
                          "host_cpu": _cpu_model()},
@@ -616,6 +631,8 @@ def main():
     ap.add_argument("--impl", default="ktanh", choices=["ktanh", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip configs 3-5 side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--config", default="c2", choices=sorted(HEADS),
+                    help="workload of the headline line (default c2, BASELINE.json's metric config)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -645,7 +662,7 @@ def main():
         time.sleep(0.3)
 
     K, W = args.steps, args.warmup
-    head_key, head_op = "c2_bf16_2p24", "ktanh_bf16"
+    head_key, head_op, head_oracle_op = HEADS[args.config]
     step = Step(kt, head_key, head_op, device, rank)
     import hashlib
     input_sha = hashlib.sha256(step.xs[0].view(torch.int16).cpu().numpy().tobytes()).hexdigest()
@@ -656,12 +673,22 @@ def main():
     value = n_total / (ms / 1e3) / 1e9
     gbs_per_gpu = step.bytes_per_step / (ms / 1e3) / 1e9
     eager_ms = time_eager(step, K, device)
-    sets = step.sets
+    sets, head_bytes = step.sets, step.bytes_per_step
     del step
     torch.cuda.empty_cache()
 
-    e2e_ms, h2d, d2h = time_e2e(kt, WL.CONFIGS[head_key], "tanh", K, W, world, device, rank)
-    e2e_val = n_total / (e2e_ms / 1e3) / 1e9
+    if head_oracle_op != "lstm":
+        e2e_ms, h2d, d2h = time_e2e(kt, WL.CONFIGS[head_key], head_oracle_op, K, W, world, device, rank)
+        e2e_val = n_total / (e2e_ms / 1e3) / 1e9
+        e2e = {"value": round(e2e_val, 4), "unit": "Gelem/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4),
+               "path": f"kt_apply_host_ex (pinned host buffers, one chunk per step; steps "
+                       f"alternate over {E2E_STREAMS} caller streams so each D2H overlaps the next "
+                       f"step's H2D)"}
+    else:
+        e2e = {"value": None, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "note": "no host-buffer entry point for the LSTM gate call (kt_apply_host serves "
+                       "the elementwise ops)"}
 
     extra = {}
     if not args.no_extra:
@@ -728,7 +755,7 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(WL.CONFIGS[head_key], "tanh", device)
+        cpu = cpu_baseline(WL.CONFIGS[head_key], head_oracle_op, device)
 
     if clocks:
         clocks.stop()
@@ -736,17 +763,22 @@ def main():
     cold_traffic, cold_src = load_traffic("tanh_bf16")
     if traffic is None:
         traffic, traffic_src = cold_traffic, cold_src
+    if args.config != "c2":     # the committed DRAM captures are of the c2 launch
+        traffic, traffic_src = None, "not captured for this config (profiles/ holds the c2 capture)"
+        cold_traffic = cold_src = None
     if rank == 0:
         out = {
             "metric": "K-TanH Gelem/s and achieved HBM GB/s vs ~8 TB/s peak at 1/2/4/8 B200",
             "value": round(value, 3), "unit": "Gelem/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": round(ms, 6), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+            "vs_baseline": None, "dtype": "u16" if WL.CONFIGS[head_key].dtype == torch.bfloat16 else "u32",
+            "data": "synthetic",
             "config": {"workload": head_key, "desc": WL.CONFIGS[head_key].desc,
                        "input_sha256": input_sha,
                        "elements_per_gpu": WL.CONFIGS[head_key].numel, "call": head_op,
                        "parallelism": f"{world} independent shards (seed+rank), no collective",
-                       "l2": f"{sets} rotating input/output sets ({sets * 4 * WL.CONFIGS[head_key].numel >> 20} MiB > 4x L2)",
+                       "l2": (f"{sets} rotating input/output sets ({sets * head_bytes >> 20} MiB > 4x L2)"
+                              if sets > 1 else "inputs larger than L2"),
                        "launch": "CUDA graph of K library calls per timed window",
                        "windows": len(windows), "window_ms_median": round(ms_win, 5),
                        "window_ms_best": round(min(windows), 5)},
@@ -755,17 +787,13 @@ def main():
                          "unit": "GB/s", "frac": round(gbs_per_gpu / peak, 4),
                          "traffic": traffic, "peak_source": peak_src,
                          "frac_of_8tbs": round(gbs_per_gpu / NOMINAL_HBM_GBS, 4),
-                         "kernel": KERNEL_NAME[head_op],
-                         "algorithmic_bytes_per_launch": 4 * WL.CONFIGS[head_key].numel,
+                         "kernel": KERNEL_NAME.get(head_op, head_op),
+                         "algorithmic_bytes_per_launch": head_bytes,
                          "traffic_source": traffic_src,
                          "traffic_single_launch_cold": cold_traffic,
                          "traffic_single_launch_source": cold_src},
             "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_val, 4), "unit": "Gelem/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4),
-                    "path": f"kt_apply_host_ex (pinned host buffers, one chunk per step; steps "
-                            f"alternate over {E2E_STREAMS} caller streams so each D2H overlaps the next "
-                            f"step's H2D)"},
+            "e2e": e2e,
             "gpu_launches": int(round(lps * K)),
             "eager_ms_per_step": round(eager_ms, 6),
             "clocks": clk,
