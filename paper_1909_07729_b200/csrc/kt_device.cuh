@@ -379,8 +379,12 @@ __device__ __forceinline__ uint32_t apply_bwd_word(uint32_t a, uint32_t dy, cons
 __device__ __forceinline__ float mul_rodd(float a, float b) {
   const float p = __fmul_rz(a, b);
   const float r = __fmaf_rn(a, b, -p);                  // exact residual
-  const uint32_t pb = __float_as_uint(p);
-  return __uint_as_float(r != 0.0f ? (pb | 1u) : pb);
+  uint32_t pb = __float_as_uint(p);
+  // sticky bit as a predicated OR (FSETP + @P LOP3, no SEL: the cell kernel
+  // 20.33 -> 20.00 us, profiles/cell_variants_r01.txt)
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.f32 q, %1, 0f00000000;\n\t@q or.b32 %0, %0, 1;\n\t}"
+      : "+r"(pb) : "f"(r));
+  return __uint_as_float(pb);
 }
 
 // 2 cells: gate words gi, gf, gg, go (BF16 pairs), c (2 floats) -> c', h (BF16 pair)
