@@ -409,3 +409,25 @@ def test_table_json_roundtrip(kt):
     bad["man_msb_bits"] = 5
     with pytest.raises(ValueError):
         kt.lut_from_json(json.dumps(bad))
+
+
+def _build_c_demo(kt, tmp_path):
+    import subprocess
+    exe = str(tmp_path / "c_api_demo")
+    libdir = os.path.dirname(kt.LIB_PATH)
+    cmd = ["gcc", "-std=c11", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+           "-I", "/usr/local/cuda/include", os.path.join(ROOT, "examples", "c_api_demo.c"),
+           "-L", libdir, "-lktanh", "-L", "/usr/local/cuda/lib64", "-lcudart",
+           f"-Wl,-rpath,{libdir}", "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_demo_builds_and_runs_host_part(kt, tmp_path):
+    """The C ABI from plain C (gcc, no torch): table handles, the optimizer and
+    validation errors (examples/c_api_demo.c, --no-gpu)."""
+    import subprocess
+    exe = _build_c_demo(kt, tmp_path)
+    out = subprocess.run([exe, "--no-gpu"], check=True, capture_output=True, text=True).stdout
+    assert "Table 1, row 11000: E=126 r=0 b=65" in out
+    assert "p = 23 table" in out and "KT_ERR_LUT" in out

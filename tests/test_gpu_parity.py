@@ -617,3 +617,14 @@ def test_apply_host_ex_chunks(kt, chunk):
     for x, y in zip(xs, ys):
         want = O.map_bf16("gelu", x.view(torch.int16).numpy().view(np.uint16))
         assert_ulp(y.view(torch.int16).numpy().view(np.uint16), want, 16, 1, ctx=f"chunk={chunk}")
+
+
+def test_c_demo_on_gpu(kt, tmp_path):
+    """examples/c_api_demo.c on the GPU: the worked examples (SURVEY.md §4,
+    Alg. 1 by hand) through the C ABI from plain C."""
+    import subprocess
+    from test_abi_cpu import _build_c_demo
+    out = subprocess.run([_build_c_demo(kt, tmp_path)], check=True, capture_output=True, text=True).stdout
+    for line in ("K-TanH(0.125) = 0.125", "K-TanH(0.5) = 0.46875", "K-TanH(1) = 0.75390625",
+                 "K-TanH(2) = 0.96484375", "K-TanH(-5) = -1"):
+        assert line in out, out
