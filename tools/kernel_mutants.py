@@ -19,6 +19,8 @@ OUT = os.path.join(ROOT, "abtmp")
 D = "kt_device.cuh"
 KK = "kt_kernels.cu"
 G = "kt_gemm.cu"
+API = "kt_api.cu"
+APX = "kt_apx.cu"
 # (name, file under csrc/, original text, mutated text, tests that must catch it)
 PARITY = "tests/test_gpu_parity.py"
 MUTANTS = [
@@ -48,6 +50,26 @@ MUTANTS = [
      "const uint32_t gf = pack_bf16x2(__uint_as_float(r[32 + 2 * k + 1]), __uint_as_float(r[32 + 2 * k]));",
      "const uint32_t gf = pack_bf16x2(__uint_as_float(r[96 + 2 * k + 1]), __uint_as_float(r[96 + 2 * k]));",
      "tests/test_gpu_gemm.py"),
+    ("p = 23 table word", API,
+     "((int64_t)E[t] << 23) + (int64_t)b[t] - ((int64_t)e_in(t) << (23 - r[t]));",
+     "((int64_t)E[t] << 23) + (int64_t)b[t] + 1 - ((int64_t)e_in(t) << (23 - r[t]));",
+     "tests/test_gpu_f32_tables.py"),
+    ("pair GEMM B rank offset", G, "(int)(nb * 256 + rank * Sh::kBRows)", "(int)(nb * 256)",
+     "tests/test_gpu_gemm.py"),
+    ("f32 inf takes bypass", D, "const bool byp = (u2 - (kT1f << 1)) > ((kInff << 1) - (kT1f << 1));",
+     "const bool byp = (u2 - (kT1f << 1)) >= ((kInff << 1) - (kT1f << 1));", PARITY),
+    ("swish bwd factor", D, "return fma2(mul2(hx, half), fma2(neg2(t), t, splat2(1.0f)), fma2(t, half, half));",
+     "return fma2(hx, fma2(neg2(t), t, splat2(1.0f)), fma2(t, half, half));", "tests/test_gpu_bwd.py"),
+    ("dual kernel output swap", KK, "    st256(ys + hb + i * kVecBytes, sw, i < nvec);",
+     "    st256(ys + hb + i * kVecBytes, g, i < nvec);", PARITY),
+    ("taylor comparator centre", APX, "h = __fsub_rn(h, k != 0 ? 0.25f : 0.0f);",
+     "h = __fsub_rn(h, k != 0 ? 0.2f : 0.0f);", "tests/test_gpu_apx.py"),
+    ("pade comparator saturation", APX, "return a >= w.xsat ? 1.0f : y;", "return a > 2.0f * w.xsat ? 1.0f : y;",
+     "tests/test_gpu_apx.py"),
+    ("host pipeline chunk offset", API,
+     "KT_CK(cudaMemcpyAsync(yh + off * es, dy, cnt * es, cudaMemcpyDeviceToHost, d2h), \"D2H\");",
+     "KT_CK(cudaMemcpyAsync(yh + off * es, dy, (cnt - (cnt > 1)) * es, cudaMemcpyDeviceToHost, d2h), \"D2H\");",
+     PARITY),
 ]
 
 
