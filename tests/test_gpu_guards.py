@@ -98,3 +98,46 @@ def test_gemm_lstm_guards(kt):
     for buf, n in ((gbuf, M * 4 * H), (cbuf, M * H), (hbuf, M * H)):
         b = buf.float().cpu().numpy()
         assert np.all(b[:4096] == -7.0) and np.all(b[4096 + n:] == -7.0)
+
+
+@pytest.mark.parametrize("n", [1, 17, 4097, 65537])
+@pytest.mark.parametrize("off", [0, 3])
+def test_other_streaming_guards(kt, n, off):
+    """Fused GELU+Swish, 64-interval K-TanH, via-BF16 and the Table 2
+    comparators (flat and pipelined launches) write only their outputs."""
+    x = (torch.randn(n, device="cuda") * 3).to(torch.bfloat16)
+    gb, g = guarded(n, torch.bfloat16, off)
+    sb, s = guarded(n, torch.bfloat16, off + 1)
+    kt.kgelu_swish_bf16(x, out_gelu=g, out_swish=s)
+    assert intact(gb, n, off) and intact(sb, n, off + 1)
+    E, r, b = kt.paper_lut().tables()
+    t64 = [(((t >> 4) << 3) | ((t & 15) >> 1)) for t in range(64)]
+    L64 = kt.Lut64([E[i] for i in t64], [r[i] for i in t64], [b[i] for i in t64])
+    buf, y = guarded(n, torch.bfloat16, off)
+    kt.ktanh64_bf16(x, L64, out=y)
+    assert intact(buf, n, off)
+    xf = x.float()
+    buf, y = guarded(n, torch.float32, off)
+    kt.ktanh_f32_via_bf16(xf, out=y)
+    assert intact(buf, n, off)
+    for kind, p, q in (("pade", 7, 8), ("minimax", 3, 0), ("taylor", 2, 0)):
+        A = kt.Apx(kind, p, q)
+        buf, y = guarded(n, torch.bfloat16, off)
+        kt.kt_apx_tanh_bf16(x, A, out=y)
+        assert intact(buf, n, off), kind
+        buf, y = guarded(n, torch.float32, off)
+        kt.kt_apx_tanh_f32(xf, A, out=y)
+        assert intact(buf, n, off), kind
+
+
+@pytest.mark.parametrize("n", [1, 1000, 3 * 65536 + 7])
+def test_apply_host_guards(kt, n):
+    """The host-buffer pipeline writes only the n output elements of the
+    (pinned) host buffer."""
+    x = (torch.randn(n) * 3).to(torch.bfloat16).pin_memory()
+    buf = torch.full((n + 2 * G,), -7.0, dtype=torch.bfloat16).pin_memory()
+    work = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    kt.apply_host("tanh", x, buf[G:G + n], work, chunk=4096)
+    torch.cuda.synchronize()
+    b = buf.float().numpy()
+    assert np.all(b[:G] == -7.0) and np.all(b[G + n:] == -7.0)
