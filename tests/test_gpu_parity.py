@@ -628,3 +628,47 @@ def test_c_demo_on_gpu(kt, tmp_path):
     for line in ("K-TanH(0.125) = 0.125", "K-TanH(0.5) = 0.46875", "K-TanH(1) = 0.75390625",
                  "K-TanH(2) = 0.96484375", "K-TanH(-5) = -1"):
         assert line in out, out
+
+
+def test_library_allocates_no_device_memory(kt):
+    """include/ktanh.h: the device entry points allocate nothing (free device
+    memory is unchanged across a burst of calls of every kind, outputs
+    preallocated by the caller)."""
+    n = 1 << 20
+    x = (torch.randn(n, device="cuda") * 3).to(torch.bfloat16)
+    xf = x.float()
+    y, y2 = torch.empty_like(x), torch.empty_like(x)
+    yf = torch.empty_like(xf)
+    H = 1024
+    g = x[: 64 * 4 * H].view(64, 4 * H)
+    c = torch.randn(64, H, device="cuda")
+    cn, hn = torch.empty_like(c), torch.empty(64, H, dtype=torch.bfloat16, device="cuda")
+    A, B = x[: 256 * 256].view(256, 256), x[: 512 * 256].view(512, 256)
+    C = torch.empty(256, 512, dtype=torch.bfloat16, device="cuda")
+    G4 = torch.empty(256, 4 * 256, dtype=torch.bfloat16, device="cuda")
+    B4 = x[: 4 * 256 * 256].view(4 * 256, 256)
+    c2, cn2, hn2 = torch.randn(256, 256, device="cuda"), torch.empty(256, 256, device="cuda"), \
+        torch.empty(256, 256, dtype=torch.bfloat16, device="cuda")
+    apx = kt.Apx("minimax", 3)
+
+    def burst():
+        for op in ("tanh", "sigmoid", "swish", "gelu"):
+            getattr(kt, f"k{op}_bf16")(x, out=y)
+            getattr(kt, f"k{op}_f32")(xf, out=yf)
+            getattr(kt, f"k{op}_bwd_bf16")(x, x, out=y)
+        kt.ktanh_f32_via_bf16(xf, out=yf)
+        kt.kgelu_swish_bf16(x, out_gelu=y, out_swish=y2)
+        kt.klstm_gates_bf16(g, H, 2, out=y[: g.numel()].view_as(g))
+        kt.klstm_cell_bf16(g, c, H, c_next=cn, h_next=hn)
+        kt.kgemm_bf16(A, B, epilogue="gelu", out=C)
+        kt.kgemm_lstm_gates_bf16(A, B4, 256, 2, out=G4)
+        kt.kgemm_lstm_cell_bf16(A, B4, c2, 256, c_next=cn2, h_next=hn2)
+        kt.kt_apx_tanh_bf16(x, apx, out=y)
+    burst()                                          # first calls: lazy one-time setup
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(50):
+        burst()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free1 == free0
