@@ -672,3 +672,50 @@ def test_library_allocates_no_device_memory(kt):
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert free1 == free0
+
+
+_GRAPH_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1909_07729_b200 as kt
+torch.manual_seed(0)
+x = (torch.randn(1 << 18, device="cuda") * 3).to(torch.bfloat16)
+A = x[: 256 * 256].view(256, 256); B4 = x[: 1024 * 256].view(1024, 256)
+c = torch.randn(256, 256, device="cuda")
+outs = {"t": torch.empty_like(x), "g": torch.empty_like(x), "s": torch.empty_like(x),
+        "C": torch.empty(256, 1024, dtype=torch.bfloat16, device="cuda"),
+        "G": torch.empty(256, 1024, dtype=torch.bfloat16, device="cuda"),
+        "cn": torch.empty_like(c), "hn": torch.empty(256, 256, dtype=torch.bfloat16, device="cuda"),
+        "m": torch.empty_like(x)}
+apx = kt.Apx("minimax", 3)
+def work():
+    kt.ktanh_bf16(x, out=outs["t"])
+    kt.kgelu_swish_bf16(x, out_gelu=outs["g"], out_swish=outs["s"])
+    kt.kgemm_bf16(A, B4, epilogue="gelu", out=outs["C"])
+    kt.kgemm_lstm_gates_bf16(A, B4, 256, 2, out=outs["G"])
+    kt.kgemm_lstm_cell_bf16(A, B4, c, 256, c_next=outs["cn"], h_next=outs["hn"])
+    kt.kt_apx_tanh_bf16(x, apx, out=outs["m"])
+s = torch.cuda.Stream()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=s):          # the very first calls happen inside the capture
+    work()
+for v in outs.values(): v.zero_()
+g.replay(); torch.cuda.synchronize()
+got = {k: v.clone() for k, v in outs.items()}
+work(); torch.cuda.synchronize()
+for k in outs:
+    assert torch.equal(got[k].view(torch.uint8), outs[k].view(torch.uint8)), k
+print("graph ok")
+"""
+
+
+def test_first_calls_inside_graph_capture(kt):
+    """Every launch path is capturable even when the process's FIRST call of
+    each entry point happens inside a CUDA-graph capture (lazy one-time setup
+    such as cudaFuncSetAttribute included); replay == eager, bitwise."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    r = subprocess.run([sys.executable, "-c", _GRAPH_SCRIPT, ROOT], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "graph ok" in r.stdout, r.stderr[-3000:]
