@@ -719,3 +719,36 @@ def test_first_calls_inside_graph_capture(kt):
     r = subprocess.run([sys.executable, "-c", _GRAPH_SCRIPT, ROOT], capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "graph ok" in r.stdout, r.stderr[-3000:]
+
+
+def test_concurrent_threads_mixed_calls(kt):
+    """include/ktanh.h 'threads': one LUT handle shared by 8 host threads, each
+    issuing a different mix of calls on its own stream; results equal the
+    single-thread ones bitwise."""
+    from concurrent.futures import ThreadPoolExecutor
+    n = (1 << 20) + 13
+    xs = [(torch.randn(n, device="cuda") * (1 + k)).to(torch.bfloat16) for k in range(8)]
+    lut = kt.paper_lut()
+    ops = ["ktanh_bf16", "ksigmoid_bf16", "kswish_bf16", "kgelu_bf16"]
+
+    def job(k, stream=None):
+        x = xs[k]
+        outs = []
+        for rep in range(20):
+            f = getattr(kt, ops[(k + rep) % 4])
+            outs.append(f(x, lut=lut, stream=stream))
+        return outs
+
+    want = [job(k) for k in range(8)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(8)]
+
+    def run(k):
+        with torch.cuda.stream(streams[k]):
+            return job(k, stream=streams[k])
+    with ThreadPoolExecutor(8) as pool:
+        got = list(pool.map(run, range(8)))
+    torch.cuda.synchronize()
+    for k in range(8):
+        for a, b in zip(got[k], want[k]):
+            assert torch.equal(a.view(torch.int16), b.view(torch.int16))
