@@ -169,3 +169,29 @@ def test_gemm_lstm_cell_bad_args(kt):
     c = torch.zeros(128, 96, device="cuda")
     with pytest.raises(kt.KTanhError):
         kt.kgemm_lstm_cell_bf16(A, B, c, 96)                             # hidden % 64 != 0
+
+
+def test_ffn_gemm_full_size(kt):
+    """bench.py's FFN line at full size (65536 x 16384 x 4096, inputs from
+    workloads/, the 1-CTA fused kernel the bench times): the fused K-GELU
+    output equals kgelu_bf16 of the plain GEMM output on every element, and
+    sampled plain outputs are within the bound of test_gemm_vs_float64 of the
+    float64 dot products."""
+    import workloads as WL
+    M, N, K = 65536, 16384, 4096
+    A = WL.make_input("c5_ffn_2p30", device="cuda", numel=M * K).reshape(M, K)
+    B = (WL.make_input("c5_ffn_2p30", device="cuda", numel=N * K, seed=7).reshape(N, K) * 0.02
+         ).to(torch.bfloat16)
+    fused = kt.kgemm_bf16(A, B, epilogue="gelu")
+    plain = kt.kgemm_bf16(A, B)
+    ref = kt.kgelu_bf16(plain)
+    assert torch.equal(fused.view(torch.int16), ref.view(torch.int16))
+    del fused, ref
+    rng = np.random.default_rng(12)
+    r, c = rng.integers(0, M, 4096), rng.integers(0, N, 4096)
+    a = O.bf16_to_f64(u16(A[torch.from_numpy(r).cuda()]))
+    b = O.bf16_to_f64(u16(B[torch.from_numpy(c).cuda()]))
+    exact = (a * b).sum(axis=1)
+    got = O.bf16_to_f64(u16(plain[torch.from_numpy(r).cuda(), torch.from_numpy(c).cuda()]))
+    bound = np.abs(exact) * 2.0 ** -8 + K * 2.0 ** -23 * (np.abs(a) * np.abs(b)).sum(axis=1) + 1e-30
+    assert np.all(np.abs(got - exact) <= bound)
