@@ -104,6 +104,8 @@ def lib():
             L.kto_bwd_map_f32_p.argtypes = [ctypes.c_int, u32p, u32p, u32p, ctypes.c_size_t, ip, ip,
                                             ip, ctypes.c_int]
             L.kto_bwd_map_f32_p.restype = None
+            L.kto_rn32_exact_sum.argtypes = [ctypes.c_double, ctypes.c_double]
+            L.kto_rn32_exact_sum.restype = ctypes.c_float
             L.kto_ktanh_f32_p23.argtypes = [ctypes.c_uint32, ip, ip, ip]
             L.kto_ktanh_f32_p23.restype = ctypes.c_uint32
             L.kto_gelu_consts.argtypes = [ctypes.c_int]
@@ -235,6 +237,10 @@ def interval_sse(t: int, lut: Lut) -> float:
 
 def overflow_flag() -> bool:
     return bool(lib().kto_overflow_flag())
+
+
+def rn32_exact_sum(a: float, b: float) -> float:
+    return float(lib().kto_rn32_exact_sum(float(a), float(b)))
 
 
 def gelu_consts():

@@ -268,6 +268,29 @@ uint32_t kto_ktanh_f32_via_bf16(uint32_t x, const int *TE, const int *Tr, const 
 /*   u  = x * fma(C1, x*x, C0)        == sqrt(2/pi)(x + a x^3) in exact math */
 static const double GELU_A = 0.044715;
 
+/* RN32 of the EXACT sum a + b of two doubles.  Reading R-DERIVED (and
+ * R-LSTM-CELL) round the exact value of the outer step ONCE to binary32; for
+ * F32 data that value can need more than binary64's 53 bits (x/2 (1 + t) with
+ * a 24-bit t spans up to 65 bits), so evaluating it in binary64 and then
+ * converting would round twice.  s = RN64(a + b) with its exact error e
+ * (Knuth's TwoSum); RN32(s) equals RN32(a + b) unless s lies exactly halfway
+ * between two floats and e != 0, in which case e decides the side. */
+static float rn32_exact_sum(double a, double b)
+{
+    double s = a + b;
+    if (!isfinite(s) || !isfinite(a) || !isfinite(b)) return (float)s;
+    double bb = s - a;
+    double e = (a - (s - bb)) + (b - bb);
+    float f = (float)s;
+    if (e == 0.0 || (double)f == s || isinf(f)) return f;
+    float g = (s > (double)f) ? nextafterf(f, INFINITY) : nextafterf(f, -INFINITY);
+    double mid = ((double)f + (double)g) / 2.0;      /* exact in binary64 */
+    if (s != mid) return f;
+    return ((e > 0.0) == ((double)g > (double)f)) ? g : f;
+}
+
+float kto_rn32_exact_sum(double a, double b) { return rn32_exact_sum(a, b); }   /* for the pins */
+
 static float gelu_arg_f32(float x)
 {
     const float C0 = (float)sqrt(2.0 / M_PI);
@@ -323,7 +346,8 @@ static uint32_t kswish_f32_pb(uint32_t x, const int *TE, const int *Tr, const in
     float h = (float)(xv / 2.0);
     uint32_t t = ktanh_f32_pb(bits_from_f32(h), TE, Tr, Tb, pb);
     double tv = (double)f32_from_bits(t);
-    return bits_from_f32((float)(xv * (1.0 + tv) / 2.0));
+    const double hx = xv / 2.0;                           /* exact */
+    return bits_from_f32(rn32_exact_sum(hx, hx * tv));    /* RN32(x (1+t)/2), products exact */
 }
 
 uint32_t kto_kswish_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
@@ -347,7 +371,8 @@ static uint32_t kgelu_f32_pb(uint32_t x, const int *TE, const int *Tr, const int
     float u = gelu_arg_f32(xf);
     uint32_t t = ktanh_f32_pb(bits_from_f32(u), TE, Tr, Tb, pb);
     double tv = (double)f32_from_bits(t);
-    return bits_from_f32((float)((double)xf / 2.0 * (1.0 + tv)));
+    const double hx = (double)xf / 2.0;                   /* exact */
+    return bits_from_f32(rn32_exact_sum(hx, hx * tv));    /* RN32(x/2 (1+t)) */
 }
 
 uint32_t kto_kgelu_f32(uint32_t x, const int *TE, const int *Tr, const int *Tb)
@@ -509,7 +534,7 @@ void kto_lstm_cell_bf16(const uint16_t *gates, const uint32_t *c_prev, uint32_t 
             double g = kto_bf16_decode(kto_ktanh_bf16(gr[2 * hidden + j], TE, Tr, Tb));
             double o = kto_bf16_decode(kto_ksigmoid_bf16(gr[3 * hidden + j], TE, Tr, Tb));
             double c = (double)f32_from_bits(c_prev[r * hidden + j]);
-            float cn = (float)(f * c + i * g);
+            float cn = rn32_exact_sum(f * c, i * g);   /* products exact, one rounding */
             double t = (double)f32_from_bits(kto_ktanh_f32(bits_from_f32(cn), TE, Tr, Tb));
             c_next[r * hidden + j] = bits_from_f32(cn);
             h_next[r * hidden + j] = kto_bf16_encode_rne(o * t);

@@ -248,6 +248,12 @@ bool overlaps(const void *p, const void *q, size_t bytes) {
   return p != q && a < b + bytes && b < a + bytes;
 }
 
+// [p, p + pb) and [q, q + qb) share a byte (ranges of different sizes).
+bool spans_overlap(const void *p, size_t pb, const void *q, size_t qb) {
+  const uintptr_t a = (uintptr_t)p, b = (uintptr_t)q;
+  return pb != 0 && qb != 0 && a < b + qb && b < a + pb;
+}
+
 kt_status run_bwd(int op, int fmt, const void *a, const void *dy, void *dx, size_t n, kt_lut lut,
                   void *stream) {
   if (op < 0 || op > 3 || fmt < 0 || fmt > 1) return fail(KT_ERR_ARG, "bad op/dtype");
@@ -644,10 +650,10 @@ KT_API kt_status klstm_cell_bf16(const uint16_t *gates, const float *c_prev, flo
   if (!gates || !c_prev || !c_next || !h_next) return fail(KT_ERR_ARG, "NULL pointer");
   if ((uintptr_t)gates % 2 || (uintptr_t)h_next % 2 || (uintptr_t)c_prev % 4 || (uintptr_t)c_next % 4)
     return fail(KT_ERR_ARG, "misaligned pointer");
-  if (overlaps(c_next, c_prev, n * 4) || overlaps(h_next, gates, n * 8) ||
-      (const void *)h_next == (const void *)gates ||
-      ((uintptr_t)h_next < (uintptr_t)c_next + n * 4 && (uintptr_t)c_next < (uintptr_t)h_next + n * 2) ||
-      ((uintptr_t)c_next < (uintptr_t)gates + n * 8 && (uintptr_t)gates < (uintptr_t)c_next + n * 4))
+  // gates n*8 B, c_prev / c_next n*4 B, h_next n*2 B; only c_next == c_prev may alias
+  if (overlaps(c_next, c_prev, n * 4) || spans_overlap(c_next, n * 4, gates, n * 8) ||
+      spans_overlap(h_next, n * 2, gates, n * 8) || spans_overlap(h_next, n * 2, c_prev, n * 4) ||
+      spans_overlap(h_next, n * 2, c_next, n * 4))
     return fail(KT_ERR_ARG, "outputs overlap inputs (only c_next == c_prev is allowed)");
   kt::LaunchInfo li;
   kt_status s = launch_info(&li);
@@ -722,6 +728,7 @@ KT_API kt_status kgemm_lstm_cell_bf16(const uint16_t *A, const uint16_t *B, cons
     return fail(KT_ERR_ARG, "A, B must be 16-byte and c_prev, c_next, h_next 32-byte aligned");
   const size_t cb = M * hidden * 4, hb = M * hidden * 2;
   if (overlaps(c_next, c_prev, cb)) return fail(KT_ERR_ARG, "c_next overlaps c_prev without being equal");
+  if (spans_overlap(h_next, hb, c_next, cb)) return fail(KT_ERR_ARG, "h_next overlaps c_next");
   const void *ins[3] = {A, B, c_prev};
   const size_t inb[3] = {M * K * 2, 4 * hidden * K * 2, cb};
   for (int j = 0; j < 3; ++j) {

@@ -431,3 +431,28 @@ def test_c_demo_builds_and_runs_host_part(kt, tmp_path):
     out = subprocess.run([exe, "--no-gpu"], check=True, capture_output=True, text=True).stdout
     assert "Table 1, row 11000: E=126 r=0 b=65" in out
     assert "p = 23 table" in out and "KT_ERR_LUT" in out
+
+
+def test_lstm_cell_overlap_rule_exact(kt):
+    """klstm_cell_bf16 / kgemm_lstm_cell_bf16 reject exactly the overlapping
+    layouts: buffers of different sizes placed right next to each other (any
+    order) are accepted by the overlap check (found when an allocator put
+    h_next just below the gate block); real overlaps are rejected."""
+    lib = kt._lib
+    lut = kt.Lut.paper().handle
+    rows, H = 4, 16
+    n = rows * H
+    base = 1 << 40                                   # fake, never dereferenced: no GPU here
+    g, cp, cn = base, base + 8 * n, base + 12 * n     # gates | c_prev | c_next
+    def cell(h, c_next=cn):
+        st = lib.klstm_cell_bf16(ctypes.c_void_p(g), ctypes.c_void_p(cp), ctypes.c_void_p(c_next),
+                                 ctypes.c_void_p(h), rows, H, lut, None)
+        return st, lib.kt_last_error().decode()
+    for h in (g - 2 * n, cn + 4 * n, g - 2 * n - 64):  # adjacent below gates, after c_next, gap
+        st, err = cell(h)
+        assert "overlap" not in err, (hex(h), err)
+    for h in (g - 2 * n + 2, g + 8 * n - 2, cp + 2, cn + 4 * n - 2):
+        st, err = cell(h)
+        assert st == kt.KT_ERR_ARG and "overlap" in err, hex(h)
+    st, err = cell(cn + 4 * n, c_next=cp)            # in place c_next == c_prev is allowed
+    assert "overlap" not in err

@@ -546,3 +546,38 @@ def test_lstm_cell_output_gate_zero_and_bounds():
     h = O.bf16_to_f64(hn)
     assert np.all(np.abs(h) <= 1.0)
     assert np.all(np.abs(h - o * np.tanh(cnv)) <= 1.67e-2 + 2.0 ** -8)
+
+
+def _rn32_fraction(v):
+    """Round the exact rational v to the nearest binary32, ties to even (brute
+    force over the two neighbouring floats with exact arithmetic)."""
+    from fractions import Fraction
+    f = np.float32(float(v))                       # within one float of v
+    cands = {f, np.nextafter(f, np.float32(np.inf)), np.nextafter(f, np.float32(-np.inf))}
+    best = min(cands, key=lambda c: (abs(Fraction(float(c)) - v),
+                                     int(np.array([c], np.float32).view(np.uint32)[0]) & 1))
+    return float(best)
+
+
+def test_rn32_exact_sum_single_rounding():
+    """The oracle's RN32 of an exact sum of two doubles (R-DERIVED, R-LSTM-CELL):
+    equal to exact rational rounding, including sums whose binary64 value sits
+    exactly on a binary32 tie while the exact sum does not."""
+    from fractions import Fraction
+    rng = np.random.default_rng(31)
+    cases = []
+    for _ in range(3000):
+        a = float(rng.standard_normal()) * 2.0 ** int(rng.integers(-30, 30))
+        b = a * float(np.float32(rng.standard_normal() * 1e-3))
+        cases.append((a, b))
+    for base in (1.0, 1.5, 3.0, 0.75, 1e-3, 6.0e-39):
+        f = np.float32(base)
+        tie = (float(f) + float(np.nextafter(f, np.float32(np.inf)))) / 2
+        for tiny in (2.0 ** -80, -(2.0 ** -80), 2.0 ** -60 * base, -(2.0 ** -60) * base):
+            cases.append((tie, tiny * base if base < 1e-30 else tiny))
+    for a, b in cases:
+        want = _rn32_fraction(Fraction(a) + Fraction(b))
+        assert O.rn32_exact_sum(a, b) == want, (a, b)
+    # the double-rounding case a plain binary64 evaluation gets wrong
+    tie = (1.0 + float(np.nextafter(np.float32(1.0), np.float32(2.0)))) / 2
+    assert O.rn32_exact_sum(tie, 2.0 ** -80) > 1.0 and np.float32(tie + 2.0 ** -80) == np.float32(1.0)

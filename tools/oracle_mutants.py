@@ -48,7 +48,8 @@ MUTANTS = [
     ("optimizer: clip value", K, "else Mhat[j] = (1 << q) - 1;", "else Mhat[j] = (1 << q) - 2;"),
     ("optimizer: E cap", K, "int E = Ei[c] < 126 ? Ei[c] : 126;", "int E = Ei[c];"),
     ("bounds: b_max", K, "*bmax = (1 << p) - 1 - ", "*bmax = (1 << p) - "),
-    ("lstm cell sum", K, "float cn = (float)(f * c + i * g);", "float cn = (float)(f * c + i * o);"),
+    ("lstm cell sum", K, "float cn = rn32_exact_sum(f * c, i * g);", "float cn = rn32_exact_sum(f * c, i * o);"),
+    ("exact-sum tie break", K, "return ((e > 0.0) == ((double)g > (double)f)) ? g : f;", "return f;"),
     ("via-bf16 widening", K, "return (uint32_t)kto_ktanh_bf16(b, TE, Tr, Tb) << 16;",
      "return (uint32_t)kto_ktanh_bf16(b, TE, Tr, Tb) << 15;"),
     ("maclaurin recurrence", A, "t[k + 1] = ((k == 0 ? 1.0L : 0.0L) - conv)",
