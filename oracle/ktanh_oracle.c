@@ -13,7 +13,9 @@
  *
  * Precision: the K-TanH core is integer-only (as the paper defines it);
  * every floating-point step that is not a "decision" is done in IEEE
- * binary64.  The one decision made in floating point -- the argument
+ * binary64, and where binary64 is not exact (F32 x/2 (1+t), the LSTM cell's
+ * f c + i g) the exact sum of two exact binary64 products is rounded once
+ * (rn32_exact_sum).  The one decision made in floating point -- the argument
  * u = sqrt(2/pi)(x + a x^3) of the K-GELU, whose rounding picks the LUT
  * entry -- is taken in binary32 with the op order written in
  * gelu_arg_f32() below (reading R-GELU-ARG), because the CUDA
