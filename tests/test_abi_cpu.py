@@ -344,7 +344,8 @@ def test_lut_f32_rejected_by_bf16_calls(kt):
     """A p = 23 handle has no BF16 words: every BF16 call returns KT_ERR_LUT
     before touching the device; F32 calls accept it (n == 0: no launch)."""
     L, _ = O.build_lut_sp(3, 23)
-    h = kt.Lut.from_tables_f32(L.E, L.r, L.b).handle
+    F = kt.Lut.from_tables_f32(L.E, L.r, L.b)       # keep the object: it owns the handle
+    h = F.handle
     lib = kt._lib
     for name in kt.MAP_CALLS:
         want = kt.KT_ERR_LUT if ("bf16" in name) else kt.KT_OK
@@ -439,7 +440,8 @@ def test_lstm_cell_overlap_rule_exact(kt):
     order) are accepted by the overlap check (found when an allocator put
     h_next just below the gate block); real overlaps are rejected."""
     lib = kt._lib
-    lut = kt.Lut.paper().handle
+    P = kt.Lut.paper()                               # keep the object: it owns the handle
+    lut = P.handle
     rows, H = 4, 16
     n = rows * H
     base = 1 << 40                                   # fake, never dereferenced: no GPU here
@@ -456,3 +458,68 @@ def test_lstm_cell_overlap_rule_exact(kt):
         assert st == kt.KT_ERR_ARG and "overlap" in err, hex(h)
     st, err = cell(cn + 4 * n, c_next=cp)            # in place c_next == c_prev is allowed
     assert "overlap" not in err
+
+
+def _ov(p, pb, q, qb):
+    return pb > 0 and qb > 0 and p < q + qb and q < p + pb
+
+
+def _layout(rng, sizes, align):
+    """Random placement of buffers of the given byte sizes inside a small
+    window (so that overlaps, adjacency and aliasing are all frequent)."""
+    span = sum(sizes) * 2
+    base = 1 << 40
+    return [base + int(rng.integers(0, span // align)) * align for _ in sizes]
+
+
+@pytest.mark.parametrize("fn", ["cell", "gemm_cell", "dual", "bwd", "gemm"])
+def test_overlap_rules_random_layouts(kt, fn):
+    """Every multi-buffer entry point flags an overlap exactly when its rule
+    says so, over 3000 random layouts each (fake device addresses: the overlap
+    check runs before any device access, so this needs no GPU)."""
+    P = kt.Lut.paper()                               # keep the object: it owns the handle
+    lib, lut = kt._lib, P.handle
+    rng = np.random.default_rng(hash(fn) % 2**32)
+    vp = ctypes.c_void_p
+    for _ in range(3000):
+        if fn == "cell":
+            rows, H = 2, 16
+            n = rows * H
+            g, cp, cn, h = _layout(rng, [8 * n, 4 * n, 4 * n, 2 * n], 32)
+            if rng.random() < 0.2:
+                cn = cp
+            want = ((cn != cp and _ov(cn, 4 * n, cp, 4 * n)) or _ov(cn, 4 * n, g, 8 * n) or
+                    _ov(h, 2 * n, g, 8 * n) or _ov(h, 2 * n, cp, 4 * n) or _ov(h, 2 * n, cn, 4 * n))
+            lib.klstm_cell_bf16(vp(g), vp(cp), vp(cn), vp(h), rows, H, lut, None)
+        elif fn == "gemm_cell":
+            M, H, K = 128, 64, 64
+            a, b, cp, cn, h = _layout(rng, [M * K * 2, 4 * H * K * 2, M * H * 4, M * H * 4, M * H * 2], 32)
+            if rng.random() < 0.2:
+                cn = cp
+            cb, hb = M * H * 4, M * H * 2
+            want = ((cn != cp and _ov(cn, cb, cp, cb)) or _ov(h, hb, cn, cb) or
+                    any(_ov(h, hb, p, s) for p, s in ((a, M * K * 2), (b, 4 * H * K * 2), (cp, cb))) or
+                    any(_ov(cn, cb, p, s) for p, s in ((a, M * K * 2), (b, 4 * H * K * 2))))
+            lib.kgemm_lstm_cell_bf16(vp(a), vp(b), vp(cp), vp(cn), vp(h), M, H, K, lut, None)
+        elif fn == "dual":
+            n = 64
+            x, yg, ys = _layout(rng, [2 * n] * 3, 2)
+            if rng.random() < 0.2:
+                yg = x
+            want = (yg == ys or _ov(yg, 2 * n, ys, 2 * n) or (yg != x and _ov(x, 2 * n, yg, 2 * n)) or
+                    (ys != x and _ov(x, 2 * n, ys, 2 * n)))
+            lib.kgelu_swish_bf16(vp(x), vp(yg), vp(ys), n, lut, None)
+        elif fn == "bwd":
+            n = 64
+            a, dy, dx = _layout(rng, [2 * n] * 3, 2)
+            if rng.random() < 0.2:
+                dx = a if rng.random() < 0.5 else dy
+            want = (dx != a and _ov(dx, 2 * n, a, 2 * n)) or (dx != dy and _ov(dx, 2 * n, dy, 2 * n))
+            lib.kgelu_bwd_bf16(vp(a), vp(dy), vp(dx), n, lut, None)
+        else:
+            M, N, K = 128, 256, 64
+            a, b, c = _layout(rng, [M * K * 2, N * K * 2, M * N * 2], 32)
+            want = _ov(c, M * N * 2, a, M * K * 2) or _ov(c, M * N * 2, b, N * K * 2)
+            lib.kgemm_bf16(vp(a), vp(b), vp(c), M, N, K, -1, None, None)
+        got = "overlap" in lib.kt_last_error().decode()
+        assert got == want, (fn, _)
