@@ -523,3 +523,49 @@ def test_overlap_rules_random_layouts(kt, fn):
             lib.kgemm_bf16(vp(a), vp(b), vp(c), M, N, K, -1, None, None)
         got = "overlap" in lib.kt_last_error().decode()
         assert got == want, (fn, _)
+
+
+def _lut_f32_ok(E, r, b):
+    """The kt_lut_create_f32 rule written out (include/ktanh.h): r in [0, 23],
+    E in [1, 127], every reachable M_o = (M23 >> r) + b in [0, 2^23), and
+    E == 127 only with M_o == 0.  Reachable M23 of interval t: [2^20 v,
+    2^20 (v + 1)), except t = 7 (E = 128), where only x = 3.75 (M23 = 7 2^20)
+    is <= T2."""
+    for t in range(32):
+        if not (0 <= r[t] <= 23 and 1 <= E[t] <= 127):
+            return False
+        v = t & 7
+        lo = v << 20
+        hi = lo if t == 7 else ((v + 1) << 20) - 1
+        mlo, mhi = (lo >> r[t]) + b[t], (hi >> r[t]) + b[t]
+        if mlo < 0 or mhi > (1 << 23) - 1 or (E[t] == 127 and mhi != 0):
+            return False
+    return True
+
+
+@settings(max_examples=300, deadline=None)
+@given(data=st.data())
+def test_lut_f32_validation_matches_the_rule(kt, data):
+    """Random tables near the p = 23 optimizer table: kt_lut_create_f32 accepts
+    exactly those the documented rule accepts."""
+    L, _ = O.build_lut_sp(3, 23)
+    E, r, b = [int(v) for v in L.E], [int(v) for v in L.r], [int(v) for v in L.b]
+    for _ in range(data.draw(st.integers(1, 4))):
+        t = data.draw(st.integers(0, 31))
+        which = data.draw(st.sampled_from(["E", "r", "b"]))
+        if which == "E":
+            E[t] = data.draw(st.sampled_from([0, 1, 100, 125, 126, 127, 128]))
+        elif which == "r":
+            r[t] = data.draw(st.integers(-1, 24))
+        else:
+            rr = min(max(r[t], 0), 23)
+            lo, hi = O.bounds_sp(rr, t & 7, 3, 23)
+            b[t] = data.draw(st.sampled_from([lo - 1, lo, hi, hi + 1, (lo + hi) // 2, b[t] + 1, b[t] - 1]))
+    ok = _lut_f32_ok(E, r, b)
+    try:
+        kt.Lut.from_tables_f32(E, r, b)
+        accepted = True
+    except kt.KTanhError as e:
+        assert e.status == kt.KT_ERR_LUT
+        accepted = False
+    assert accepted == ok, (E, r, b)
