@@ -434,9 +434,10 @@ HEADS = {"c1": ("c1_exhaustive_bf16", "ktanh_bf16", "tanh"), "c2": ("c2_bf16_2p2
          "c3": ("c3_f32_2p28", "ktanh_f32", "tanh"), "c4": ("c4_lstm_gates", "lstm", "lstm"),
          "c5": ("c5_ffn_2p30", "kgelu_bf16", "gelu")}
 
-KERNEL_NAME = {"ktanh_bf16": "k_map<0, 0, true>", "ktanh_f32": "k_map<0, 1, true>",
-               "kgelu_bf16": "k_map<3, 0, true>", "kswish_bf16": "k_map<2, 0, true>",
-               "lstm": "k_lstm<true>"}
+# demangled names as ncu lists them (profiles/launches_r01.csv): <OP, FMT, NC, PF>
+KERNEL_NAME = {"ktanh_bf16": "kt::k_map<0, 0, 1, 1>", "ktanh_f32": "kt::k_map<0, 1, 1, 1>",
+               "kgelu_bf16": "kt::k_map<3, 0, 1, 1>", "kswish_bf16": "kt::k_map<2, 0, 1, 1>",
+               "lstm": "kt::k_lstm<1>"}
 
 EXTRA = [("c2_bf16_2p24", "ktanh64_bf16"), ("c3_f32_2p28", "ktanh_f32"), ("c3_f32_2p28", "ktanh_f32:p23"),
          ("c3_f32_2p28", "ktanh_f32_via_bf16"), ("c4_lstm_gates", "lstm"),
