@@ -24,6 +24,14 @@ def ktanh_all(lut=None):
     return O.map_bf16("tanh", W, lut)
 
 
+def _survey_exact_rows(key):
+    return [row[1:] for row in read_golden("survey_exact.txt") if row[0] == key]
+
+
+def _survey_exact():
+    return {row[0]: row[1:] for row in read_golden("survey_exact.txt")}
+
+
 # --------------------------------------------------------------------------
 # Table 1 / thresholds as printed
 # --------------------------------------------------------------------------
@@ -126,8 +134,11 @@ def test_error_bound_table2():
     s = O.error_sweep()
     assert s["max_abs"] <= g["max_err_e-2"] * 1e-2
     assert s["max_rel"] <= g["rel_err_pct"] / 100
-    # tighter than the printed bound (Table 1 is better than the printed row)
-    assert s["max_abs"] < 0.009
+    # tighter than the printed bound (Table 1 is better than the printed row):
+    # the exact maximum and its argument computed by SURVEY.md (reading A11)
+    ex = _survey_exact()
+    assert s["max_abs"] == pytest.approx(float(ex["max_abs_table1"][0]), rel=1e-12, abs=0)
+    assert s["argmax_abs"] == int(ex["argmax_abs_table1"][0], 16)
 
 
 def test_value_domain_reconstruction(golden_table1):
@@ -162,6 +173,20 @@ def test_monotone_piecewise_and_bounded_drops():
     assert np.all(d[same] >= 0)
     assert np.all(d[~same] >= -2 * 0.0167)
     # negative side mirrors by odd symmetry (checked above)
+
+
+def test_monotone_exception_list_exact():
+    """Reading A10, exact: with Table 1 the ONLY decreases of K-TanH over the
+    positive BF16 inputs (in increasing order) are the six interval-boundary
+    drops SURVEY.md Sec. 8(c) computed, each of the stated size in output ulps
+    (tests/golden/survey_exact.txt); every other step is non-decreasing."""
+    pos = np.arange(0x0000, 0x7F81)
+    yb = ktanh_all()[pos].astype(np.int64)    # positive outputs: bit order == value order
+    d = np.diff(yb)
+    idx = np.nonzero(d < 0)[0]
+    got = [(int(pos[i + 1]), int(-d[i])) for i in idx]
+    want = [(int(a, 16), int(b)) for a, b in _survey_exact_rows("drop")]
+    assert got == want
 
 
 # --------------------------------------------------------------------------
@@ -221,6 +246,11 @@ def test_ablation_reproduces_table2_printed_accuracy():
     s = O.error_sweep(A)
     assert round(s["max_abs"] * 100, 2) == g["max_err_e-2"]
     assert round(s["max_rel"] * 100, 2) == g["rel_err_pct"]
+    # the exact values behind the printed digits
+    ex = _survey_exact()
+    assert s["max_abs"] == pytest.approx(float(ex["max_abs_ablation"][0]), rel=1e-12, abs=0)
+    assert round(s["max_rel"] * 100, 4) == float(ex["max_rel_ablation_pct"][0])
+    assert s["argmax_abs"] == s["argmax_rel"] == int(ex["argmax_rel_ablation"][0], 16)
     # and the ablated table is worse than the optimized one
     assert s["max_abs"] > O.error_sweep(O.build_lut(False)[0])["max_abs"]
 
