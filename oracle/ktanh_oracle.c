@@ -13,9 +13,10 @@
  *
  * Precision: the K-TanH core is integer-only (as the paper defines it);
  * every floating-point step that is not a "decision" is done in IEEE
- * binary64, and where binary64 is not exact (F32 x/2 (1+t), the LSTM cell's
+ * binary64, and where binary64 is not exact (x/2 (1+t) in both formats --
+ * for a subnormal BF16 x the two terms are 2^133 apart -- and the LSTM cell's
  * f c + i g) the exact sum of two exact binary64 products is rounded once
- * (rn32_exact_sum).  The one decision made in floating point -- the argument
+ * (rn32_exact_sum, rnbf16_exact_sum).  The one decision made in floating point -- the argument
  * u = sqrt(2/pi)(x + a x^3) of the K-GELU, whose rounding picks the LUT
  * entry -- is taken in binary32 with the op order written in
  * gelu_arg_f32() below (reading R-GELU-ARG), because the CUDA
@@ -31,7 +32,9 @@
  *   kto_ktanh_f32 ............................. pinned (BF16 closed-form relation,
  *                                               error bound, invariants)
  *   kto_ksigmoid_* ............................ pinned (exact rational (1+t)/2)
- *   kto_kswish_* / kto_kgelu_* ................ pinned (special cases + error bound)
+ *   kto_kswish_* / kto_kgelu_* ................ pinned (BF16: exact rational single
+ *                                               rounding over all 65,536 patterns;
+ *                                               special cases + error bound)
  *   kto_bwd_* (reading R-BWD) ................. pinned (closed forms at 0, in the
  *                                               bypass/saturation regions, and
  *                                               error bounds vs the true derivative)
@@ -261,8 +264,8 @@ uint32_t kto_ktanh_f32_via_bf16(uint32_t x, const int *TE, const int *Tr, const 
 /*   Swish(x)   = x * Sigmoid(x)                                          */
 /*   GELU(x)   ~= x/2 (1 + TanH(sqrt(2/pi)(x + a x^3))),  a = 0.044715    */
 /* The TanH is K-TanH on the format's own bits: its argument is rounded   */
-/* (RNE) to the format first; the outer affine step is done in binary64   */
-/* and rounded once to the format.                                        */
+/* (RNE) to the format first; the outer affine step is exact and rounded  */
+/* once to the format (R-DERIVED).                                        */
 /* ------------------------------------------------------------------ */
 
 /* GELU argument, decision precision binary32 (reading R-GELU-ARG):       */
@@ -292,6 +295,28 @@ static float rn32_exact_sum(double a, double b)
 }
 
 float kto_rn32_exact_sum(double a, double b) { return rn32_exact_sum(a, b); }   /* for the pins */
+
+/* RN_bf16 of the EXACT sum a + b of two doubles (reading R-DERIVED for the
+ * BF16 K-Swish / K-GELU outer step x/2 + (x/2) t).  For a subnormal x the two
+ * terms are ~2^133 apart, so RN64(a + b) drops b; when a itself is a BF16
+ * tie (x/2 with x odd in the last subnormal place) b decides the side.  Same
+ * TwoSum construction as rn32_exact_sum: RN_bf16(s) is the answer unless s is
+ * exactly a BF16 midpoint and the error e of s is non-zero. */
+static uint16_t rnbf16_exact_sum(double a, double b)
+{
+    double s = a + b;
+    uint16_t f = kto_bf16_encode_rne(s);
+    if (!isfinite(s) || !isfinite(a) || !isfinite(b)) return f;
+    double bb = s - a;
+    double e = (a - (s - bb)) + (b - bb);
+    double fv = kto_bf16_decode(f);
+    if (e == 0.0 || fv == s || isinf(fv)) return f;
+    uint16_t sg = f & 0x8000, mag = f & 0x7FFF;
+    uint16_t g = sg | (uint16_t)(fabs(s) > fabs(fv) ? mag + 1 : mag - 1);   /* neighbour on s's side */
+    double gv = kto_bf16_decode(g);
+    if (s != (fv + gv) / 2.0) return f;                   /* not a midpoint: s rounds as the sum */
+    return ((e > 0.0) == (gv > fv)) ? g : f;              /* midpoint: the exact sum lies on e's side */
+}
 
 static float gelu_arg_f32(float x)
 {
@@ -339,7 +364,8 @@ uint16_t kto_kswish_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb
     uint16_t h = kto_bf16_encode_rne(xv / 2.0);
     uint16_t t = kto_ktanh_bf16(h, TE, Tr, Tb);
     double tv = kto_bf16_decode(t);
-    return kto_bf16_encode_rne(xv * (1.0 + tv) / 2.0);   /* x * Sigmoid(x) */
+    const double hx = xv / 2.0;                           /* exact */
+    return rnbf16_exact_sum(hx, hx * tv);                 /* RN_bf16(x (1+t)/2), product exact */
 }
 
 static uint32_t kswish_f32_pb(uint32_t x, const int *TE, const int *Tr, const int *Tb, int pb)
@@ -364,7 +390,8 @@ uint16_t kto_kgelu_bf16(uint16_t x, const int *TE, const int *Tr, const int *Tb)
     uint16_t ub = kto_bf16_encode_rne((double)u);        /* argument in BF16 */
     uint16_t t = kto_ktanh_bf16(ub, TE, Tr, Tb);
     double tv = kto_bf16_decode(t);
-    return kto_bf16_encode_rne(xv / 2.0 * (1.0 + tv));
+    const double hx = xv / 2.0;                           /* exact */
+    return rnbf16_exact_sum(hx, hx * tv);                 /* RN_bf16(x/2 (1+t)), product exact */
 }
 
 static uint32_t kgelu_f32_pb(uint32_t x, const int *TE, const int *Tr, const int *Tb, int pb)

@@ -342,6 +342,93 @@ def test_ksigmoid_exact_rational():
         assert ys[w] == want, hex(w)
 
 
+def _rn_frac(q: Fraction, p: int, emin: int = -126, emax: int = 127):
+    """Exact round-to-nearest-even of the rational q to a binary format with p
+    significand bits (hidden bit included) and exponent range [emin, emax]:
+    integer arithmetic on the rational, no floating point.  Returns a Fraction,
+    or +-inf (float) on overflow."""
+    if q == 0:
+        return Fraction(0)
+    a = abs(q)
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1
+    quantum = Fraction(2) ** (max(e, emin) - (p - 1))
+    r = round(a / quantum) * quantum          # Fraction.__round__: half to even
+    if r >= Fraction(2) ** (emax + 1):
+        return math.copysign(math.inf, q)
+    return r if q > 0 else -r
+
+
+def _bf16_bits(v) -> int:
+    """Bits of a value already representable in BF16 (or +-inf)."""
+    return O.bf16_encode_rne(float(v))
+
+
+def _outer_exact(w: int, t_bits: int) -> Fraction:
+    """The exact rational x/2 (1 + t) of K-Swish / K-GELU."""
+    return _frac_bf16(w) / 2 * (1 + _frac_bf16(t_bits))
+
+
+def _check_exact_outer(y, t_bits_of):
+    """y[w] == RN_bf16(x/2 (1 + t)) rounded ONCE from the exact rational, for
+    every finite BF16 x; a zero result is compared as a value (reading A21)."""
+    bad = []
+    for w in range(65536):
+        if not FINITE[w]:
+            continue
+        want = _rn_frac(_outer_exact(w, t_bits_of(w)), 8)
+        if want == 0:
+            ok = O.bf16_decode(int(y[w])) == 0.0
+        else:
+            ok = int(y[w]) == _bf16_bits(want)
+        if not ok:
+            bad.append(hex(w))
+    assert not bad, (len(bad), bad[:8])
+
+
+def test_kswish_exact_rational():
+    """K-Swish (reading R-DERIVED): y = RN_bf16(x/2 (1 + t)),
+    t = K-TanH(RN_bf16(x/2)), with the outer step rounded once from the exact
+    rational -- over all finite BF16 patterns, including the subnormal x whose
+    x/2 is a BF16 tie (there the exact t-term decides the rounding)."""
+    y = O.map_bf16("swish", W)
+    h = np.array([_bf16_bits(_rn_frac(_frac_bf16(w) / 2, 8)) if FINITE[w] else 0
+                  for w in range(65536)], np.uint16)
+    t = O.map_bf16("tanh", h)
+    _check_exact_outer(y, lambda w: int(t[w]))
+
+
+def _gelu_u_bits(w: int, c0: Fraction, c1: Fraction) -> int:
+    """RN_bf16 of the GELU argument u = x fma(C1, x^2, C0), each binary32 step
+    rounded once from its exact rational value (reading R-GELU-ARG)."""
+    x = _frac_bf16(w)
+    if x == 0:
+        return int(W[w])
+    x2 = _rn_frac(x * x, 24)
+    if isinstance(x2, float):                   # x^2 overflows binary32
+        return 0xFF80 if x < 0 else 0x7F80
+    pp = _rn_frac(c1 * x2 + c0, 24)
+    u = _rn_frac(x * pp, 24)
+    if isinstance(u, float):
+        return 0xFF80 if u < 0 else 0x7F80
+    return _bf16_bits(_rn_frac(u, 8))
+
+
+def test_kgelu_exact_rational():
+    """K-GELU (readings R-GELU-ARG / R-DERIVED): y =
+    RN_bf16(x/2 (1 + t)), t = K-TanH(RN_bf16(u)), u in binary32 per
+    R-GELU-ARG (each step re-derived here from exact rationals), the outer
+    step rounded once from the exact rational, over all finite BF16 x."""
+    a = float(read_golden("gelu_a.txt")[0][1])
+    c0 = Fraction(float(np.float32(math.sqrt(2 / math.pi))))
+    c1 = Fraction(float(np.float32(math.sqrt(2 / math.pi) * a)))
+    y = O.map_bf16("gelu", W)
+    ub = np.array([_gelu_u_bits(w, c0, c1) if FINITE[w] else 0 for w in range(65536)], np.uint16)
+    t = O.map_bf16("tanh", ub)
+    _check_exact_outer(y, lambda w: int(t[w]))
+
+
 def test_ksigmoid_special_values_and_bound():
     ys = O.map_bf16("sigmoid", W)
     assert ys[0x0000] == 0x3F00 and ys[0x8000] == 0x3F00       # sigmoid(0) = 1/2

@@ -35,8 +35,12 @@ MUTANTS = [
      "return kto_bf16_encode_rne((1.0 - tv) / 2.0);"),
     ("sigmoid argument", K, "uint16_t h = kto_bf16_encode_rne(xv / 2.0);          /* x/2 in BF16 */",
      "uint16_t h = kto_bf16_encode_rne(xv / 4.0);"),
-    ("swish factor", K, "return kto_bf16_encode_rne(xv * (1.0 + tv) / 2.0);",
-     "return kto_bf16_encode_rne(xv * (1.0 + tv) / 4.0);"),
+    ("swish factor", K, "return rnbf16_exact_sum(hx, hx * tv);                 /* RN_bf16(x (1+t)/2), product exact */",
+     "return rnbf16_exact_sum(hx, hx * tv / 2.0);"),
+    ("gelu outer: binary64 double rounding", K,
+     "return rnbf16_exact_sum(hx, hx * tv);                 /* RN_bf16(x/2 (1+t)), product exact */",
+     "return kto_bf16_encode_rne(xv / 2.0 * (1.0 + tv));"),
+    ("bf16 exact-sum tie break", K, "return ((e > 0.0) == (gv > fv)) ? g : f;", "return f;"),
     ("gelu constant a", K, "static const double GELU_A = 0.044715;", "static const double GELU_A = 0.04715;"),
     ("gelu cubic term", K, "float p = fmaf(C1, x2, C0);", "float p = fmaf(C1, x, C0);"),
     ("bwd tanh", K, "case 0: return 1.0 - a * a;", "case 0: return 1.0 - a;"),
