@@ -6,22 +6,35 @@
         --master-addr 127.0.0.1 --master-port P bench.py --gpus N ...
 
 Metric (BASELINE.json): "K-TanH Gelem/s and achieved HBM GB/s vs ~8 TB/s
-peak at 1/2/4/8 B200".  The headline workload is BASELINE.json configs[1]:
-BF16 K-TanH over a flat 2^24-element tensor ~ N(0, 2^2), one library call
-(= one kernel) per step.  Every rank processes its own independent tensor
-(seed + rank, weak scaling, no collective on the data path); `value` is the
-elements of all ranks / the max over ranks of the timed region.
+peak at 1/2/4/8 B200".  The headline workload is the one the metric is
+quoted on at 1/2/4/8 GPUs, BASELINE.json configs[4]: K-GELU
+over a [65536, 16384] BF16 tensor ~ N(0, 1) per GPU (2^30 elements), one
+library call (= one kernel) per step.  Every rank processes its own
+independent tensor (seed + rank, weak scaling, no collective on the data
+path); `value` is the elements of all ranks / the max over ranks of the
+timed region.  configs 2-4, K-Swish and the fused K-GELU+K-Swish pass are
+`extra` lines (`--config` picks another headline).
 
 Timing: W warm-up steps, then windows of exactly K steps, each bracketed by
 a barrier and cuda synchronize, timed with CUDA events on the launching
 stream; the K launches of a window are replayed from a CUDA graph (the
 library calls are capturable).  Inputs smaller than L2 rotate through
-buffer sets totalling > 4x L2 so every step reads cold HBM.  nvidia-smi
-clocks are sampled during the timed windows.  Reported: the median window.
+buffer sets totalling > 4x L2 so every step reads cold HBM (config 5's
+4 GiB per step is larger than L2 by itself).  nvidia-smi clocks are sampled
+during the timed windows.  Reported: the median window.
 
 `--impl reference` times the CPU oracle (oracle/, the scalar C
 implementation of the paper's algorithm) on the host cores on a bounded
-sample of the same workload; under torchrun only rank 0 runs it.
+sample of the same workload; under torchrun only rank 0 runs it.  The only
+other use of oracle/ is the main arm's cpu_baseline leg: the oracle timed on
+a sample of the headline input, plus every rank's sampled check of its own
+GPU outputs against the oracle (outside the timed region).
+
+`--stub` (test hook, CPU only): the same multi-rank driver -- device
+selection, barriers, per-rank timing, max-over-ranks aggregation, the
+per-rank check and the JSON line -- around a trivial host copy instead of the
+library, so tests/test_bench_contract.py can run the N > 1 path under
+torchrun with gloo on a machine without a GPU.  Its numbers mean nothing.
 """
 from __future__ import annotations
 
@@ -237,7 +250,7 @@ def time_windows(step: Step, K: int, W: int, world: int, device, clocks: ClockSa
     nwin = int(max(3, min(max_windows, math.ceil(min_total_s / max(est, 1e-6)))))
     nwin = int(max_over_ranks(nwin, world, device))
     mark0 = clocks.mark() if clocks else 0
-    times = []
+    times, own = [], []
     for _ in range(nwin):
         barrier(world)
         torch.cuda.synchronize(device)
@@ -250,7 +263,9 @@ def time_windows(step: Step, K: int, W: int, world: int, device, clocks: ClockSa
         torch.cuda.synchronize(device)
         barrier(world)
         ms = e0.elapsed_time(e1)
+        own.append(ms)
         times.append(max_over_ranks(ms, world, device))
+    step.own = own                           # this rank's windows (before the max)
     time.sleep(0.12)
     clk = clocks.summary(mark0, None) if clocks else None
     del g
@@ -378,54 +393,38 @@ def _cpu_model():
     return "unknown"
 
 
-def load_range_traffic():
-    """Steady-state DRAM bytes per config-2 launch from the committed ncu
-    range-replay capture (profiles/ncu_range_traffic_rNN.csv: dram bytes over
-    a range of back-to-back launches, so the write-back of earlier launches'
-    dirty lines is counted)."""
+def load_traffic(key, op):
+    """Steady-state DRAM bytes (read + write) per launch of the headline kernel
+    from the newest committed ncu range-replay capture of THIS workload and
+    call (profiles/ncu_range_traffic_<workload>_<op>_rNN.csv, written by
+    tools/range_traffic.py: dram bytes over a range of back-to-back launches,
+    so the write-back of earlier launches' dirty lines is counted)."""
     import csv
     pdir = os.path.join(ROOT, "profiles")
     if not os.path.isdir(pdir):
         return None, None
+    prefix = f"ncu_range_traffic_{key}_{op}_r"
     for name in sorted(os.listdir(pdir), reverse=True):
-        if not (name.startswith("ncu_range_traffic_") and name.endswith(".csv")):
+        if not (name.startswith(prefix) and name.endswith(".csv")):
             continue
         try:
-            lines = [l for l in open(os.path.join(pdir, name)) if not l.startswith("#")]
-            launches = 64
-            for l in open(os.path.join(pdir, name)):
-                if "range of" in l or "tools/range_traffic.py" in l:
-                    for tok in l.split():
-                        if tok.isdigit():
-                            launches = int(tok)
-                            break
+            text = open(os.path.join(pdir, name)).read().splitlines()
+            launches = None
+            for l in text:
+                if "range of" in l:
+                    toks = l.split("range of", 1)[1].split()
+                    if toks and toks[0].isdigit():
+                        launches = int(toks[0])
+                        break
+            rows = [l for l in text if l.startswith('"')]
             tot = 0.0
-            for row in csv.DictReader(lines):
+            for row in csv.DictReader(rows):
                 if row.get("Metric Name") in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                    tot += float(row["Metric Value"])
-            if tot > 0:
+                    tot += float(row["Metric Value"].replace(",", ""))
+            if tot > 0 and launches:
                 return tot / launches, f"profiles/{name} (ncu range replay, {launches} launches)"
         except Exception:
             continue
-    return None, None
-
-
-def load_traffic(tag_substr):
-    """dram bytes per launch of the dominant kernel from the newest committed
-    ncu --set full summary (profiles/ncu_full_rNN.json), if any."""
-    pdir = os.path.join(ROOT, "profiles")
-    if not os.path.isdir(pdir):
-        return None, None
-    for name in sorted(os.listdir(pdir), reverse=True):
-        if not (name.startswith("ncu_full_") and name.endswith(".json")):
-            continue
-        try:
-            d = json.load(open(os.path.join(pdir, name)))
-        except Exception:
-            continue
-        for tag, ks in d.items():
-            if tag_substr in tag and ks and ks[0].get("dram_bytes_per_launch"):
-                return float(ks[0]["dram_bytes_per_launch"]), f"profiles/{name}:{tag}"
     return None, None
 
 
@@ -433,28 +432,37 @@ def load_traffic(tag_substr):
 HEADS = {"c1": ("c1_exhaustive_bf16", "ktanh_bf16", "tanh"), "c2": ("c2_bf16_2p24", "ktanh_bf16", "tanh"),
          "c3": ("c3_f32_2p28", "ktanh_f32", "tanh"), "c4": ("c4_lstm_gates", "lstm", "lstm"),
          "c5": ("c5_ffn_2p30", "kgelu_bf16", "gelu")}
+DTYPE_NAME = {torch.bfloat16: "bf16", torch.float32: "f32"}
 
-# demangled names as ncu lists them (profiles/launches_r01.csv): <OP, FMT, NC, PF>
+# demangled names as ncu lists them (profiles/launches_r02.csv): <OP, FMT, NC, PF>
 KERNEL_NAME = {"ktanh_bf16": "kt::k_map<0, 0, 1, 1>", "ktanh_f32": "kt::k_map<0, 1, 1, 1>",
                "kgelu_bf16": "kt::k_map<3, 0, 1, 1>", "kswish_bf16": "kt::k_map<2, 0, 1, 1>",
                "lstm": "kt::k_lstm<1>"}
 
-EXTRA = [("c2_bf16_2p24", "ktanh64_bf16"), ("c3_f32_2p28", "ktanh_f32"), ("c3_f32_2p28", "ktanh_f32:p23"),
-         ("c3_f32_2p28", "ktanh_f32_via_bf16"), ("c4_lstm_gates", "lstm"),
-         ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16"),
+EXTRA = [("c2_bf16_2p24", "ktanh_bf16"), ("c2_bf16_2p24", "ktanh64_bf16"), ("c3_f32_2p28", "ktanh_f32"),
+         ("c3_f32_2p28", "ktanh_f32:p23"), ("c3_f32_2p28", "ktanh_f32_via_bf16"),
+         ("c4_lstm_gates", "lstm"), ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16"),
          ("c5_ffn_2p30", "kgelu_swish_bf16"), ("c5_ffn_2p30", "kgelu_bwd_bf16"),
          ("c4_lstm_gates", "lstm_cell")]
+
+
+def head_config(key, call, world):
+    """The `config` object of the headline line; the reference arm prints the
+    identical object (same workload, same per-GPU size, same call)."""
+    cfg = WL.CONFIGS[key]
+    return {"workload": key, "desc": cfg.desc, "elements_per_gpu": cfg.numel, "call": call,
+            "parallelism": f"{world} independent shard(s) (seed + rank), no collective"}
 
 
 def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
         return 0
-    key, _, op = HEADS[args.config]
+    key, call, op = HEADS[args.config]
     cfg = WL.CONFIGS[key]
     import oracle as O
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    x = WL.make_input(cfg, device=dev)
+    x = WL.make_input(cfg, device=dev, numel=None if cfg.numel <= 1 << 24 else 1 << 24)
     m = min(x.numel(), 1 << 22)                   # bounded sample per step
     if op == "lstm":
         m -= m % (4 * WL.LSTM_HIDDEN)             # whole gate rows
@@ -475,18 +483,18 @@ def run_reference(args):
         ts.append(time.perf_counter() - t0)
     sec = sum(ts) / len(ts)
     val = m / sec / 1e9
+    sample = (f"each step: the scalar C oracle (oracle/ktanh_oracle.c, single-threaded) on {m} "
+              f"elements of the {key} workload (a prefix of a tensor drawn with the GPU arm's "
+              f"generator, seed and distribution), {args.steps} timed steps")
     out = {
         "impl": "reference",
         "metric": "K-TanH Gelem/s and achieved HBM GB/s vs ~8 TB/s peak at 1/2/4/8 B200",
         "value": round(val, 6), "unit": "Gelem/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
-        "dtype": "u16" if cfg.dtype == torch.bfloat16 else "u32", "data": "synthetic",
-        "config": {"workload": cfg.key, "desc": cfg.desc, "elements_per_step": m,
-                   "note": f"each step = a bounded sample (first {m} elements) of the workload"},
+        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_NAME[cfg.dtype], "data": "synthetic",
+        "config": head_config(key, call, world),
         "cpu_baseline": {"value": round(val, 6), "unit": "Gelem/s", "cores": 1, "kind": "oracle",
-                         "sample": f"first {m} elements of {cfg.key}, {args.steps} timed steps",
-                         "host_cpu": _cpu_model()},
+                         "sample": sample, "host_cpu": _cpu_model()},
         "e2e": {"value": round(val, 6), "unit": "Gelem/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -558,7 +566,8 @@ def table2_b200(kt, K, W, world, device, rank, peak):
     import numpy as np
     xall = WL.make_input("c1_exhaustive_bf16", device=device)
     xb = xall.view(torch.int16).cpu().numpy().view(np.uint16)
-    xv = (xb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    with np.errstate(invalid="ignore"):          # NaN patterns widen to NaN (no warning)
+        xv = (xb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
     fin = np.isfinite(xv)
     ref = np.tanh(xv)
     g = torch.Generator().manual_seed(2)
@@ -581,7 +590,8 @@ def table2_b200(kt, K, W, world, device, rank, peak):
             cyc, _ = kt.alu_probe("bf16", sample, apx=A)
             st = Step(kt, "c2_bf16_2p24", op, device, rank)
         yb = y.view(torch.int16).cpu().numpy().view(np.uint16)
-        yv = (yb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        with np.errstate(invalid="ignore"):
+            yv = (yb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
         err = np.abs(yv[fin] - ref[fin])
         nz = fin & (xv != 0)
         rel = np.abs(yv[nz] - ref[nz]) / np.abs(ref[nz])
@@ -605,7 +615,8 @@ def table2_b200(kt, K, W, world, device, rank, peak):
                           lambda t: torch.nn.functional.gelu(t, approximate="tanh")),
                          ("torch_gelu_erf", "torch:gelu_erf", lambda t: torch.nn.functional.gelu(t))):
         yb = fn(xall).view(torch.int16).cpu().numpy().view(np.uint16)
-        yv = (yb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        with np.errstate(invalid="ignore"):
+            yv = (yb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
         ok = fin & np.isfinite(ref_g)
         err = np.abs(yv[ok] - ref_g[ok])
         st = Step(kt, "c2_bf16_2p24", op, device, rank)
@@ -624,162 +635,193 @@ def table2_b200(kt, K, W, world, device, rank, peak):
             "rows": rows, "gelu_rows": grows}
 
 
+class StubStep:
+    """--stub test hook: a host copy standing in for the library call."""
+
+    def __init__(self, n=1 << 16, rank=0):
+        g = torch.Generator().manual_seed(5 + rank)
+        self.xs = [torch.randn(n, generator=g).to(torch.bfloat16)]
+        self.ys = [torch.empty_like(self.xs[0])]
+        self.n, self.sets, self.bytes_per_step = n, 1, 4 * n
+        self.cell = self.dual = self.bwd = False
+
+    def run(self, i):
+        self.ys[0].copy_(self.xs[0])
+
+
+def time_windows_stub(step, K, W, world, nwin=3):
+    """The multi-rank window protocol of time_windows with a host timer."""
+    for i in range(W):
+        step.run(i)
+    times, own = [], []
+    for _ in range(nwin):
+        barrier(world)
+        t0 = time.perf_counter()
+        for i in range(K):
+            step.run(W + i)
+        ms = (time.perf_counter() - t0) * 1e3
+        barrier(world)
+        own.append(ms)
+        times.append(max_over_ranks(ms, world, torch.device("cpu")))
+    step.own = own
+    return times, {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["stub"], "samples": 0}, 1.0
+
+
+def oracle_check(x, y, op, m=1 << 16, seed=0, stub=False):
+    """Part of the cpu_baseline leg, run by EVERY rank after its timed region:
+    m seeded sample positions (plus the first and last element) of this rank's
+    output y against the oracle on the same input bytes.  Bit-exact, NaN by
+    class, +-0 by value for the derived ops (DESIGN.md R-DERIVED / A21)."""
+    n = x.numel()
+    idx = np.random.default_rng(seed).integers(0, n, m, dtype=np.int64)
+    idx = np.concatenate([idx, [0, n - 1]])
+    it = torch.from_numpy(idx).to(x.device)
+    bf16 = x.dtype == torch.bfloat16
+    iv = torch.int16 if bf16 else torch.int32
+    nv = np.uint16 if bf16 else np.uint32
+    xs = x.reshape(-1)[it].view(iv).cpu().numpy().view(nv)
+    ys = y.reshape(-1)[it].view(iv).cpu().numpy().view(nv)
+    if stub:
+        want = xs                                   # the stub step is a copy
+    else:
+        import oracle as O
+        want = O.map_bf16(op, xs) if bf16 else O.map_f32(op, xs)
+    bits = 16 if bf16 else 32
+    mag = (1 << (bits - 1)) - 1
+
+    def isnan(w):
+        return (w.astype(np.int64) & mag) > (0x7F80 if bf16 else 0x7F800000)
+    def iszero(w):
+        return (w.astype(np.int64) & mag) == 0
+
+    bad = ys != want
+    if op != "tanh":
+        bad &= ~(isnan(ys) & isnan(want))
+    if op in ("swish", "gelu"):
+        bad &= ~(iszero(ys) & iszero(want))
+    return int(bad.sum()), int(idx.size)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ktanh", choices=["ktanh", "reference"])
-    ap.add_argument("--no-extra", action="store_true", help="skip configs 3-5 side measurements")
+    ap.add_argument("--no-extra", action="store_true", help="skip the side measurements (extra)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--config", default="c2", choices=sorted(HEADS),
-                    help="workload of the headline line (default c2, BASELINE.json's metric config)")
+    ap.add_argument("--config", default="c5", choices=sorted(HEADS),
+                    help="workload of the headline line (default c5: BASELINE.json configs[4], "
+                         "the configuration the metric is quoted on at 1/2/4/8 GPUs)")
+    ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
 
     rank, local_rank, world = dist_env()
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py needs a CUDA device (there is no CPU path)")
-    ndev = torch.cuda.device_count()
+    if args.stub:
+        ndev = world                                   # pretend: one device per rank
+        device = torch.device("cpu")
+    else:
+        if not torch.cuda.is_available():
+            raise SystemExit("bench.py needs a CUDA device (there is no CPU path)")
+        ndev = torch.cuda.device_count()
     dev_index = local_rank % ndev           # one GPU per rank on a full node
-    torch.cuda.set_device(dev_index)
-    device = torch.device("cuda", dev_index)
+    if not args.stub:
+        torch.cuda.set_device(dev_index)
+        device = torch.device("cuda", dev_index)
     if world > 1:
-        # gloo: the only collectives are timing scalars (barrier, max, sum);
-        # the data path has none (north_star item (c))
+        # gloo: the only collectives are timing scalars (barrier, max, sum,
+        # gather); the data path has none (north_star item (c))
         _kd().init("gloo")
         if world > ndev and rank == 0:
             print(f"warning: {world} ranks on {ndev} GPU(s): functional run, not a measurement",
                   file=sys.stderr)
 
-    import paper_1909_07729_b200 as kt
-
-    peak, peak_src = measured_peaks()
-    clocks = ClockSampler(dev_index) if rank == 0 or world > 1 else None
-    if clocks:
-        clocks.start()
-        time.sleep(0.3)
-
     K, W = args.steps, args.warmup
     head_key, head_op, head_oracle_op = HEADS[args.config]
-    step = Step(kt, head_key, head_op, device, rank)
-    import hashlib
-    input_sha = hashlib.sha256(step.xs[0].view(torch.int16).cpu().numpy().tobytes()).hexdigest()
-    windows, clk, lps = time_windows(step, K, W, world, device, clocks)
+    hcfg = WL.CONFIGS[head_key]
+    if args.stub:
+        kt = None
+        peak, peak_src = measured_peaks()
+        clocks = None
+        step = StubStep(rank=rank)
+        windows, clk, lps = time_windows_stub(step, K, W, world)
+        input_sha = "stub"
+    else:
+        import paper_1909_07729_b200 as kt
+        peak, peak_src = measured_peaks()
+        clocks = ClockSampler(dev_index) if rank == 0 or world > 1 else None
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        step = Step(kt, head_key, head_op, device, rank)
+        import hashlib
+        input_sha = hashlib.sha256(step.xs[0].view(torch.int16).cpu().numpy().tobytes()).hexdigest()
+        windows, clk, lps = time_windows(step, K, W, world, device, clocks)
     ms_win = statistics.median(windows)
     ms = ms_win / K
     n_total = step.n * world
     value = n_total / (ms / 1e3) / 1e9
     gbs_per_gpu = step.bytes_per_step / (ms / 1e3) / 1e9
-    eager_ms = time_eager(step, K, device)
+    own_ms = statistics.median(step.own) / K       # this rank's own windows (per-rank report)
+    # every rank: sampled check of its own output against the oracle (cpu_baseline leg)
+    bad = checked = 0
+    if not args.no_cpu and head_oracle_op != "lstm":
+        bad, checked = oracle_check(step.xs[0], step.ys[0], head_oracle_op, seed=rank, stub=args.stub)
+    per_rank = _kd().gather_over_ranks([rank, dev_index, own_ms, bad, checked]) if world > 1 else \
+        [[rank, dev_index, own_ms, bad, checked]]
+    eager_ms = ms if args.stub else time_eager(step, K, device)
     sets, head_bytes = step.sets, step.bytes_per_step
     del step
-    torch.cuda.empty_cache()
+    if not args.stub:
+        torch.cuda.empty_cache()
 
-    if head_oracle_op != "lstm":
-        e2e_ms, h2d, d2h = time_e2e(kt, WL.CONFIGS[head_key], head_oracle_op, K, W, world, device, rank)
+    K_e2e = min(K, 20)
+    if args.stub:
+        e2e = {"value": None, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "note": "stub"}
+    elif head_oracle_op != "lstm":
+        e2e_ms, h2d, d2h = time_e2e(kt, hcfg, head_oracle_op, K_e2e, W, world, device, rank)
         e2e_val = n_total / (e2e_ms / 1e3) / 1e9
         e2e = {"value": round(e2e_val, 4), "unit": "Gelem/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4),
-               "path": f"kt_apply_host_ex (pinned host buffers, one chunk per step; steps "
-                       f"alternate over {E2E_STREAMS} caller streams so each D2H overlaps the next "
-                       f"step's H2D)"}
+               "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4), "steps": K_e2e,
+               "path": f"kt_apply_host_ex through the Python binding (pinned host buffers of the "
+                       f"{head_key} input, one chunk per step; steps alternate over {E2E_STREAMS} "
+                       f"caller streams so each D2H overlaps the next step's H2D)"}
     else:
         e2e = {"value": None, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "note": "no host-buffer entry point for the LSTM gate call (kt_apply_host serves "
                        "the elementwise ops)"}
 
     extra = {}
-    if not args.no_extra:
-        for key, op in EXTRA:
-            st = Step(kt, key, op, device, rank)
-            wts, _, _ = time_windows(st, K, W, world, device, None, min_total_s=0.3, max_windows=10)
-            m_ = statistics.median(wts) / K
-            units = st.n // 4 if st.cell else st.n
-            extra[f"{key}:{op}"] = {
-                "elements_per_gpu": units, "ms_per_step": round(m_, 5),
-                "gelem_s": round(units * world / (m_ / 1e3) / 1e9, 3),
-                "hbm_gbs_per_gpu": round(st.bytes_per_step / (m_ / 1e3) / 1e9, 1),
-                "frac_of_measured": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / peak, 4),
-                "frac_of_8tbs": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / NOMINAL_HBM_GBS, 4),
-                "l2": "inputs larger than L2" if st.sets == 1 else f"{st.sets} rotating sets"}
-            if st.dual:
-                extra[f"{key}:{op}"]["note"] = ("one pass, two outputs (K-GELU and K-Swish of x, "
-                                                "6 B/element); gelem_s counts input elements")
-            del st
-            torch.cuda.empty_cache()
-
-    if not args.no_extra:
-        # NEXT-2: the FFN up-projection that produces config 5's [65536, 16384]
-        # activations, K-GELU fused into the tcgen05 GEMM epilogue (K = 4096)
-        Mg, Ng, Kg = WL.CONFIGS["c5_ffn_2p30"].shape[0], WL.CONFIGS["c5_ffn_2p30"].shape[1], 4096
-        gA = WL.make_input("c5_ffn_2p30", device=device, rank=rank, numel=Mg * Kg).reshape(Mg, Kg)
-        gB = (WL.make_input("c5_ffn_2p30", device=device, rank=rank, numel=Ng * Kg, seed=7)
-              .reshape(Ng, Kg) * 0.02).to(torch.bfloat16)
-        gC = torch.empty(Mg, Ng, dtype=torch.bfloat16, device=device)
-
-        class _G:
-            n, bytes_per_step, sets = Mg * Ng, 0, 1
-            kt_ = kt
-
-            def run(self, i):
-                kt.kgemm_bf16(gA, gB, epilogue="gelu", out=gC)
-        gst = _G()
-        gst.kt = kt
-        wts, _, _ = time_windows(gst, K, W, world, device, None, min_total_s=0.3, max_windows=5)
-        m_ = statistics.median(wts) / K
-        tf = 2.0 * Mg * Ng * Kg / (m_ / 1e3) / 1e12
-        bf16_peak, bf16_sus = 1674.5, 1376.5
-        try:
-            _mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-            bf16_peak, bf16_sus = float(_mp["bf16_tflops"]), float(_mp["bf16_tflops_sustained"])
-        except Exception:
-            pass
-        extra["ffn_gemm_M65536_N16384_K4096:kgemm_bf16+kgelu"] = {
-            "ms_per_step": round(m_, 4), "tflops_per_gpu": round(tf, 1),
-            "roofline": {"bound": "tensor", "peak": bf16_sus, "unit": "TFLOP/s",
-                         "frac": round(tf / bf16_sus, 4), "frac_of_burst": round(tf / bf16_peak, 4),
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (a "
-                                        f"{m_ * K:.0f} ms loop of {m_:.1f} ms kernels)"},
-            "note": "tcgen05 GEMM, fp32 TMEM accumulation, K-GELU applied in the epilogue"}
-        del gA, gB, gC
-        torch.cuda.empty_cache()
-
-    if not args.no_extra:
-        extra["table2_b200"] = table2_b200(kt, K, W, world, device, rank, peak)
-
-    if not args.no_extra:
-        extra["lstm_gates_gemm_M6400_N4096_K1024:kgemm_lstm_gates_bf16"] = lstm_gemm_line(
-            kt, K, W, world, device, rank)
+    if not args.no_extra and not args.stub:
+        extra = side_lines(kt, args, K, W, world, device, rank, peak, head_key, head_op)
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(WL.CONFIGS[head_key], head_oracle_op, device)
+    if rank == 0 and not args.no_cpu and not args.stub:
+        cpu = cpu_baseline(hcfg, head_oracle_op, device)
+    if cpu is not None:
+        cpu["check"] = {"what": "every rank: seeded sample of its own GPU output vs the oracle on the "
+                                "same input bytes, after the timed region",
+                        "samples_per_rank": int(per_rank[0][4]),
+                        "mismatches": int(sum(r[3] for r in per_rank))}
 
     if clocks:
         clocks.stop()
-    traffic, traffic_src = load_range_traffic()
-    cold_traffic, cold_src = load_traffic("tanh_bf16")
-    if traffic is None:
-        traffic, traffic_src = cold_traffic, cold_src
-    if args.config != "c2":     # the committed DRAM captures are of the c2 launch
-        traffic, traffic_src = None, "not captured for this config (profiles/ holds the c2 capture)"
-        cold_traffic = cold_src = None
+    traffic, traffic_src = load_traffic(head_key, head_op)
     if rank == 0:
         out = {
             "metric": "K-TanH Gelem/s and achieved HBM GB/s vs ~8 TB/s peak at 1/2/4/8 B200",
             "value": round(value, 3), "unit": "Gelem/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": round(ms, 6), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u16" if WL.CONFIGS[head_key].dtype == torch.bfloat16 else "u32",
+            "vs_baseline": None, "dtype": DTYPE_NAME[hcfg.dtype],
             "data": "synthetic",
-            "config": {"workload": head_key, "desc": WL.CONFIGS[head_key].desc,
-                       "input_sha256": input_sha,
-                       "elements_per_gpu": WL.CONFIGS[head_key].numel, "call": head_op,
-                       "parallelism": f"{world} independent shards (seed+rank), no collective",
+            "config": head_config(head_key, head_op, world),
+            "timing": {"input_sha256_rank0": input_sha,
                        "l2": (f"{sets} rotating input/output sets ({sets * head_bytes >> 20} MiB > 4x L2)"
-                              if sets > 1 else "inputs larger than L2"),
+                              if sets > 1 else "inputs larger than L2 (no flush needed)"),
                        "launch": "CUDA graph of K library calls per timed window",
                        "windows": len(windows), "window_ms_median": round(ms_win, 5),
                        "window_ms_best": round(min(windows), 5)},
@@ -790,9 +832,9 @@ def main():
                          "frac_of_8tbs": round(gbs_per_gpu / NOMINAL_HBM_GBS, 4),
                          "kernel": KERNEL_NAME.get(head_op, head_op),
                          "algorithmic_bytes_per_launch": head_bytes,
-                         "traffic_source": traffic_src,
-                         "traffic_single_launch_cold": cold_traffic,
-                         "traffic_single_launch_source": cold_src},
+                         "traffic_source": traffic_src},
+            "per_rank": [{"rank": int(r[0]), "device": int(r[1]), "ms_per_step": round(r[2], 6),
+                          "checked": int(r[4]), "mismatches": int(r[3])} for r in per_rank],
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(round(lps * K)),
@@ -800,10 +842,80 @@ def main():
             "clocks": clk,
             "extra": extra,
         }
+        if args.stub:
+            out["stub"] = True
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def side_lines(kt, args, K, W, world, device, rank, peak, head_key, head_op):
+    """The `extra` object: the other configs and calls (the headline excluded)."""
+    extra = {}
+    for key, op in EXTRA:
+        if (key, op) == (head_key, head_op):
+            continue
+        st = Step(kt, key, op, device, rank)
+        wts, _, _ = time_windows(st, K, W, world, device, None, min_total_s=0.3, max_windows=10)
+        m_ = statistics.median(wts) / K
+        units = st.n // 4 if st.cell else st.n
+        tr, tr_src = load_traffic(key, op)
+        extra[f"{key}:{op}"] = {
+            "elements_per_gpu": units, "ms_per_step": round(m_, 5),
+            "gelem_s": round(units * world / (m_ / 1e3) / 1e9, 3),
+            "hbm_gbs_per_gpu": round(st.bytes_per_step / (m_ / 1e3) / 1e9, 1),
+            "frac_of_measured": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / peak, 4),
+            "frac_of_8tbs": round(st.bytes_per_step / (m_ / 1e3) / 1e9 / NOMINAL_HBM_GBS, 4),
+            "algorithmic_bytes_per_launch": st.bytes_per_step,
+            "l2": "inputs larger than L2" if st.sets == 1 else f"{st.sets} rotating sets"}
+        if tr is not None:
+            extra[f"{key}:{op}"]["traffic"] = tr
+            extra[f"{key}:{op}"]["traffic_source"] = tr_src
+        if st.dual:
+            extra[f"{key}:{op}"]["note"] = ("one pass, two outputs (K-GELU and K-Swish of x, "
+                                            "6 B/element); gelem_s counts input elements")
+        del st
+        torch.cuda.empty_cache()
+
+    # NEXT-2: the FFN up-projection that produces config 5's [65536, 16384]
+    # activations, K-GELU fused into the tcgen05 GEMM epilogue (K = 4096)
+    Mg, Ng, Kg = WL.CONFIGS["c5_ffn_2p30"].shape[0], WL.CONFIGS["c5_ffn_2p30"].shape[1], 4096
+    gA = WL.make_input("c5_ffn_2p30", device=device, rank=rank, numel=Mg * Kg).reshape(Mg, Kg)
+    gB = (WL.make_input("c5_ffn_2p30", device=device, rank=rank, numel=Ng * Kg, seed=7)
+          .reshape(Ng, Kg) * 0.02).to(torch.bfloat16)
+    gC = torch.empty(Mg, Ng, dtype=torch.bfloat16, device=device)
+
+    class _G:
+        n, bytes_per_step, sets = Mg * Ng, 0, 1
+
+        def run(self, i):
+            kt.kgemm_bf16(gA, gB, epilogue="gelu", out=gC)
+    gst = _G()
+    gst.kt = kt
+    wts, _, _ = time_windows(gst, K, W, world, device, None, min_total_s=0.3, max_windows=5)
+    m_ = statistics.median(wts) / K
+    tf = 2.0 * Mg * Ng * Kg / (m_ / 1e3) / 1e12
+    bf16_peak, bf16_sus = 1674.5, 1376.5
+    try:
+        _mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        bf16_peak, bf16_sus = float(_mp["bf16_tflops"]), float(_mp["bf16_tflops_sustained"])
+    except Exception:
+        pass
+    extra["ffn_gemm_M65536_N16384_K4096:kgemm_bf16+kgelu"] = {
+        "ms_per_step": round(m_, 4), "tflops_per_gpu": round(tf, 1),
+        "roofline": {"bound": "tensor", "peak": bf16_sus, "unit": "TFLOP/s",
+                     "frac": round(tf / bf16_sus, 4), "frac_of_burst": round(tf / bf16_peak, 4),
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (a "
+                                    f"{m_ * K:.0f} ms loop of {m_:.1f} ms kernels)"},
+        "note": "tcgen05 GEMM, fp32 TMEM accumulation, K-GELU applied in the epilogue"}
+    del gA, gB, gC
+    torch.cuda.empty_cache()
+
+    extra["table2_b200"] = table2_b200(kt, K, W, world, device, rank, peak)
+    extra["lstm_gates_gemm_M6400_N4096_K1024:kgemm_lstm_gates_bf16"] = lstm_gemm_line(
+        kt, K, W, world, device, rank)
+    return extra
 
 
 if __name__ == "__main__":

@@ -326,6 +326,29 @@ def _prep(x, out, dtype):
     return out
 
 
+def _check_out(t, name, dtype, numel, device):
+    """Validate a caller-supplied output tensor: the C ABI only sees a raw
+    pointer and cannot bound-check it."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.device != device:
+        raise TypeError(f"{name} must be a CUDA tensor on {device}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous() or t.numel() != numel:
+        raise ValueError(f"{name} must be contiguous with {numel} elements")
+    return t
+
+
+def _fmt_of(dtype):
+    """'bf16' / 'f32' for the two formats the library has; TypeError otherwise."""
+    import torch
+    if dtype == torch.bfloat16:
+        return "bf16"
+    if dtype == torch.float32:
+        return "f32"
+    raise TypeError(f"unsupported dtype {dtype}: the library has BF16 and FP32 paths only")
+
+
 def _make_call(name, dtype_name):
     fn = getattr(_lib, name)
 
@@ -421,10 +444,14 @@ def klstm_cell_bf16(gates, c_prev, hidden: int, c_next=None, h_next=None,
     rows = c_prev.numel() // hidden
     if c_prev.numel() != rows * hidden or gates.numel() != rows * 4 * hidden:
         raise ValueError("shapes: gates [rows, 4*hidden], c_prev [rows, hidden]")
+    if gates.device != c_prev.device:
+        raise ValueError("gates and c_prev must be on the same device")
     if c_next is None:
         c_next = torch.empty_like(c_prev)
+    _check_out(c_next, "c_next", torch.float32, rows * hidden, c_prev.device)
     if h_next is None:
         h_next = torch.empty(c_prev.shape, dtype=torch.bfloat16, device=c_prev.device)
+    _check_out(h_next, "h_next", torch.bfloat16, rows * hidden, c_prev.device)
     lut = lut or paper_lut()
     idx = gates.device.index
     with _on_device(idx):
@@ -444,10 +471,13 @@ def kgemm_bf16(A, B, epilogue: str | None = None, out=None, lut: Lut | None = No
         raise ValueError("A [M, K], B [N, K]")
     if not (A.is_contiguous() and B.is_contiguous()):
         raise ValueError("A, B must be contiguous")
+    if A.device != B.device:
+        raise ValueError("A and B must be on the same device")
     M, K = A.shape
     N = B.shape[0]
     if out is None:
         out = torch.empty(M, N, dtype=torch.bfloat16, device=A.device)
+    _check_out(out, "out", torch.bfloat16, M * N, A.device)
     epi = -1 if epilogue is None else OPS[epilogue]
     lut = lut or paper_lut()
     idx = A.device.index
@@ -460,7 +490,7 @@ def kgemm_bf16(A, B, epilogue: str | None = None, out=None, lut: Lut | None = No
 def apply(op: str, x, out=None, lut: Lut | None = None, stream=None):
     """Generic kt_apply dispatch by op name and the tensor's dtype."""
     import torch
-    dname = "bf16" if x.dtype == torch.bfloat16 else "f32"
+    dname = _fmt_of(x.dtype)
     out = _prep(x, out, x.dtype)
     lut = lut or paper_lut()
     with torch.cuda.device(x.device):
@@ -475,11 +505,17 @@ def apply_host(op: str, x_host, y_host, work, lut: Lut | None = None, stream=Non
     uint8 scratch tensor on the current device, `chunk` elements per pipeline
     chunk (0 = default).  Asynchronous on `stream`."""
     import torch
-    if x_host.is_cuda or y_host.is_cuda or not work.is_cuda:
-        raise TypeError("x_host / y_host must be CPU tensors, work a CUDA tensor")
+    dname = _fmt_of(x_host.dtype)
     if x_host.dtype != y_host.dtype or x_host.numel() != y_host.numel():
         raise ValueError("x_host and y_host must match")
-    dname = "bf16" if x_host.dtype == torch.bfloat16 else "f32"
+    if not (x_host.is_contiguous() and y_host.is_contiguous()):
+        raise ValueError("x_host and y_host must be contiguous")
+    if x_host.is_cuda or y_host.is_cuda or not work.is_cuda:
+        raise TypeError("x_host / y_host must be CPU tensors, work a CUDA tensor")
+    if not work.is_contiguous():
+        raise ValueError("work must be contiguous")
+    if stream is None and work.device.index != torch.cuda.current_device():
+        raise ValueError("work must be on the current CUDA device (or pass its stream)")
     lut = lut or paper_lut()
     with torch.cuda.device(work.device):
         _check(_lib.kt_apply_host_ex(OPS[op], DTYPES[dname], x_host.data_ptr(), y_host.data_ptr(),
@@ -609,9 +645,12 @@ def kgemm_lstm_gates_bf16(A, B, hidden: int, tanh_quarter: int = 2, out=None, lu
         raise ValueError("A [M, K], B [4*hidden, K]")
     if not (A.is_contiguous() and B.is_contiguous()):
         raise ValueError("A, B must be contiguous")
+    if A.device != B.device:
+        raise ValueError("A and B must be on the same device")
     M, K = A.shape
     if out is None:
         out = torch.empty(M, 4 * hidden, dtype=torch.bfloat16, device=A.device)
+    _check_out(out, "out", torch.bfloat16, M * 4 * hidden, A.device)
     lut = lut or paper_lut()
     idx = A.device.index
     with _on_device(idx):
@@ -634,10 +673,14 @@ def kgemm_lstm_cell_bf16(A, B, c_prev, hidden: int, c_next=None, h_next=None, lu
         raise ValueError("A [M, K], B [4*hidden, K], c_prev [M, hidden]")
     if not (A.is_contiguous() and B.is_contiguous() and c_prev.is_contiguous()):
         raise ValueError("inputs must be contiguous")
+    if not (A.device == B.device == c_prev.device):
+        raise ValueError("A, B and c_prev must be on the same device")
     if c_next is None:
         c_next = torch.empty_like(c_prev)
+    _check_out(c_next, "c_next", torch.float32, M * hidden, A.device)
     if h_next is None:
         h_next = torch.empty(c_prev.shape, dtype=torch.bfloat16, device=c_prev.device)
+    _check_out(h_next, "h_next", torch.bfloat16, M * hidden, A.device)
     lut = lut or paper_lut()
     idx = A.device.index
     with _on_device(idx):

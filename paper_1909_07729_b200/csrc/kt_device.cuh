@@ -44,6 +44,11 @@ __device__ __forceinline__ uint32_t hset2_gt(uint32_t a, uint32_t b) {
   asm("set.gt.u32.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
 }
+__device__ __forceinline__ uint32_t hset2_ne(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("set.ne.u32.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
 
 // hi32(a*b) and hi32(a*b) + c (IMAD.HI, FMA pipe)
 __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {
@@ -124,7 +129,7 @@ constexpr uint32_t kGeluC1Bits = 0x3D122279u;
 // lane shifts, the pack and the masks/selects.  Exhaustively checked against
 // the oracle (tests/test_gpu_parity.py).
 //   lw = this lane's word LutWords::bf16[lane] = L_lane.
-__device__ __forceinline__ uint32_t ktanh_bf16x2(uint32_t x, uint32_t lw) {
+__device__ __forceinline__ uint32_t ktanh_bf16x2(uint32_t x, uint32_t lw, uint32_t &mag) {
   // line 6: t = bits [8:4] of each half = (E & 3) : (M >> 4)
   // line 7: theta_t by shuffle from lane t
   const uint32_t Ll = shfl_lut(lw, x >> 4);
@@ -136,14 +141,17 @@ __device__ __forceinline__ uint32_t ktanh_bf16x2(uint32_t x, uint32_t lw) {
   // lines 3-4: region masks per half.  |x| by abs.bf16x2, which ptxas
   // emits as HFMA2 (-0 * 0 + |x|) on the FMA pipe: one ALU op fewer per
   // pair than x & 0x7FFF7FFF (NaN stays NaN, subnormals compare as bypass
-  // either way)
-  uint32_t mag;
+  // either way).  |x| is handed back to the caller (K-Swish/K-GELU reuse it).
   asm("abs.bf16x2 %0, %1;" : "=r"(mag) : "r"(x));
   const uint32_t byp = hset2_ltu(mag, kT1x2);      // |x| < T1, or NaN
   const uint32_t sat = hset2_gt(mag, kT2x2);       // |x| > T2, incl. inf
   const uint32_t m = bsel(sat, kOnex2, ymag);      // line 4: (s, E_bias, 0)
   const uint32_t o = bsel(byp, x, m);              // line 3: y = x
   return o | (x & kSignx2);                        // s_o = s_i
+}
+__device__ __forceinline__ uint32_t ktanh_bf16x2(uint32_t x, uint32_t lw) {
+  uint32_t mag;
+  return ktanh_bf16x2(x, lw, mag);
 }
 
 // Algorithm 1 with the 64-interval table of PAPER.md:223 (4 mantissa index
@@ -217,15 +225,72 @@ __device__ __forceinline__ uint32_t ksigmoid_bf16x2(uint32_t x, uint32_t lw) {
   return hfma2_bf16(t, kHalfx2, kHalfx2);                                 // RN((1+t)/2)
 }
 
-// K-Swish / K-GELU outer step as one packed BF16 fma: RN_bf16(h + h t) with
-// h = RN_bf16(x/2), the exact value rounded once -- the oracle's definition
-// whenever x/2 is a BF16 (all but subnormal x, where the result equals it
-// too: checked over all 65,536 patterns, 0 ulp).  The fp32 route needed
-// widen + FMUL2/FFMA2 + pack (5 more ALU ops per pair).
-__device__ __forceinline__ uint32_t kswish_bf16x2(uint32_t x, uint32_t lw) {
+// K-Swish / K-GELU outer step y = RN_bf16(x/2 (1 + t)), the exact value
+// rounded once (reading R-DERIVED).  With h = RN_bf16(x/2) (one packed mul),
+// one packed fma RN_bf16(h + h t) IS that value whenever x/2 is a BF16, i.e.
+// for every x except |x| < 2^-125 with an odd last bit, where x/2 is a BF16
+// tie.  There t is tiny with the sign of x, so the exact term (x/2) t > 0
+// breaks the tie toward +inf (when t != 0): r = x - 2h (exact, +-1 subnormal
+// ulp) is > 0 exactly when h was rounded down, and the addend becomes h + r.
+//   outer_exact:  3 FMA-pipe + 3 ALU ops more than the plain fma, exact for
+//                 every x (the element-wise paths and the GEMM epilogue).
+//   streaming kernels: the plain fma, plus ONE packed-u16 min per pair over the
+//                 |argument| the K-TanH core computes anyway (|x/2| or
+//                 |RN_bf16(u)|); a warp whose minimum is < 0x100 in some half
+//                 (an argument below 2^-125, or a zero) re-reads x and patches
+//                 the pairs with |x| < 2^-125 from the closed form tie_patch
+//                 (never taken on the bench's N(0,1) data).
+constexpr uint32_t kNegTwox2 = 0xC000C000u;   // (-2, -2) in BF16
+
+__device__ __forceinline__ uint32_t outer_exact(uint32_t x, uint32_t h, uint32_t t) {
+  const uint32_t r = hfma2_bf16(h, kNegTwox2, x);                     // x - 2h, exact
+  const uint32_t up = hset2_gt(r, 0u) & hset2_ne(t, 0u) & kOnex2;     // 1.0 where the t-term rounds up
+  return hfma2_bf16(h, t, hfma2_bf16(r, up, h));                      // RN(h t + (h + [up] r))
+}
+
+__device__ __forceinline__ uint32_t umin16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+// some half of the running minimum of |argument| is < 0x100 (2^-125)
+__device__ __forceinline__ bool tie_possible(uint32_t kmin) {
+  return (kmin & 0xFF00u) == 0 || (kmin & 0xFF000000u) == 0;
+}
+
+// Closed form of the exact outer step for |x| < 2^-125 (magnitude bits
+// m < 0x100 are then linear in 2^-133 units, x/2 = m/2 units, t is tiny with
+// the sign s of x): y = s | ((m + 1 - s) >> 1), except K-Swish at m = 1 where
+// t = K-TanH(RN(x/2)) = 0 and the tie goes to even (0).  y (the plain-fma
+// result) is kept for every half with |x| >= 2^-125.
+template <int OP>
+__device__ __forceinline__ uint32_t tie_patch(uint32_t x, uint32_t y) {
+  uint32_t out = 0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t xv = (x >> (16 * k)) & 0xFFFFu, m = xv & 0x7FFFu, s = xv & 0x8000u;
+    uint32_t yv = (y >> (16 * k)) & 0xFFFFu;
+    if (m < 0x100u) {
+      const uint32_t inc = (s == 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;
+      yv = s | ((m + inc) >> 1);
+    }
+    out |= yv << (16 * k);
+  }
+  return out;
+}
+
+// plain-fma forms (exact unless tie_patch applies); mag = |argument| of the
+// K-TanH core (the caller folds it into the tie screen's running minimum)
+__device__ __forceinline__ uint32_t kswish_bf16x2_fast(uint32_t x, uint32_t lw, uint32_t &mag) {
   const uint32_t h = hmul2_bf16(x, kHalfx2);                              // RN_bf16(x/2)
-  const uint32_t t = ktanh_bf16x2(h, lw);
+  const uint32_t t = ktanh_bf16x2(h, lw, mag);
   return hfma2_bf16(h, t, h);                                             // RN(h (1+t))
+}
+
+__device__ __forceinline__ uint32_t kswish_bf16x2(uint32_t x, uint32_t lw) {
+  const uint32_t h = hmul2_bf16(x, kHalfx2);
+  const uint32_t t = ktanh_bf16x2(h, lw);
+  return outer_exact(x, h, t);
 }
 
 __device__ __forceinline__ float gelu_arg(float x) {
@@ -234,13 +299,24 @@ __device__ __forceinline__ float gelu_arg(float x) {
   return __fmul_rn(x, p);
 }
 
-__device__ __forceinline__ uint32_t kgelu_bf16x2(uint32_t x, uint32_t lw) {
+// t = K-TanH(RN_bf16(u)) of the GELU argument (R-GELU-ARG, fp32x2), |RN_bf16(u)| in mag
+__device__ __forceinline__ uint32_t kgelu_t_bf16x2(uint32_t x, uint32_t lw, uint32_t &mag) {
   const float2 xv = widen2(x);
   const float2 x2 = mul2(xv, xv);
   const float2 p = fma2(splat2(__uint_as_float(kGeluC1Bits)), x2, splat2(__uint_as_float(kGeluC0Bits)));
-  const uint32_t t = ktanh_bf16x2(pack2(mul2(xv, p)), lw);                 // RN_bf16(u)
+  return ktanh_bf16x2(pack2(mul2(xv, p)), lw, mag);                       // RN_bf16(u)
+}
+
+__device__ __forceinline__ uint32_t kgelu_bf16x2_fast(uint32_t x, uint32_t lw, uint32_t &mag) {
+  const uint32_t t = kgelu_t_bf16x2(x, lw, mag);   // |x| < 2^-125 => |RN(u)| < 0xCD ulps
   const uint32_t h = hmul2_bf16(x, kHalfx2);                              // RN_bf16(x/2)
   return hfma2_bf16(h, t, h);                                             // RN(h (1+t))
+}
+
+__device__ __forceinline__ uint32_t kgelu_bf16x2(uint32_t x, uint32_t lw) {
+  uint32_t mag;
+  const uint32_t t = kgelu_t_bf16x2(x, lw, mag);
+  return outer_exact(x, hmul2_bf16(x, kHalfx2), t);
 }
 
 __device__ __forceinline__ uint32_t ksigmoid_f32(uint32_t u, uint32_t lk, uint32_t lc) {
@@ -249,17 +325,29 @@ __device__ __forceinline__ uint32_t ksigmoid_f32(uint32_t u, uint32_t lk, uint32
   return __float_as_uint(__fmaf_rn(0.5f, t, 0.5f));
 }
 
+// F32 outer step y = RN32(x/2 (1 + t)), exact (R-DERIVED): hx = RN32(x/2) is
+// x/2 except for |x| < 2^-125 with an odd last bit (an F32 tie); as for BF16
+// the exact t-term (sign of x, t != 0) then breaks the tie toward +inf.
+// r = x - 2 hx is exact (0 or +-1 subnormal ulp).  4 more ops per element
+// than fma(hx, t, hx); the F32 derived ops are not on the headline path.
+__device__ __forceinline__ float outer_exact_f32(float x, float hx, float t) {
+  const float r = __fmaf_rn(hx, -2.0f, x);
+  const float c = (r > 0.0f && t != 0.0f) ? __fadd_rn(hx, r) : hx;
+  return __fmaf_rn(hx, t, c);
+}
+
 __device__ __forceinline__ uint32_t kswish_f32(uint32_t u, uint32_t lk, uint32_t lc) {
-  const float hx = __fmul_rn(__uint_as_float(u), 0.5f);
+  const float x = __uint_as_float(u);
+  const float hx = __fmul_rn(x, 0.5f);
   const float t = __uint_as_float(ktanh_f32(__float_as_uint(hx), lk, lc));
-  return __float_as_uint(__fmaf_rn(hx, t, hx));
+  return __float_as_uint(outer_exact_f32(x, hx, t));
 }
 
 __device__ __forceinline__ uint32_t kgelu_f32(uint32_t u, uint32_t lk, uint32_t lc) {
   const float x = __uint_as_float(u);
   const float t = __uint_as_float(ktanh_f32(__float_as_uint(gelu_arg(x)), lk, lc));
   const float hx = __fmul_rn(x, 0.5f);
-  return __float_as_uint(__fmaf_rn(hx, t, hx));
+  return __float_as_uint(outer_exact_f32(x, hx, t));
 }
 
 // ------------------------------------------------------- backward (NEXT-1) --
@@ -340,6 +428,32 @@ __device__ __forceinline__ uint32_t apply_bf16x2(uint32_t x, const LaneLut &L) {
   return kgelu_bf16x2(x, L.w16);
 }
 
+// Streaming form: K-Swish / K-GELU BF16 take the plain-fma outer step and
+// return |argument| in mag (the kernel folds it into the screen's minimum and
+// patches a flagged warp's chunk with tie_patch); every other op is
+// apply_word itself (mag = all ones).
+// KT_TIE_MODE (dev A/B builds only): 0 = tie screen (default), 1 = the exact
+// outer step on every pair, 2 = the plain fma with no screen (NOT exact on
+// the x/2 ties; measures the screen's cost).
+#ifndef KT_TIE_MODE
+#define KT_TIE_MODE 0
+#endif
+template <int OP>
+__device__ __forceinline__ uint32_t apply_bf16x2_fast(uint32_t x, const LaneLut &L, uint32_t &mag) {
+  mag = 0xFFFFFFFFu;
+#if KT_TIE_MODE == 1
+  return apply_bf16x2<OP>(x, L);
+#else
+  uint32_t m = 0xFFFFFFFFu;
+  uint32_t r;
+  if (OP == OP_SWISH) r = kswish_bf16x2_fast(x, L.w16, m);
+  else if (OP == OP_GELU) r = kgelu_bf16x2_fast(x, L.w16, m);
+  else r = apply_bf16x2<OP>(x, L);
+  if (KT_TIE_MODE == 0) mag = m;
+  return r;
+#endif
+}
+
 // K-TanH of an F32 value through BF16 (the A8 alternative;
 // PAPER.md:256 "We assume BFloat16 input ... conversion cost is not
 // considered"): RNE to BF16 (F2FP), Alg. 1 on the BF16 bits, widen exactly.
@@ -362,6 +476,18 @@ template <int OP, int FMT>
 __device__ __forceinline__ uint32_t apply_word(uint32_t w, const LaneLut &L) {
   if (FMT == FMT_BF16) return apply_bf16x2<OP>(w, L);
   return apply_f32<OP>(w, L);
+}
+
+template <int OP, int FMT>
+__device__ __forceinline__ uint32_t apply_word_fast(uint32_t w, const LaneLut &L, uint32_t &mag) {
+  mag = 0xFFFFFFFFu;
+  if (FMT == FMT_BF16) return apply_bf16x2_fast<OP>(w, L, mag);
+  return apply_f32<OP>(w, L);
+}
+// does apply_word_fast need the tie screen for this op/format?
+template <int OP, int FMT>
+__host__ __device__ constexpr bool needs_tie_screen() {
+  return FMT == FMT_BF16 && (OP == OP_SWISH || OP == OP_GELU);
 }
 
 template <int OP, int FMT>

@@ -45,6 +45,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "kt_async.cuh"
 #include "kt_device.cuh"
 #include "kt_internal.h"
 
@@ -54,29 +55,6 @@ constexpr int kBK = 64;                               // K block (one 128-byte s
 constexpr uint32_t kABytes = 128 * kBK * 2;          // A tile per CTA and stage: 16 KiB
 constexpr uint32_t kTmemCols = 256;                  // one accumulator stage
 static_assert(16 * 6 + 64 <= 256, "barrier area");
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t phase) {
-  uint32_t ok = 0;
-  for (uint32_t spin = 0;; ++spin) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok) : "r"(a), "r"(phase) : "memory");
-    if (ok) return;
-    if (spin > (1u << 26)) __trap();   // never hang the GPU on a protocol bug
-  }
-}
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
                                             uint32_t mbar) {
@@ -531,13 +509,22 @@ template <int EPI, int CTAS>
 static cudaError_t launch_t(const CUtensorMap &ma, const CUtensorMap &mb, const GemmArgs &g,
                             const LutWords &lut, cudaStream_t s, int sms) {
   using Sh = GemmShape<CTAS>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_gemm_t<EPI, CTAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)Sh::kSmem);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  // The dynamic-smem limit is a per-device (per-context) function attribute:
+  // set it once per device, not once per process, so the first call on a
+  // second GPU does not launch with the 48 KB default.  Two threads racing on
+  // a fresh device both set the same value (idempotent).
+  constexpr int kMaxDevGemm = 64;
+  static int attr_done[kMaxDevGemm];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevGemm) return cudaErrorInvalidDevice;
+  if (!__atomic_load_n(&attr_done[dev], __ATOMIC_ACQUIRE)) {
+    e = cudaFuncSetAttribute(k_gemm_t<EPI, CTAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Sh::kSmem);
+    if (e != cudaSuccess) return e;
+    __atomic_store_n(&attr_done[dev], 1, __ATOMIC_RELEASE);
+  }
   const size_t tiles = (g.M / (128 * CTAS)) * (EPI == kEpiCell ? g.H / 64 : g.N / 256);
   const size_t units = (size_t)(sms / CTAS);
   const unsigned grid = (unsigned)(CTAS * (tiles < units ? tiles : units));
@@ -553,7 +540,7 @@ static cudaError_t launch_t(const CUtensorMap &ma, const CUtensorMap &mb, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CTAS == 2 ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm_t<EPI, CTAS>, ma, mb, g, lut);
+  e = cudaLaunchKernelEx(&cfg, k_gemm_t<EPI, CTAS>, ma, mb, g, lut);
   count_launch();
   return e;
 }

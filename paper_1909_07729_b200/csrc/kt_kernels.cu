@@ -25,6 +25,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "kt_async.cuh"
 #include "kt_device.cuh"
 #include "kt_internal.h"
 
@@ -94,11 +95,57 @@ __device__ __forceinline__ void scalar_span(const uint8_t *xp, uint8_t *yp, uint
   }
 }
 
+// Tie-screen fix-up (K-Swish / K-GELU BF16, kt_device.cuh tie_patch): after
+// the chunk's stores, this lane re-reads its x and y words and rewrites the
+// BF16 pairs with |x| < 2^-125 from the closed form.  Out of line and word by
+// word so that it costs the streaming kernels no registers; plain (coherent)
+// loads see the lane's own preceding stores.  Out-of-place calls only.
+template <int OP>
+__device__ __noinline__ void tie_fixup(const uint8_t *xb, uint8_t *yb, uint64_t base, uint64_t nvec) {
+#pragma unroll 1
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t i = base + (uint64_t)u * 32;
+    if (i >= nvec) continue;
+    const uint32_t *xs = reinterpret_cast<const uint32_t *>(xb + i * kVecBytes);
+    uint32_t *ys = reinterpret_cast<uint32_t *>(yb + i * kVecBytes);
+#pragma unroll 1
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t w = xs[j];
+      if ((w & 0x7F00u) == 0 || (w & 0x7F000000u) == 0) ys[j] = tie_patch<OP>(w, ys[j]);
+    }
+  }
+}
+
+__device__ __noinline__ void tie_fixup_dual(const uint8_t *xb, uint8_t *gb, uint8_t *sb, uint64_t base,
+                                            uint64_t nvec) {
+#pragma unroll 1
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t i = base + (uint64_t)u * 32;
+    if (i >= nvec) continue;
+    const uint32_t *xs = reinterpret_cast<const uint32_t *>(xb + i * kVecBytes);
+    uint32_t *gs = reinterpret_cast<uint32_t *>(gb + i * kVecBytes);
+    uint32_t *ss = reinterpret_cast<uint32_t *>(sb + i * kVecBytes);
+#pragma unroll 1
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t w = xs[j];
+      if ((w & 0x7F00u) == 0 || (w & 0x7F000000u) == 0) {
+        gs[j] = tie_patch<OP_GELU>(w, gs[j]);
+        ss[j] = tie_patch<OP_SWISH>(w, ss[j]);
+      }
+    }
+  }
+}
+
 // Main streaming kernel.  x/y: original (element-aligned) pointers; `head`
 // elements precede the first 32-B boundary of x (and of y: same offset mod
 // 32, checked on the host); nvec vectors follow; then `tail` elements.
+#ifdef KT_MAP_MINB
+template <int OP, int FMT, bool NC, bool PF>
+__global__ void __launch_bounds__(kThreads, KT_MAP_MINB)
+#else
 template <int OP, int FMT, bool NC, bool PF>
 __global__ void __launch_bounds__(kThreads)
+#endif
 k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
       uint32_t pf_blocks, uint32_t pf_depth, const __grid_constant__ LutWords lut) {
   constexpr uint32_t es = (FMT == FMT_BF16) ? 2 : 4;
@@ -125,16 +172,37 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
     const uint64_t i = base + (uint64_t)u * 32;
     ld256<NC>(xb + i * kVecBytes, v[u], i < nvec);
   }
+  // K-Swish / K-GELU BF16 out of place: plain-fma outer step + tie screen
+  // (kt_device.cuh); in place (x == y, no copy of x survives the stores) the
+  // exact outer step on every pair
+  constexpr bool kScreen = needs_tie_screen<OP, FMT>() && NC;
+  uint32_t kmin = 0xFFFFFFFFu;
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[u][j] = apply_word<OP, FMT>(v[u][j], L);
+    for (int j = 0; j < 8; j += 2) {
+      if (kScreen) {
+        uint32_t m0, m1;
+        v[u][j] = apply_word_fast<OP, FMT>(v[u][j], L, m0);
+        v[u][j + 1] = apply_word_fast<OP, FMT>(v[u][j + 1], L, m1);
+#if defined(KT_TIE_SERIAL) && KT_TIE_SERIAL
+        kmin = umin16x2(umin16x2(kmin, m0), m1);          // dev A/B: serial chain
+#else
+        kmin = umin16x2(kmin, umin16x2(m0, m1));          // one VIMNMX3 per two pairs
+#endif
+      } else {
+        v[u][j] = apply_word<OP, FMT>(v[u][j], L);
+        v[u][j + 1] = apply_word<OP, FMT>(v[u][j + 1], L);
+      }
+    }
   }
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     st256(yb + i * kVecBytes, v[u], i < nvec);
   }
+  if (kScreen && __any_sync(0xffffffffu, tie_possible(kmin)))
+    tie_fixup<OP>(xb, yb, base, nvec);   // rare: an |argument| < 2^-125 (or a zero) in the chunk
   if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
     scalar_span<OP, FMT>(x, y, head, L);
     const size_t toff = ((size_t)head + (size_t)nvec * (kVecBytes / es)) * es;
@@ -261,18 +329,30 @@ k_dual(const uint8_t *x, uint8_t *yg, uint8_t *ys, uint32_t head, uint64_t nvec,
     const uint64_t i = base + (uint64_t)u * 32;
     ld256<NC>(x + hb + i * kVecBytes, v[u], i < nvec);
   }
+  constexpr bool kScreen = needs_tie_screen<OP_GELU, FMT>() && NC;   // as in k_map
+  uint32_t kmin = 0xFFFFFFFFu;
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
     uint32_t g[8], sw[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      g[j] = apply_word<OP_GELU, FMT>(v[u][j], L);
-      sw[j] = apply_word<OP_SWISH, FMT>(v[u][j], L);
+      if (kScreen) {
+        // |RN_bf16(u)| < 2^-125 for every |x| < 2^-125: the K-GELU key covers both outputs
+        uint32_t m, munused;
+        g[j] = apply_word_fast<OP_GELU, FMT>(v[u][j], L, m);
+        sw[j] = apply_word_fast<OP_SWISH, FMT>(v[u][j], L, munused);
+        kmin = umin16x2(kmin, m);
+      } else {
+        g[j] = apply_word<OP_GELU, FMT>(v[u][j], L);
+        sw[j] = apply_word<OP_SWISH, FMT>(v[u][j], L);
+      }
     }
     const uint64_t i = base + (uint64_t)u * 32;
     st256(yg + hb + i * kVecBytes, g, i < nvec);
     st256(ys + hb + i * kVecBytes, sw, i < nvec);
   }
+  if (kScreen && __any_sync(0xffffffffu, tie_possible(kmin)))
+    tie_fixup_dual(x + hb, yg + hb, ys + hb, base, nvec);   // rare
   if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
     dual_span<FMT>(x, yg, ys, head, L);
     const size_t toff = ((size_t)head + (size_t)nvec * (kVecBytes / es)) * es;
@@ -482,6 +562,224 @@ k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_
   st256(c_next + cidx * 4, cn0, on);
   st256(c_next + cidx * 4 + 32, cn1, on);
   st256(h_next + cidx * 2, h, on);
+}
+
+// ---- fused LSTM cell, staged through shared memory (bulk async copies) -------
+// The register-staged k_lstm_cell holds six 256-bit loads per lane across the
+// whole cell computation, so its bytes in flight are bounded by the register
+// file (64 regs, ~41% warps active, long-scoreboard bound: 0.91 of the copy
+// bandwidth).  Here the loads are decoupled from the registers:
+//   * persistent CTAs, each owning a contiguous, balanced range of cells,
+//     cut into tiles of kCellTile cells;
+//   * one producer warp per CTA streams each tile's 4 gate segments (per row
+//     the tile touches) and its c segment into a kCellStages-deep ring of
+//     shared-memory stages with cp.async.bulk (TMA engine), completion counted
+//     in bytes on the stage's "full" mbarrier;
+//   * kCellConsumerWarps consumer warps: thread i takes kCellGroups groups of
+//     4 cells (group g: cells g T/G + 4i .. +3 of the tile, so every shared
+//     load is conflict-free: LDS.64 per gate row, LDS.128 for c), releases the
+//     stage ("empty" mbarrier, one arrive per warp), computes the cells
+//     (lstm_cell2, the same device code as the register kernel) and stores c'
+//     (128-bit) and h (64-bit) straight from registers.
+// c_next may alias c_prev: a tile's c is in shared memory before any c' of
+// that tile is written, and other tiles' c ranges are disjoint.
+#ifndef KT_CELL_WARPS
+#define KT_CELL_WARPS 8
+#endif
+#ifndef KT_CELL_GROUPS
+#define KT_CELL_GROUPS 2
+#endif
+#ifndef KT_CELL_STAGES
+#define KT_CELL_STAGES 4
+#endif
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+constexpr int kCellConsumerWarps = KT_CELL_WARPS;
+constexpr int kCellGroups = KT_CELL_GROUPS;
+constexpr int kCellThreads = (kCellConsumerWarps + 1) * 32;             // + producer warp
+constexpr uint32_t kCellGroupCells = kCellConsumerWarps * 32 * 4;       // cells per group
+constexpr uint32_t kCellTile = kCellGroupCells * kCellGroups;           // cells per tile
+constexpr int kCellStages = KT_CELL_STAGES;
+constexpr uint32_t kCellStageBytes = kCellTile * (4 * 2 + 4);           // gates BF16 + c F32
+constexpr uint32_t kCellSmem = kCellStages * kCellStageBytes + 2 * kCellStages * 8;
+constexpr uint32_t kCellMinHidden = 256;   // tiles touch few rows: few, large copies
+#ifndef KT_CELL_DEFAULT
+#define KT_CELL_DEFAULT 2
+#endif
+
+__global__ void __launch_bounds__(kCellThreads)
+k_lstm_cell_tma(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_t *h_next,
+                uint64_t n, uint32_t hidden, const __grid_constant__ LutWords lut) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_full = sbase + kCellStages * kCellStageBytes;      // kCellStages x 8 B
+  const uint32_t bar_empty = bar_full + kCellStages * 8;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const LaneLut L = load_lane_lut(lut);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kCellStages; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, kCellConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // this CTA's contiguous range [v_beg, v_end), 16-cell granules balanced over the grid
+  const uint64_t gran = n / 16, gq = gran / gridDim.x, gr = gran % gridDim.x;
+  const uint64_t v_beg = (gq * blockIdx.x + umin64(blockIdx.x, gr)) * 16;
+  const uint64_t v_end = v_beg + (gq + (blockIdx.x < gr ? 1 : 0)) * 16;
+  const uint32_t ntiles = (uint32_t)((v_end - v_beg + kCellTile - 1) / kCellTile);
+
+  if (warp == kCellConsumerWarps) {
+    // ---------------- producer warp ----------------
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // the preceding grid's writes are visible
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t s = t % kCellStages, ph = (t / kCellStages) & 1;
+      const uint64_t v0 = v_beg + (uint64_t)t * kCellTile;
+      const uint32_t len = (uint32_t)umin64(kCellTile, v_end - v0);
+      mbar_wait(bar_empty + 8 * s, ph ^ 1);               // every consumer warp released it
+      if (lane == 0) mbar_expect_tx(bar_full + 8 * s, len * 12u);
+      __syncwarp();
+      const uint32_t st = sbase + s * kCellStageBytes;
+      const uint64_t row0 = v0 / hidden;
+      const uint32_t nseg = (uint32_t)((v0 + len - 1) / hidden - row0 + 1);
+      // copy k < 4 nseg: gate q = k & 3 of row segment k >> 2; copy 4 nseg: c
+      for (uint32_t k = lane; k <= 4 * nseg; k += 32) {
+        if (k == 4 * nseg) {
+          bulk_g2s(st + kCellTile * 8, c_prev + v0 * 4, len * 4, bar_full + 8 * s);
+          continue;
+        }
+        const uint32_t q = k & 3;
+        const uint64_t row = row0 + (k >> 2);
+        const uint64_t sb = row * hidden > v0 ? row * hidden : v0;           // segment [sb, se)
+        const uint64_t se = umin64((row + 1) * hidden, v0 + len);
+        const uint8_t *src = gates + (row * 4 * hidden + (uint64_t)q * hidden + (sb - row * hidden)) * 2;
+        bulk_g2s(st + q * kCellTile * 2 + (uint32_t)(sb - v0) * 2, src, (uint32_t)(se - sb) * 2,
+                 bar_full + 8 * s);
+      }
+    }
+    return;
+  }
+  // ---------------- consumer warps ----------------
+  for (uint32_t t = 0; t < ntiles; ++t) {
+    const uint32_t s = t % kCellStages, ph = (t / kCellStages) & 1;
+    const uint64_t v0 = v_beg + (uint64_t)t * kCellTile;
+    const uint32_t len = (uint32_t)umin64(kCellTile, v_end - v0);
+    mbar_wait(bar_full + 8 * s, ph);
+    const uint8_t *st = smem + s * kCellStageBytes;
+    uint2 gi[kCellGroups], gf[kCellGroups], gg[kCellGroups], go[kCellGroups];
+    float4 c[kCellGroups];
+#pragma unroll
+    for (int g = 0; g < kCellGroups; ++g) {
+      const uint32_t i4 = g * kCellGroupCells + threadIdx.x * 4;         // first cell of the group
+      gi[g] = *reinterpret_cast<const uint2 *>(st + 0 * kCellTile * 2 + i4 * 2);
+      gf[g] = *reinterpret_cast<const uint2 *>(st + 1 * kCellTile * 2 + i4 * 2);
+      gg[g] = *reinterpret_cast<const uint2 *>(st + 2 * kCellTile * 2 + i4 * 2);
+      go[g] = *reinterpret_cast<const uint2 *>(st + 3 * kCellTile * 2 + i4 * 2);
+      c[g] = *reinterpret_cast<const float4 *>(st + kCellTile * 8 + i4 * 4);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_empty + 8 * s);       // stage s may be refilled
+#pragma unroll
+    for (int g = 0; g < kCellGroups; ++g) {
+      const uint32_t i4 = g * kCellGroupCells + threadIdx.x * 4;
+      float2 cn0, cn1;
+      const uint32_t h0 = lstm_cell2(gi[g].x, gf[g].x, gg[g].x, go[g].x, make_float2(c[g].x, c[g].y), cn0, L);
+      const uint32_t h1 = lstm_cell2(gi[g].y, gf[g].y, gg[g].y, go[g].y, make_float2(c[g].z, c[g].w), cn1, L);
+      if (i4 < len) {
+        const uint64_t v = v0 + i4;
+        asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(c_next + v * 4),
+                     "f"(cn0.x), "f"(cn0.y), "f"(cn1.x), "f"(cn1.y) : "memory");
+        asm volatile("st.global.L1::no_allocate.v2.b32 [%0], {%1, %2};" ::"l"(h_next + v * 2), "r"(h0),
+                     "r"(h1) : "memory");
+      }
+    }
+  }
+}
+
+// Flat variant of the shared-memory-staged cell: one tile per CTA, grid =
+// tiles (the "flat" address-order launch that wins for the streaming maps),
+// no ring -- the CTAs resident on an SM are the pipeline.  Warp 0 issues the
+// tile's bulk copies (after an L2 prefetch of the same bytes issued before
+// griddepcontrol.wait, as k_map does) and every thread waits on one mbarrier.
+#ifndef KT_CELLF_GROUPS
+#define KT_CELLF_GROUPS 2
+#endif
+constexpr int kCellFGroups = KT_CELLF_GROUPS;
+constexpr uint32_t kCellFGroupCells = kThreads * 4;                       // 1024 cells per group
+constexpr uint32_t kCellFTile = kCellFGroupCells * kCellFGroups;
+constexpr uint32_t kCellFSmem = kCellFTile * 12 + 8;
+
+__device__ __forceinline__ void cell_tile_copies(const uint8_t *gates, const uint8_t *c_prev, uint64_t v0,
+                                                 uint32_t len, uint32_t hidden, uint32_t lane, uint32_t sdst,
+                                                 uint32_t bar, uint32_t tile_cells, bool prefetch) {
+  const uint64_t row0 = v0 / hidden;
+  const uint32_t nseg = (uint32_t)((v0 + len - 1) / hidden - row0 + 1);
+  for (uint32_t k = lane; k <= 4 * nseg; k += 32) {
+    const uint8_t *src;
+    uint32_t dst, bytes;
+    if (k == 4 * nseg) {
+      src = c_prev + v0 * 4;
+      dst = sdst + tile_cells * 8;
+      bytes = len * 4;
+    } else {
+      const uint32_t q = k & 3;
+      const uint64_t row = row0 + (k >> 2);
+      const uint64_t sb = row * hidden > v0 ? row * hidden : v0;
+      const uint64_t se = umin64((row + 1) * hidden, v0 + len);
+      src = gates + (row * 4 * hidden + (uint64_t)q * hidden + (sb - row * hidden)) * 2;
+      dst = sdst + q * tile_cells * 2 + (uint32_t)(sb - v0) * 2;
+      bytes = (uint32_t)(se - sb) * 2;
+    }
+    if (prefetch) prefetch_l2(src, bytes);
+    else bulk_g2s(dst, src, bytes, bar);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_lstm_cell_tile(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_t *h_next,
+                 uint64_t n, uint32_t hidden, const __grid_constant__ LutWords lut) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar = sbase + kCellFTile * 12;
+  const uint32_t lane = threadIdx.x & 31;
+  const LaneLut L = load_lane_lut(lut);
+  const uint64_t v0 = (uint64_t)blockIdx.x * kCellFTile;
+  const uint32_t len = (uint32_t)umin64(kCellFTile, n - v0);
+  if (threadIdx.x < 32) {
+    cell_tile_copies(gates, c_prev, v0, len, hidden, lane, sbase, bar, kCellFTile, true);   // L2 warm-up
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_expect_tx(bar, len * 12u);
+    __syncwarp();
+    cell_tile_copies(gates, c_prev, v0, len, hidden, lane, sbase, bar, kCellFTile, false);
+  }
+  __syncthreads();                 // the barrier is initialised before anyone waits on it
+  mbar_wait(bar, 0);
+#pragma unroll
+  for (int g = 0; g < kCellFGroups; ++g) {
+    const uint32_t i4 = g * kCellFGroupCells + threadIdx.x * 4;
+    const uint2 gi = *reinterpret_cast<const uint2 *>(smem + 0 * kCellFTile * 2 + i4 * 2);
+    const uint2 gf = *reinterpret_cast<const uint2 *>(smem + 1 * kCellFTile * 2 + i4 * 2);
+    const uint2 gg = *reinterpret_cast<const uint2 *>(smem + 2 * kCellFTile * 2 + i4 * 2);
+    const uint2 go = *reinterpret_cast<const uint2 *>(smem + 3 * kCellFTile * 2 + i4 * 2);
+    const float4 c = *reinterpret_cast<const float4 *>(smem + kCellFTile * 8 + i4 * 4);
+    float2 cn0, cn1;
+    const uint32_t h0 = lstm_cell2(gi.x, gf.x, gg.x, go.x, make_float2(c.x, c.y), cn0, L);
+    const uint32_t h1 = lstm_cell2(gi.y, gf.y, gg.y, go.y, make_float2(c.z, c.w), cn1, L);
+    if (i4 < len) {
+      const uint64_t v = v0 + i4;
+      asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(c_next + v * 4),
+                   "f"(cn0.x), "f"(cn0.y), "f"(cn1.x), "f"(cn1.y) : "memory");
+      asm volatile("st.global.L1::no_allocate.v2.b32 [%0], {%1, %2};" ::"l"(h_next + v * 2), "r"(h0),
+                   "r"(h1) : "memory");
+    }
+  }
 }
 
 // Fused LSTM cell, element fallback.
@@ -790,6 +1088,74 @@ cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *
                          reinterpret_cast<uintptr_t>(c_next) | reinterpret_cast<uintptr_t>(h_next)) %
                         kVecBytes) == 0;
   const uint64_t nvec = n / 16;
+  static const int which = [] {
+    // dev A/B: 0 = register-staged, 1 = persistent ring, 2 = flat one-tile CTAs
+    const char *e = getenv("KT_CELL_KERNEL");
+    return e ? atoi(e) : KT_CELL_DEFAULT;
+  }();
+  if (which == 2 && aligned && hidden % 16 == 0 && hidden >= kCellMinHidden && n > 0) {
+    static int attr_done[64];
+    if (li.device < 0 || li.device >= 64) return cudaErrorInvalidDevice;
+    if (!__atomic_load_n(&attr_done[li.device], __ATOMIC_ACQUIRE)) {
+      const cudaError_t ea = cudaFuncSetAttribute(k_lstm_cell_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)kCellFSmem);
+      if (ea != cudaSuccess) return ea;
+      __atomic_store_n(&attr_done[li.device], 1, __ATOMIC_RELEASE);
+    }
+    const uint64_t tiles = (n + kCellFTile - 1) / kCellFTile;
+    if (tiles >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)tiles);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kCellFSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_lstm_cell_tile, reinterpret_cast<const uint8_t *>(gates),
+                                             reinterpret_cast<const uint8_t *>(c_prev),
+                                             reinterpret_cast<uint8_t *>(c_next), reinterpret_cast<uint8_t *>(h_next),
+                                             (uint64_t)n, (uint32_t)hidden, lut);
+    count_launch();
+    return e;
+  }
+  if (which == 1 && aligned && hidden % 16 == 0 && hidden >= kCellMinHidden && n > 0) {
+    static int attr_done[64];   // per device: the limit is a per-context function attribute
+    if (li.device < 0 || li.device >= 64) return cudaErrorInvalidDevice;
+    if (!__atomic_load_n(&attr_done[li.device], __ATOMIC_ACQUIRE)) {
+      const cudaError_t ea = cudaFuncSetAttribute(k_lstm_cell_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)kCellSmem);
+      if (ea != cudaSuccess) return ea;
+      __atomic_store_n(&attr_done[li.device], 1, __ATOMIC_RELEASE);
+    }
+    static const int bps = [] {
+      int b = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_lstm_cell_tma, kCellThreads, kCellSmem) !=
+              cudaSuccess || b < 1)
+        b = 1;
+      return b;
+    }();
+    const uint64_t tiles = (n + kCellTile - 1) / kCellTile;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)li.sm_count * bps));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kCellThreads);
+    cfg.dynamicSmemBytes = kCellSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_lstm_cell_tma, reinterpret_cast<const uint8_t *>(gates),
+                                             reinterpret_cast<const uint8_t *>(c_prev),
+                                             reinterpret_cast<uint8_t *>(c_next), reinterpret_cast<uint8_t *>(h_next),
+                                             (uint64_t)n, (uint32_t)hidden, lut);
+    count_launch();
+    return e;
+  }
   if (aligned && hidden % 16 == 0 && nvec < (1ull << 31)) {
     const uint64_t nwarps = (nvec + 31) / 32;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, (nwarps + kWarps - 1) / kWarps);

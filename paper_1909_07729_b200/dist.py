@@ -66,6 +66,22 @@ def sum_over_ranks(v: float, device=None) -> float:
     return _reduce_scalar(v, dist.ReduceOp.SUM, device)
 
 
+def gather_over_ranks(values, device=None) -> list:
+    """Every rank's list of floats (same length on all ranks), in rank order;
+    [values] when not distributed.  Timing / bookkeeping plumbing only."""
+    vals = [float(v) for v in values]
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [vals]
+    if dist.get_backend() != "nccl":
+        device = torch.device("cpu")
+    elif device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    return [[float(v) for v in p.cpu()] for p in parts]
+
+
 def barrier():
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.barrier()

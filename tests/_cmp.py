@@ -26,14 +26,23 @@ def ulp_dist(a, b, bits):
     return d
 
 
-def assert_bitexact(got, want, bits, nan_by_class=False, ctx=""):
+def _iszero(w, bits):
+    w = np.asarray(w).astype(np.int64)
+    return (w & ((1 << (bits - 1)) - 1)) == 0
+
+
+def assert_bitexact(got, want, bits, nan_by_class=False, zero_by_value=False, ctx=""):
+    """Bit-for-bit equality; nan_by_class: any NaN matches any NaN (GPU
+    arithmetic canonicalises payloads); zero_by_value: +0 matches -0 (reading
+    A21: the sign of a zero result of the derived ops is not specified)."""
     got = np.asarray(got).reshape(-1)
     want = np.asarray(want).reshape(-1)
     assert got.shape == want.shape
+    bad = got != want
     if nan_by_class:
-        bad = (got != want) & ~(_isnan(got, bits) & _isnan(want, bits))
-    else:
-        bad = got != want
+        bad &= ~(_isnan(got, bits) & _isnan(want, bits))
+    if zero_by_value:
+        bad &= ~(_iszero(got, bits) & _iszero(want, bits))
     if bad.any():
         i = np.flatnonzero(bad)[:8]
         raise AssertionError(f"{ctx}: {bad.sum()} mismatches, first at {i.tolist()}: "

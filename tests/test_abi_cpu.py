@@ -569,3 +569,31 @@ def test_lut_f32_validation_matches_the_rule(kt, data):
         assert e.status == kt.KT_ERR_LUT
         accepted = False
     assert accepted == ok, (E, r, b)
+
+
+def test_binding_rejects_unsupported_dtypes_and_strided_host_buffers(kt):
+    """the generic entry points accept only bfloat16 and
+    float32 (a float16 / int16 tensor used to go down the F32 path and read or
+    write numel*4 bytes of a 2-byte buffer), and apply_host needs contiguous
+    host tensors (the C ABI sees one pointer and an element count)."""
+    import torch
+    for dt in (torch.float16, torch.int16, torch.float64, torch.int32):
+        x = torch.zeros(64, dtype=dt)
+        with pytest.raises(TypeError, match="unsupported dtype"):
+            kt.apply("tanh", x)
+        with pytest.raises(TypeError, match="unsupported dtype"):
+            kt.apply_host("tanh", x, torch.zeros_like(x), x)
+    xs = torch.zeros(128, dtype=torch.bfloat16)[::2]
+    with pytest.raises(ValueError, match="contiguous"):
+        kt.apply_host("tanh", xs, torch.zeros(64, dtype=torch.bfloat16), xs)
+    with pytest.raises(ValueError, match="must match"):
+        kt.apply_host("tanh", torch.zeros(64, dtype=torch.bfloat16), torch.zeros(64), xs)
+
+
+def test_binding_output_checks_cpu_side(kt):
+    """caller-supplied outputs are validated before any
+    pointer reaches the C ABI (_check_out): wrong dtype, size, device or layout."""
+    import torch
+    t = torch.zeros(16, dtype=torch.float32)
+    with pytest.raises(TypeError, match="CUDA tensor"):
+        kt._check_out(t, "c_next", torch.float32, 16, torch.device("cuda", 0))

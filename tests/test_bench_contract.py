@@ -26,7 +26,8 @@ def test_reference_arm_contract():
     d = _run(["--impl", "reference", "--steps", "1", "--warmup", "3"], 600)
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
     assert d["unit"] == "Gelem/s" and d["higher_is_better"] is True and d["value"] > 0
-    assert d["warmup"] >= 3 and d["config"]["workload"] == "c2_bf16_2p24"
+    assert d["warmup"] >= 3 and d["config"]["workload"] == "c5_ffn_2p30" and d["dtype"] == "bf16"
+    assert d["config"]["elements_per_gpu"] == 1 << 30 and d["config"]["call"] == "kgelu_bf16"
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": "Gelem/s", "h2d_bytes_per_step": 0,
@@ -41,13 +42,50 @@ def test_main_arm_contract():
     d = _run(["--steps", "20", "--warmup", "3", "--no-extra", "--no-cpu"], 900)
     assert BASE_KEYS <= set(d) and "impl" not in d
     assert d["n_gpus"] == 1 and d["steps"] == 20 and d["warmup"] == 3 and d["scaling"] == "weak"
-    assert d["data"] == "synthetic" and d["dtype"] == "u16" and d["vs_baseline"] is None
-    assert d["config"]["workload"] == "c2_bf16_2p24" and d["config"]["l2"]
+    assert d["data"] == "synthetic" and d["dtype"] == "bf16" and d["vs_baseline"] is None
+    assert d["config"]["workload"] == "c5_ffn_2p30" and d["timing"]["l2"]
     rf = d["roofline"]
     assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and rf["peak"] > 0
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3 and rf["traffic"] > 0
+    assert rf["algorithmic_bytes_per_launch"] == 4 << 30
     e = d["e2e"]
-    assert e["value"] > 0 and e["h2d_bytes_per_step"] == e["d2h_bytes_per_step"] == 2 << 24
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == e["d2h_bytes_per_step"] == 2 << 30
     assert d["gpu_launches"] == 20
     c = d["clocks"]
     assert c["sm_max_mhz"] > 0 and isinstance(c["reasons"], list)
+    assert d["per_rank"] == [{"rank": 0, "device": 0, "ms_per_step": d["per_rank"][0]["ms_per_step"],
+                              "checked": 65538, "mismatches": 0}] or d["cpu_baseline"] is None
+
+
+def test_reference_arm_same_config_as_main_arm():
+    """Both arms print the identical `config` object (the driver compares them)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    ref = _run(["--impl", "reference", "--steps", "1", "--warmup", "3"], 600)
+    assert ref["config"] == bench.head_config("c5_ffn_2p30", "kgelu_bf16", 1)
+
+
+def test_multirank_path_under_torchrun_stub():
+    """bench.py's N > 1 path end to end on CPU (gloo, world size 2, --stub):
+    device selection (local_rank % devices), barriers, per-rank windows, the
+    max over ranks, the per-rank check and one JSON line from rank 0 only."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "5", "--warmup", "3", "--stub"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["stub"] is True and d["n_gpus"] == 2 and d["steps"] == 5 and d["warmup"] == 3
+    pr = d["per_rank"]
+    assert [p["rank"] for p in pr] == [0, 1] and [p["device"] for p in pr] == [0, 1]
+    assert all(p["mismatches"] == 0 and p["checked"] == (1 << 16) + 2 for p in pr)
+    # value = all ranks' elements / the slowest rank's (median) window
+    assert max(p["ms_per_step"] for p in pr) <= d["ms_per_step"] * 1.5 + 1e-3
+    assert abs(d["value"] - 2 * (1 << 16) / (d["ms_per_step"] / 1e3) / 1e9) <= 1e-3 * d["value"] + 1e-3

@@ -47,6 +47,7 @@ def _worker(rank, world, port, n_list, q):
     # aggregation: rank r "took" (r + 1) ms on (r + 1) * 1000 elements
     tot, ms, eps = kd.aggregate_throughput((r + 1) * 1000, float(r + 1))
     out["agg"] = (tot, ms, eps)
+    out["gather"] = kd.gather_over_ranks([r, 10.0 * r + 0.5])
     kd.barrier()
     q.put((r, out))
     dist.destroy_process_group()
@@ -71,3 +72,4 @@ def test_gloo_shards_and_aggregation(world):
     for r in range(world):
         tot, ms, eps = res[r]["agg"]
         assert tot == 3000 and ms == 2.0 and abs(eps - 1.5e6) < 1e-6
+        assert res[r]["gather"] == [[float(k), 10.0 * k + 0.5] for k in range(world)]

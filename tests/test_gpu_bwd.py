@@ -1,18 +1,32 @@
 """GPU parity of the backward kernels (reading R-BWD) against the oracle.
 
-Tolerance: tanh/sigmoid backward <= 1 ulp of the format (two fp32 roundings
-then one rounding to the format, against the oracle's one rounding of the
-exact value).  Swish/GELU backward additionally allow the fp32 evaluation
-error of the sum (1+t)/2 + ... when it cancels: |dx - oracle| <= 1 ulp +
-2^-20 |dy| S, with S an upper bound on the magnitude of the summed terms.
-NaN compared by class."""
+Tolerance, derived from the kernels' fp32 evaluation (kt_device.cuh
+bwd_f32 / bwd_factor2) against the oracle's one rounding of the exact
+binary64 value, u = 2^-24:
+
+    |dx - oracle| <= ulp_fmt(oracle) + c u |dy| S
+
+  tanh     g = fma(-y, y, 1)              one rounding of g, one of dy g: c = 3, S = 1
+  sigmoid  g = fma(-s, s, s)              the same:                           c = 3, S = 1
+  swish    g = fma(x/4, RN(1 - t^2), RN((1 + t)/2))                           c = 4, S = 1 + |x|/4
+  gelu     g = fma(RN(x/2 RN(1 - t^2)), RN(C3 RN(x^2) + C0), RN((1 + t)/2))   c = 8,
+           S = 1 + 0.8 |x| (1 + 0.134 x^2)  (>= |(1+t)/2| + |x/2 (1 - t^2) u'(x)|)
+
+(relative errors: 1 - t^2 and (1+t)/2 one rounding each, x/2 (1 - t^2) two,
+u' = C3 x^2 + C0 three (C0, C3 themselves RN32 of their binary64 values), the
+final fma one, dy g one: |g_hat - g| <= (c - 1) u S and |dy g_hat rounded -
+dy g| <= c u |dy| S; the last rounding to the format costs the ulp term).
+The c u |dy| S term only matters where g cancels ((1+t)/2 against the
+negative x-term); elsewhere the bound is ~1 ulp.  Each check also returns
+the largest measured fraction of the c u |dy| S allowance actually used,
+printed by the tests.  NaN compared by class."""
 import numpy as np
 import pytest
 import torch
 
 import oracle as O
 import workloads as WL
-from _cmp import _isnan, ulp_dist
+from _cmp import _isnan
 
 pytestmark = pytest.mark.gpu
 
@@ -39,22 +53,43 @@ def _vals(bits, nbits):
     return np.asarray(bits, np.uint32).view(np.float32).astype(np.float64)
 
 
+BWD_C = {"tanh": 3, "sigmoid": 3, "swish": 4, "gelu": 8}
+
+
+def _spacing(v, nbits):
+    """ulp of the format at |v| (the upward spacing; min subnormal spacing at 0)."""
+    a = np.abs(v).astype(np.float32)
+    sp = np.spacing(a).astype(np.float64)
+    if nbits == 16:
+        sp = np.maximum(sp * 65536.0, 2.0 ** -133)
+    return sp
+
+
 def check_bwd(op, nbits, a, dy, got, want):
-    d = ulp_dist(got, want, nbits)
-    if op in ("tanh", "sigmoid"):
-        ok = d <= 1
-    else:
-        x = _vals(a, nbits)
-        g = _vals(dy, nbits)
-        S = (1 + np.abs(x) / 4) if op == "swish" else (1 + np.abs(x) * 0.8 * (1 + 0.134 * x * x))
-        with np.errstate(invalid="ignore", over="ignore"):
-            diff = np.abs(_vals(got, nbits) - _vals(want, nbits))
-            ok = (d <= 1) | (diff <= 2.0 ** -20 * np.abs(g) * S)
+    """Assert the derived bound of the module docstring; return the largest
+    fraction of the c u |dy| S allowance used (0 when within the ulp term)."""
+    x = _vals(a, nbits)
+    g = _vals(dy, nbits)
+    with np.errstate(invalid="ignore", over="ignore"):
+        if op in ("tanh", "sigmoid"):
+            S = np.ones_like(x)
+        elif op == "swish":
+            S = 1 + np.abs(x) / 4
+        else:
+            S = 1 + np.abs(x) * 0.8 * (1 + 0.134 * x * x)
+        gv, wv = _vals(got, nbits), _vals(want, nbits)
+        allow = BWD_C[op] * 2.0 ** -24 * np.abs(g) * S
+        excess = np.abs(gv - wv) - _spacing(wv, nbits)
+        finite = np.isfinite(wv) & np.isfinite(gv)
+        ok = np.where(finite, excess <= allow, got == want)
     nan = _isnan(got, nbits) & _isnan(want, nbits)
     bad = ~(ok | nan)
     assert not bad.any(), (op, nbits, int(bad.sum()), [hex(int(v)) for v in a[bad][:4]],
                            [hex(int(v)) for v in got[bad][:4]], [hex(int(v)) for v in want[bad][:4]])
-    return int(d[~nan].max()) if (~nan).any() else 0
+    m = finite & ~nan & (allow > 0)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        frac = np.where(m & (excess > 0), excess / np.where(m, allow, 1.0), 0.0)
+    return float(frac.max()) if frac.size else 0.0
 
 
 def _domain(op, a_vals):
@@ -76,8 +111,8 @@ def test_bwd_bf16_all_patterns(kt, op):
     dy = torch.randn(a.numel(), device="cuda", generator=g).to(torch.bfloat16)
     dx = getattr(kt, f"k{op}_bwd_bf16")(a, dy)
     want = O.bwd_bf16(op, u16(a), u16(dy))
-    worst = check_bwd(op, 16, u16(a), u16(dy), u16(dx), want)
-    print(f"{op} bwd bf16 max ulp {worst}")
+    used = check_bwd(op, 16, u16(a), u16(dy), u16(dx), want)
+    print(f"{op} bwd bf16: largest fraction of the derived c u |dy| S allowance used: {used:.3g}")
 
 
 @pytest.mark.parametrize("op", ["tanh", "sigmoid", "swish", "gelu"])
@@ -93,7 +128,8 @@ def test_bwd_f32_patterns(kt, op):
     dy = torch.from_numpy(dy_bits.view(np.int32)).cuda().view(torch.float32)
     dx = getattr(kt, f"k{op}_bwd_f32")(a, dy)
     want = O.bwd_f32(op, a_bits, dy_bits)
-    check_bwd(op, 32, a_bits, dy_bits, u32(dx), want)
+    used = check_bwd(op, 32, a_bits, dy_bits, u32(dx), want)
+    print(f"{op} bwd f32: largest fraction of the derived c u |dy| S allowance used: {used:.3g}")
 
 
 @pytest.mark.parametrize("n,off", [(1, 0), (17, 1), (1000, 3), (65537, 0), (100003, 5)])

@@ -83,8 +83,10 @@ def test_kgelu_swish_bf16_past_2p32(kt):
     g, s = kt.kgelu_swish_bf16(x)
     idx = sample_idx(n)
     xb = bits16(take(x, idx))
-    assert_ulp(bits16(take(g, idx)), O.map_bf16("gelu", xb), 16, 1, ctx="dual gelu n > 2^32")
-    assert_ulp(bits16(take(s, idx)), O.map_bf16("swish", xb), 16, 1, ctx="dual swish n > 2^32")
+    assert_bitexact(bits16(take(g, idx)), O.map_bf16("gelu", xb), 16, nan_by_class=True,
+                    zero_by_value=True, ctx="dual gelu n > 2^32")
+    assert_bitexact(bits16(take(s, idx)), O.map_bf16("swish", xb), 16, nan_by_class=True,
+                    zero_by_value=True, ctx="dual swish n > 2^32")
 
 
 def test_kgelu_bwd_bf16_past_2p32(kt):
