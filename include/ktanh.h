@@ -168,13 +168,19 @@ KT_API kt_status ktanh_f32_via_bf16(const float *x, float *y, size_t n, kt_lut l
 KT_API kt_status ksigmoid_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream);
 KT_API kt_status ksigmoid_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream);
 
-/* K-Swish = x K-Sigmoid(x) = hx (1 + K-TanH(RN(hx))), hx = x/2. */
+/* K-Swish = x K-Sigmoid(x) = hx (1 + K-TanH(RN(hx))), hx = x/2.
+ * The outer step is the exact value hx (1 + t) rounded ONCE to the format
+ * (reading R-DERIVED), also where x/2 itself is not representable (|x| <
+ * 2^-125 with an odd last bit): there the exact t-term decides the tie.
+ * The sign of a zero result is not specified (reading A21). */
 KT_API kt_status kswish_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream);
 KT_API kt_status kswish_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream);
 
 /* K-GELU = x/2 (1 + K-TanH(u)), u = x fma(C1, x^2, C0) in fp32 with
  * C0 = f32(sqrt(2/pi)), C1 = f32(sqrt(2/pi) 0.044715) (PAPER.md:69-71,
- * reading R-GELU-ARG); for BF16, u is rounded to BF16 before K-TanH. */
+ * reading R-GELU-ARG); for BF16, u is rounded to BF16 before K-TanH.  The
+ * outer step x/2 (1 + t) is rounded once from its exact value, as for
+ * kswish_* (reading R-DERIVED). */
 KT_API kt_status kgelu_bf16(const uint16_t *x, uint16_t *y, size_t n, kt_lut lut, void *stream);
 KT_API kt_status kgelu_f32(const float *x, float *y, size_t n, kt_lut lut, void *stream);
 

@@ -513,16 +513,17 @@ __global__ void __launch_bounds__(kThreads, KT_CELL_MINB)
 __global__ void __launch_bounds__(kThreads)   // (kThreads, 1) lets ptxas take > 64 regs: slower
 #endif
 k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_t *h_next,
-            uint32_t nvec, uint32_t vpr, uint32_t hidden, uint32_t pf_stride,
+            uint32_t nvec, uint32_t vpr, uint32_t hidden, uint32_t pf_blocks,
             const __grid_constant__ LutWords lut) {
   const LaneLut L = load_lane_lut(lut);
-  pdl_enter();
-  // Optional L2 prefetch of the NEXT wave's data (KT_CELL_PF=k: the
-  // counterpart warp k resident waves later).  Measured slower on config 4
-  // (26.3 vs 20.8 us: the prefetched lines compete with the current wave's
-  // reads and writes in L2), so off by default.
-  if (pf_stride != 0 && (threadIdx.x & 31) < 5) {
-    const uint32_t v2 = ((blockIdx.x + pf_stride) * kWarps + (threadIdx.x >> 5)) * 32;
+  // First resident wave (blockIdx.x < pf_blocks): lanes 0-4 prefetch this
+  // warp's own 4 gate segments and c segment into L2 BEFORE
+  // griddepcontrol.wait, so under PDL the DRAM reads start while the previous
+  // launch drains (k_map does the same).  A prefetch has no architectural
+  // effect on the values later loads see.  (Round 1 tried prefetching the NEXT
+  // wave's data instead: slower, 26.3 vs 20.8 us.)
+  if (blockIdx.x < pf_blocks && (threadIdx.x & 31) < 5) {
+    const uint32_t v2 = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32;
     if (v2 < nvec) {
       const uint32_t row2 = v2 / vpr, j2 = v2 - row2 * vpr;
       const uint32_t cnt = min(min(32u, nvec - v2), vpr - j2);
@@ -534,6 +535,7 @@ k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_
         prefetch_l2(c_prev + ((size_t)row2 * hidden + (size_t)j2 * 16) * 4, cnt * 64);
     }
   }
+  pdl_enter();
   const uint32_t v = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32 + (threadIdx.x & 31);
   const bool on = v < nvec;
   const uint32_t row = on ? v / vpr : 0, j16 = on ? v - row * vpr : 0;
@@ -584,10 +586,10 @@ k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_
 // c_next may alias c_prev: a tile's c is in shared memory before any c' of
 // that tile is written, and other tiles' c ranges are disjoint.
 #ifndef KT_CELL_WARPS
-#define KT_CELL_WARPS 8
+#define KT_CELL_WARPS 16
 #endif
 #ifndef KT_CELL_GROUPS
-#define KT_CELL_GROUPS 2
+#define KT_CELL_GROUPS 1
 #endif
 #ifndef KT_CELL_STAGES
 #define KT_CELL_STAGES 4
@@ -603,7 +605,7 @@ constexpr uint32_t kCellStageBytes = kCellTile * (4 * 2 + 4);           // gates
 constexpr uint32_t kCellSmem = kCellStages * kCellStageBytes + 2 * kCellStages * 8;
 constexpr uint32_t kCellMinHidden = 256;   // tiles touch few rows: few, large copies
 #ifndef KT_CELL_DEFAULT
-#define KT_CELL_DEFAULT 2
+#define KT_CELL_DEFAULT 0
 #endif
 
 __global__ void __launch_bounds__(kCellThreads)
@@ -693,91 +695,6 @@ k_lstm_cell_tma(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, ui
         asm volatile("st.global.L1::no_allocate.v2.b32 [%0], {%1, %2};" ::"l"(h_next + v * 2), "r"(h0),
                      "r"(h1) : "memory");
       }
-    }
-  }
-}
-
-// Flat variant of the shared-memory-staged cell: one tile per CTA, grid =
-// tiles (the "flat" address-order launch that wins for the streaming maps),
-// no ring -- the CTAs resident on an SM are the pipeline.  Warp 0 issues the
-// tile's bulk copies (after an L2 prefetch of the same bytes issued before
-// griddepcontrol.wait, as k_map does) and every thread waits on one mbarrier.
-#ifndef KT_CELLF_GROUPS
-#define KT_CELLF_GROUPS 2
-#endif
-constexpr int kCellFGroups = KT_CELLF_GROUPS;
-constexpr uint32_t kCellFGroupCells = kThreads * 4;                       // 1024 cells per group
-constexpr uint32_t kCellFTile = kCellFGroupCells * kCellFGroups;
-constexpr uint32_t kCellFSmem = kCellFTile * 12 + 8;
-
-__device__ __forceinline__ void cell_tile_copies(const uint8_t *gates, const uint8_t *c_prev, uint64_t v0,
-                                                 uint32_t len, uint32_t hidden, uint32_t lane, uint32_t sdst,
-                                                 uint32_t bar, uint32_t tile_cells, bool prefetch) {
-  const uint64_t row0 = v0 / hidden;
-  const uint32_t nseg = (uint32_t)((v0 + len - 1) / hidden - row0 + 1);
-  for (uint32_t k = lane; k <= 4 * nseg; k += 32) {
-    const uint8_t *src;
-    uint32_t dst, bytes;
-    if (k == 4 * nseg) {
-      src = c_prev + v0 * 4;
-      dst = sdst + tile_cells * 8;
-      bytes = len * 4;
-    } else {
-      const uint32_t q = k & 3;
-      const uint64_t row = row0 + (k >> 2);
-      const uint64_t sb = row * hidden > v0 ? row * hidden : v0;
-      const uint64_t se = umin64((row + 1) * hidden, v0 + len);
-      src = gates + (row * 4 * hidden + (uint64_t)q * hidden + (sb - row * hidden)) * 2;
-      dst = sdst + q * tile_cells * 2 + (uint32_t)(sb - v0) * 2;
-      bytes = (uint32_t)(se - sb) * 2;
-    }
-    if (prefetch) prefetch_l2(src, bytes);
-    else bulk_g2s(dst, src, bytes, bar);
-  }
-}
-
-__global__ void __launch_bounds__(kThreads)
-k_lstm_cell_tile(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_t *h_next,
-                 uint64_t n, uint32_t hidden, const __grid_constant__ LutWords lut) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar = sbase + kCellFTile * 12;
-  const uint32_t lane = threadIdx.x & 31;
-  const LaneLut L = load_lane_lut(lut);
-  const uint64_t v0 = (uint64_t)blockIdx.x * kCellFTile;
-  const uint32_t len = (uint32_t)umin64(kCellFTile, n - v0);
-  if (threadIdx.x < 32) {
-    cell_tile_copies(gates, c_prev, v0, len, hidden, lane, sbase, bar, kCellFTile, true);   // L2 warm-up
-    if (lane == 0) {
-      mbar_init(bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) mbar_expect_tx(bar, len * 12u);
-    __syncwarp();
-    cell_tile_copies(gates, c_prev, v0, len, hidden, lane, sbase, bar, kCellFTile, false);
-  }
-  __syncthreads();                 // the barrier is initialised before anyone waits on it
-  mbar_wait(bar, 0);
-#pragma unroll
-  for (int g = 0; g < kCellFGroups; ++g) {
-    const uint32_t i4 = g * kCellFGroupCells + threadIdx.x * 4;
-    const uint2 gi = *reinterpret_cast<const uint2 *>(smem + 0 * kCellFTile * 2 + i4 * 2);
-    const uint2 gf = *reinterpret_cast<const uint2 *>(smem + 1 * kCellFTile * 2 + i4 * 2);
-    const uint2 gg = *reinterpret_cast<const uint2 *>(smem + 2 * kCellFTile * 2 + i4 * 2);
-    const uint2 go = *reinterpret_cast<const uint2 *>(smem + 3 * kCellFTile * 2 + i4 * 2);
-    const float4 c = *reinterpret_cast<const float4 *>(smem + kCellFTile * 8 + i4 * 4);
-    float2 cn0, cn1;
-    const uint32_t h0 = lstm_cell2(gi.x, gf.x, gg.x, go.x, make_float2(c.x, c.y), cn0, L);
-    const uint32_t h1 = lstm_cell2(gi.y, gf.y, gg.y, go.y, make_float2(c.z, c.w), cn1, L);
-    if (i4 < len) {
-      const uint64_t v = v0 + i4;
-      asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(c_next + v * 4),
-                   "f"(cn0.x), "f"(cn0.y), "f"(cn1.x), "f"(cn1.y) : "memory");
-      asm volatile("st.global.L1::no_allocate.v2.b32 [%0], {%1, %2};" ::"l"(h_next + v * 2), "r"(h0),
-                   "r"(h1) : "memory");
     }
   }
 }
@@ -1089,38 +1006,11 @@ cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *
                         kVecBytes) == 0;
   const uint64_t nvec = n / 16;
   static const int which = [] {
-    // dev A/B: 0 = register-staged, 1 = persistent ring, 2 = flat one-tile CTAs
+    // dev A/B: 0 = register-staged (default, measured fastest), 1 = persistent
+    // shared-memory ring (profiles/cell_variants_r02.txt)
     const char *e = getenv("KT_CELL_KERNEL");
     return e ? atoi(e) : KT_CELL_DEFAULT;
   }();
-  if (which == 2 && aligned && hidden % 16 == 0 && hidden >= kCellMinHidden && n > 0) {
-    static int attr_done[64];
-    if (li.device < 0 || li.device >= 64) return cudaErrorInvalidDevice;
-    if (!__atomic_load_n(&attr_done[li.device], __ATOMIC_ACQUIRE)) {
-      const cudaError_t ea = cudaFuncSetAttribute(k_lstm_cell_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)kCellFSmem);
-      if (ea != cudaSuccess) return ea;
-      __atomic_store_n(&attr_done[li.device], 1, __ATOMIC_RELEASE);
-    }
-    const uint64_t tiles = (n + kCellFTile - 1) / kCellFTile;
-    if (tiles >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)tiles);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kCellFSmem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_lstm_cell_tile, reinterpret_cast<const uint8_t *>(gates),
-                                             reinterpret_cast<const uint8_t *>(c_prev),
-                                             reinterpret_cast<uint8_t *>(c_next), reinterpret_cast<uint8_t *>(h_next),
-                                             (uint64_t)n, (uint32_t)hidden, lut);
-    count_launch();
-    return e;
-  }
   if (which == 1 && aligned && hidden % 16 == 0 && hidden >= kCellMinHidden && n > 0) {
     static int attr_done[64];   // per device: the limit is a per-context function attribute
     if (li.device < 0 || li.device >= 64) return cudaErrorInvalidDevice;
@@ -1161,14 +1051,14 @@ cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *
     const unsigned grid = (unsigned)std::max<uint64_t>(1, (nwarps + kWarps - 1) / kWarps);
     static const int bps = resident_blocks(k_lstm_cell);
     static const int pf_on = [] {
-      const char *e = getenv("KT_CELL_PF");
-      return e ? atoi(e) : 0;
+      const char *e = getenv("KT_CELL_PF");     // dev A/B: 0 = no first-wave L2 prefetch
+      return e ? atoi(e) : 1;
     }();
-    const uint32_t pf_stride = pf_on > 0 ? (uint32_t)(li.sm_count * bps * pf_on) : 0u;
+    const uint32_t pf_blocks = (pf_on && prefetch_enabled()) ? (uint32_t)(li.sm_count * bps) : 0u;
     return launch(k_lstm_cell, grid, s, reinterpret_cast<const uint8_t *>(gates),
                   reinterpret_cast<const uint8_t *>(c_prev), reinterpret_cast<uint8_t *>(c_next),
                   reinterpret_cast<uint8_t *>(h_next), (uint32_t)nvec, (uint32_t)(hidden / 16),
-                  (uint32_t)hidden, pf_stride, lut);
+                  (uint32_t)hidden, pf_blocks, lut);
   }
   static const int bps = resident_blocks(k_lstm_cell_elem);
   const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);

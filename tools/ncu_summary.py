@@ -95,7 +95,7 @@ if __name__ == "__main__":
             alg[tag] = 0
         elif "gelu" in tag or "swish" in tag:
             alg[tag] = 4 << 30
-        elif "lstm_cell" in tag:
+        elif "lstm_cell" in tag or "cell" in tag:
             alg[tag] = 18 * 128 * 50 * 1024
         elif "gelu_bwd" in tag:
             alg[tag] = 6 << 30
