@@ -40,6 +40,29 @@ constexpr int kUnroll = KT_UNROLL;            // 32-B vectors per lane per chunk
 constexpr int kVecBytes = 32;
 constexpr int kChunkVecs = 32 * kUnroll;      // vectors per warp-chunk
 
+// Vectors per lane per chunk, per kernel (measured on B200 under the power
+// cap, profiles/unroll_r02.txt): the ALU-heavier maps keep more loads in
+// flight per warp -- K-GELU BF16 and every F32 map 4 (+6% / +11% over 2);
+// K-TanH / K-Sigmoid / K-Swish BF16 and the LSTM gates 2; the fused
+// K-GELU + K-Swish pass (40 registers, 6 CTAs/SM) 1 (+6% over 2).
+#ifndef KT_UNROLL_GELU
+#define KT_UNROLL_GELU 4
+#endif
+#ifndef KT_UNROLL_F32
+#define KT_UNROLL_F32 4
+#endif
+#ifndef KT_UNROLL_DUAL
+#define KT_UNROLL_DUAL 1
+#endif
+template <int OP, int FMT>
+__host__ __device__ constexpr int map_unroll() {
+  return FMT == FMT_F32 ? KT_UNROLL_F32 : (OP == OP_GELU ? KT_UNROLL_GELU : kUnroll);
+}
+template <int FMT>
+__host__ __device__ constexpr int dual_unroll() {
+  return FMT == FMT_BF16 ? KT_UNROLL_DUAL : kUnroll;
+}
+
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
@@ -100,10 +123,10 @@ __device__ __forceinline__ void scalar_span(const uint8_t *xp, uint8_t *yp, uint
 // BF16 pairs with |x| < 2^-125 from the closed form.  Out of line and word by
 // word so that it costs the streaming kernels no registers; plain (coherent)
 // loads see the lane's own preceding stores.  Out-of-place calls only.
-template <int OP>
+template <int OP, int U>
 __device__ __noinline__ void tie_fixup(const uint8_t *xb, uint8_t *yb, uint64_t base, uint64_t nvec) {
 #pragma unroll 1
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     if (i >= nvec) continue;
     const uint32_t *xs = reinterpret_cast<const uint32_t *>(xb + i * kVecBytes);
@@ -116,10 +139,11 @@ __device__ __noinline__ void tie_fixup(const uint8_t *xb, uint8_t *yb, uint64_t 
   }
 }
 
+template <int U>
 __device__ __noinline__ void tie_fixup_dual(const uint8_t *xb, uint8_t *gb, uint8_t *sb, uint64_t base,
                                             uint64_t nvec) {
 #pragma unroll 1
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     if (i >= nvec) continue;
     const uint32_t *xs = reinterpret_cast<const uint32_t *>(xb + i * kVecBytes);
@@ -140,10 +164,10 @@ __device__ __noinline__ void tie_fixup_dual(const uint8_t *xb, uint8_t *gb, uint
 // elements precede the first 32-B boundary of x (and of y: same offset mod
 // 32, checked on the host); nvec vectors follow; then `tail` elements.
 #ifdef KT_MAP_MINB
-template <int OP, int FMT, bool NC, bool PF>
+template <int OP, int FMT, bool NC, bool PF, int U>
 __global__ void __launch_bounds__(kThreads, KT_MAP_MINB)
 #else
-template <int OP, int FMT, bool NC, bool PF>
+template <int OP, int FMT, bool NC, bool PF, int U>
 __global__ void __launch_bounds__(kThreads)
 #endif
 k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
@@ -158,17 +182,17 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
   if (PF && blockIdx.x < pf_blocks && lane < pf_depth) {
     // lane d prefetches the chunk of the warp d resident waves later
     const uint64_t cc = c + (uint64_t)lane * pf_blocks * kWarps;
-    if (cc * kChunkVecs < nvec) {
-      const uint64_t left = nvec - cc * kChunkVecs;
-      prefetch_l2(xb + cc * kChunkVecs * kVecBytes,
-                  (uint32_t)((left < kChunkVecs ? left : kChunkVecs) * kVecBytes));
+    if (cc * (32 * U) < nvec) {
+      const uint64_t left = nvec - cc * (32 * U);
+      prefetch_l2(xb + cc * (32 * U) * kVecBytes,
+                  (uint32_t)((left < (32 * U) ? left : (32 * U)) * kVecBytes));
     }
   }
   pdl_enter();
-  const uint64_t base = c * kChunkVecs + lane;
-  uint32_t v[kUnroll][8];
+  const uint64_t base = c * (32 * U) + lane;
+  uint32_t v[U][8];
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     ld256<NC>(xb + i * kVecBytes, v[u], i < nvec);
   }
@@ -178,7 +202,7 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
   constexpr bool kScreen = needs_tie_screen<OP, FMT>() && NC;
   uint32_t kmin = 0xFFFFFFFFu;
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
 #pragma unroll
     for (int j = 0; j < 8; j += 2) {
       if (kScreen) {
@@ -197,12 +221,12 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
     }
   }
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     st256(yb + i * kVecBytes, v[u], i < nvec);
   }
   if (kScreen && __any_sync(0xffffffffu, tie_possible(kmin)))
-    tie_fixup<OP>(xb, yb, base, nvec);   // rare: an |argument| < 2^-125 (or a zero) in the chunk
+    tie_fixup<OP, U>(xb, yb, base, nvec);   // rare: an |argument| < 2^-125 (or a zero) in the chunk
   if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
     scalar_span<OP, FMT>(x, y, head, L);
     const size_t toff = ((size_t)head + (size_t)nvec * (kVecBytes / es)) * es;
@@ -307,7 +331,7 @@ __device__ __forceinline__ void dual_span(const uint8_t *xp, uint8_t *gp, uint8_
 #ifndef KT_BWD_MINB
 #define KT_BWD_MINB 5    // 48 regs: 5 CTAs/SM (+17% on config 5 backward)
 #endif
-template <int FMT, bool NC>
+template <int FMT, bool NC, int U>
 __global__ void __launch_bounds__(kThreads, KT_DUAL_MINB)
 k_dual(const uint8_t *x, uint8_t *yg, uint8_t *ys, uint32_t head, uint64_t nvec, uint32_t tail,
        uint32_t pf_blocks, const __grid_constant__ LutWords lut) {
@@ -316,23 +340,23 @@ k_dual(const uint8_t *x, uint8_t *yg, uint8_t *ys, uint32_t head, uint64_t nvec,
   const uint32_t lane = threadIdx.x & 31;
   const size_t hb = (size_t)head * es;
   const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (NC && blockIdx.x < pf_blocks && lane == 0 && c * kChunkVecs < nvec) {
-    const uint64_t left = nvec - c * kChunkVecs;
-    prefetch_l2(x + hb + c * kChunkVecs * kVecBytes,
-                (uint32_t)((left < kChunkVecs ? left : kChunkVecs) * kVecBytes));
+  if (NC && blockIdx.x < pf_blocks && lane == 0 && c * (32 * U) < nvec) {
+    const uint64_t left = nvec - c * (32 * U);
+    prefetch_l2(x + hb + c * (32 * U) * kVecBytes,
+                (uint32_t)((left < (32 * U) ? left : (32 * U)) * kVecBytes));
   }
   pdl_enter();
-  const uint64_t base = c * kChunkVecs + lane;
-  uint32_t v[kUnroll][8];
+  const uint64_t base = c * (32 * U) + lane;
+  uint32_t v[U][8];
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     ld256<NC>(x + hb + i * kVecBytes, v[u], i < nvec);
   }
   constexpr bool kScreen = needs_tie_screen<OP_GELU, FMT>() && NC;   // as in k_map
   uint32_t kmin = 0xFFFFFFFFu;
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     uint32_t g[8], sw[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -352,7 +376,7 @@ k_dual(const uint8_t *x, uint8_t *yg, uint8_t *ys, uint32_t head, uint64_t nvec,
     st256(ys + hb + i * kVecBytes, sw, i < nvec);
   }
   if (kScreen && __any_sync(0xffffffffu, tie_possible(kmin)))
-    tie_fixup_dual(x + hb, yg + hb, ys + hb, base, nvec);   // rare
+    tie_fixup_dual<U>(x + hb, yg + hb, ys + hb, base, nvec);   // rare
   if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
     dual_span<FMT>(x, yg, ys, head, L);
     const size_t toff = ((size_t)head + (size_t)nvec * (kVecBytes / es)) * es;
@@ -829,20 +853,21 @@ static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &l
   const size_t body = n - head;
   const uint64_t nvec = body / (kVecBytes / es);
   const uint32_t tail = (uint32_t)(body - nvec * (kVecBytes / es));
-  const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+  constexpr int U = map_unroll<OP, FMT>();
+  const uint64_t nchunks = (nvec + 32 * U - 1) / (32 * U);
   if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const unsigned grid = flat_grid(nchunks);
   if (x != y) {
     if (prefetch_enabled() && !sysmem) {   // L2 prefetch is for HBM inputs only
-      static const int bps = resident_blocks(k_map<OP, FMT, true, true>);
+      static const int bps = resident_blocks(k_map<OP, FMT, true, true, U>);
       const uint32_t pf_blocks = (uint32_t)(li.sm_count * bps);
-      return launch(k_map<OP, FMT, true, true>, grid, s, xp, yp, (uint32_t)head, nvec, tail,
+      return launch(k_map<OP, FMT, true, true, U>, grid, s, xp, yp, (uint32_t)head, nvec, tail,
                     pf_blocks, prefetch_depth(), lut);
     }
-    return launch(k_map<OP, FMT, true, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
+    return launch(k_map<OP, FMT, true, false, U>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
                   lut);
   }
-  return launch(k_map<OP, FMT, false, false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
+  return launch(k_map<OP, FMT, false, false, U>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
                 lut);
 }
 
@@ -952,15 +977,16 @@ static cudaError_t launch_dual_t(const void *x, void *yg, void *ys, size_t n, co
   const size_t body = n - head;
   const uint64_t nvec = body / (kVecBytes / es);
   const uint32_t tail = (uint32_t)(body - nvec * (kVecBytes / es));
-  const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+  constexpr int U = dual_unroll<FMT>();
+  const uint64_t nchunks = (nvec + 32 * U - 1) / (32 * U);
   if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const unsigned grid = flat_grid(nchunks);
   if (x != yg && x != ys) {
-    static const int bps = resident_blocks(k_dual<FMT, true>);
+    static const int bps = resident_blocks(k_dual<FMT, true, U>);
     const uint32_t pf = prefetch_enabled() ? (uint32_t)(li.sm_count * bps) : 0u;
-    return launch(k_dual<FMT, true>, grid, s, xp, gp, sp, (uint32_t)head, nvec, tail, pf, lut);
+    return launch(k_dual<FMT, true, U>, grid, s, xp, gp, sp, (uint32_t)head, nvec, tail, pf, lut);
   }
-  return launch(k_dual<FMT, false>, grid, s, xp, gp, sp, (uint32_t)head, nvec, tail, 0u, lut);
+  return launch(k_dual<FMT, false, U>, grid, s, xp, gp, sp, (uint32_t)head, nvec, tail, 0u, lut);
 }
 
 cudaError_t launch_dual(int fmt, const void *x, void *yg, void *ys, size_t n, const LutWords &lut,

@@ -1,9 +1,11 @@
-# round-2 dev call: staged-ring cell parity, first-wave prefetch A/B, then the round capture
+# round-2 dev call: parity of the per-kernel unroll build, then unroll A/B
 set -x
-KT_CELL_KERNEL=1 timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_guards.py tests/test_gpu_large.py -k "cell" -x -q -p no:cacheprovider > gpurun_out/gputest_r02f_k1.log 2>&1
-tail -2 gpurun_out/gputest_r02f_k1.log
-for rep in 1 2; do for pf in 1 0; do
-  echo "{\"variant\": \"KT_CELL_PF=$pf\"}" >> gpurun_out/ab_r02f.jsonl
-  KT_CELL_PF=$pf timeout 300 python tools/ab_stream.py c4_lstm_gates:lstm_cell >> gpurun_out/ab_r02f.jsonl 2>> gpurun_out/ab_r02f.err
+R=$GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_guards.py tests/test_gpu_exhaustive_f32.py tests/test_gpu_f32_tables.py -x -q -p no:cacheprovider > gpurun_out/gputest_r02h.log 2>&1
+tail -2 gpurun_out/gputest_r02h.log
+L="c5_ffn_2p30:kgelu_bf16 c5_ffn_2p30:kgelu_swish_bf16 c3_f32_2p28:ktanh_f32 c3_f32_2p28:ktanh_f32_via_bf16"
+for rep in 1 2; do for v in default g8 f8 d1m8 g2; do
+  unset KT_LIB; [ $v != default ] && export KT_LIB=$R/abtmp/lib_$v.so
+  echo "{\"variant\": \"$v\"}" >> gpurun_out/ab_r02h.jsonl
+  timeout 400 python tools/ab_stream.py $L >> gpurun_out/ab_r02h.jsonl 2>> gpurun_out/ab_r02h.err
 done; done
-TAG=r02a bash tools/gpu_round_capture.sh
