@@ -62,6 +62,12 @@ template <int FMT>
 __host__ __device__ constexpr int dual_unroll() {
   return FMT == FMT_BF16 ? KT_UNROLL_DUAL : kUnroll;
 }
+#ifndef KT_UNROLL_BWD
+#define KT_UNROLL_BWD 2
+#endif
+#ifndef KT_UNROLL_64
+#define KT_UNROLL_64 2
+#endif
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -245,7 +251,7 @@ __device__ __forceinline__ void span64(const uint8_t *xp, uint8_t *yp, uint32_t 
   if (on) reinterpret_cast<uint16_t *>(yp)[lane] = (uint16_t)r;
 }
 
-template <bool NC>
+template <bool NC, int U>
 __global__ void __launch_bounds__(kThreads)
 k_map64(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail, uint32_t pf_blocks,
         const __grid_constant__ LutWords64 lut) {
@@ -254,26 +260,26 @@ k_map64(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tai
   const uint8_t *xb = x + (size_t)head * 2;
   uint8_t *yb = y + (size_t)head * 2;
   const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (NC && blockIdx.x < pf_blocks && lane == 0 && c * kChunkVecs < nvec) {
-    const uint64_t left = nvec - c * kChunkVecs;
-    prefetch_l2(xb + c * kChunkVecs * kVecBytes,
-                (uint32_t)((left < kChunkVecs ? left : kChunkVecs) * kVecBytes));
+  if (NC && blockIdx.x < pf_blocks && lane == 0 && c * (32 * U) < nvec) {
+    const uint64_t left = nvec - c * (32 * U);
+    prefetch_l2(xb + c * (32 * U) * kVecBytes,
+                (uint32_t)((left < (32 * U) ? left : (32 * U)) * kVecBytes));
   }
   pdl_enter();
-  const uint64_t base = c * kChunkVecs + lane;
-  uint32_t v[kUnroll][8];
+  const uint64_t base = c * (32 * U) + lane;
+  uint32_t v[U][8];
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     ld256<NC>(xb + i * kVecBytes, v[u], i < nvec);
   }
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[u][j] = ktanh64_bf16x2(v[u][j], w0, w1);
   }
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     st256(yb + i * kVecBytes, v[u], i < nvec);
   }
@@ -421,7 +427,7 @@ __device__ __forceinline__ void scalar_span_bwd(const uint8_t *ap, const uint8_t
   }
 }
 
-template <int OP, int FMT, bool NC>
+template <int OP, int FMT, bool NC, int U>
 __global__ void __launch_bounds__(kThreads, KT_BWD_MINB)
 k_bwd(const uint8_t *a, const uint8_t *dy, uint8_t *dx, uint32_t head, uint64_t nvec, uint32_t tail,
       const __grid_constant__ LutWords lut) {
@@ -431,21 +437,21 @@ k_bwd(const uint8_t *a, const uint8_t *dy, uint8_t *dx, uint32_t head, uint64_t 
   const uint32_t lane = threadIdx.x & 31;
   const size_t hb = (size_t)head * es;
   const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint64_t base = c * kChunkVecs + lane;
-  uint32_t va[kUnroll][8], vd[kUnroll][8];
+  const uint64_t base = c * (32 * U) + lane;
+  uint32_t va[U][8], vd[U][8];
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     ld256<NC>(a + hb + i * kVecBytes, va[u], i < nvec);
     ld256<NC>(dy + hb + i * kVecBytes, vd[u], i < nvec);
   }
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) va[u][j] = apply_bwd_word<OP, FMT>(va[u][j], vd[u][j], L);
   }
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
     st256(dx + hb + i * kVecBytes, va[u], i < nvec);
   }
@@ -907,12 +913,13 @@ static cudaError_t launch_bwd_op(const void *a, const void *dy, void *dx, size_t
   const size_t body = n - head;
   const uint64_t nvec = body / (kVecBytes / es);
   const uint32_t tail = (uint32_t)(body - nvec * (kVecBytes / es));
-  const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+  constexpr int U = KT_UNROLL_BWD;
+  const uint64_t nchunks = (nvec + 32 * U - 1) / (32 * U);
   if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const unsigned grid = flat_grid(nchunks);
   if (dx != a && dx != dy)
-    return launch(k_bwd<OP, FMT, true>, grid, s, ap, dp, xp, (uint32_t)head, nvec, tail, lut);
-  return launch(k_bwd<OP, FMT, false>, grid, s, ap, dp, xp, (uint32_t)head, nvec, tail, lut);
+    return launch(k_bwd<OP, FMT, true, U>, grid, s, ap, dp, xp, (uint32_t)head, nvec, tail, lut);
+  return launch(k_bwd<OP, FMT, false, U>, grid, s, ap, dp, xp, (uint32_t)head, nvec, tail, lut);
 }
 
 cudaError_t launch_bwd(int op, int fmt, const void *a, const void *dy, void *dx, size_t n,
@@ -947,15 +954,16 @@ cudaError_t launch_map64(const void *x, void *y, size_t n, const LutWords64 &lut
   const size_t body = n - head;
   const uint64_t nvec = body / 16;
   const uint32_t tail = (uint32_t)(body - nvec * 16);
-  const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+  constexpr int U = KT_UNROLL_64;
+  const uint64_t nchunks = (nvec + 32 * U - 1) / (32 * U);
   if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const unsigned grid = flat_grid(nchunks);
   if (x != y) {
-    static const int bps = resident_blocks(k_map64<true>);
+    static const int bps = resident_blocks(k_map64<true, U>);
     const uint32_t pf = prefetch_enabled() ? (uint32_t)(li.sm_count * bps) : 0u;
-    return launch(k_map64<true>, grid, s, xp, yp, (uint32_t)head, nvec, tail, pf, lut);
+    return launch(k_map64<true, U>, grid, s, xp, yp, (uint32_t)head, nvec, tail, pf, lut);
   }
-  return launch(k_map64<false>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, lut);
+  return launch(k_map64<false, U>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, lut);
 }
 
 template <int FMT>
