@@ -390,7 +390,11 @@ k_gemm_t(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUte
       const uint32_t row = mb * 128 * CTAS + rank * 128 + 32 * q + lane;
       if (kCell) {
         const size_t cbase = (size_t)row * g.H + nb * 64 + half * 32;
-        uint32_t cp[4][8];                                          // c_prev, before the wait
+        // c_prev, before the wait.  Non-coherent loads are safe even when
+        // c_next == c_prev: the only write to these 32 elements is this
+        // thread's own c' store, issued after this read; other threads may
+        // write other elements of the same lines, which this read never uses.
+        uint32_t cp[4][8];
 #pragma unroll
         for (int v = 0; v < 4; ++v) ld256<true>(g.c_prev + cbase + 8 * v, cp[v], true);
         mbar_wait(tfull_bar + 8 * a, (i / 2) & 1);

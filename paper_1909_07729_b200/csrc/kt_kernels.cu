@@ -537,9 +537,13 @@ k_lstm(const uint8_t *x, uint8_t *y, uint32_t nvec, uint32_t vpr, uint32_t vpq, 
 // Fused LSTM cell, vector path: 16 consecutive cells of one row per lane
 // (hidden % 16 == 0, all pointers 32-B aligned).  Per 16 cells: 4 x 32 B of
 // gates + 64 B of c in, 64 B of c' + 32 B of h out (18 B per cell).
+// NCC: c_prev read on the non-coherent path; the launcher picks the coherent
+// instantiation when c_next == c_prev (in place), as launch_op does for x == y.
 #ifdef KT_CELL_MINB
+template <bool NCC>
 __global__ void __launch_bounds__(kThreads, KT_CELL_MINB)
 #else
+template <bool NCC>
 __global__ void __launch_bounds__(kThreads)   // (kThreads, 1) lets ptxas take > 64 regs: slower
 #endif
 k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_t *h_next,
@@ -577,8 +581,8 @@ k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_
   ld256<true>(gr + qb, gf, on);
   ld256<true>(gr + 2 * qb, gg, on);
   ld256<true>(gr + 3 * qb, go, on);
-  ld256<true>(c_prev + cidx * 4, c0, on);
-  ld256<true>(c_prev + cidx * 4 + 32, c1, on);
+  ld256<NCC>(c_prev + cidx * 4, c0, on);
+  ld256<NCC>(c_prev + cidx * 4 + 32, c1, on);
   uint32_t cn0[8], cn1[8], h[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -1083,13 +1087,15 @@ cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *
   if (aligned && hidden % 16 == 0 && nvec < (1ull << 31)) {
     const uint64_t nwarps = (nvec + 31) / 32;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, (nwarps + kWarps - 1) / kWarps);
-    static const int bps = resident_blocks(k_lstm_cell);
+    static const int bps = resident_blocks(k_lstm_cell<true>);
     static const int pf_on = [] {
       const char *e = getenv("KT_CELL_PF");     // dev A/B: 0 = no first-wave L2 prefetch
       return e ? atoi(e) : 1;
     }();
     const uint32_t pf_blocks = (pf_on && prefetch_enabled()) ? (uint32_t)(li.sm_count * bps) : 0u;
-    return launch(k_lstm_cell, grid, s, reinterpret_cast<const uint8_t *>(gates),
+    auto kern = (static_cast<const void *>(c_next) == static_cast<const void *>(c_prev)) ? k_lstm_cell<false>
+                                                                                         : k_lstm_cell<true>;
+    return launch(kern, grid, s, reinterpret_cast<const uint8_t *>(gates),
                   reinterpret_cast<const uint8_t *>(c_prev), reinterpret_cast<uint8_t *>(c_next),
                   reinterpret_cast<uint8_t *>(h_next), (uint32_t)nvec, (uint32_t)(hidden / 16),
                   (uint32_t)hidden, pf_blocks, lut);
