@@ -789,6 +789,27 @@ def test_concurrent_threads_mixed_calls(kt):
             assert torch.equal(a.view(torch.int16), b.view(torch.int16))
 
 
+@pytest.mark.parametrize("op", DERIVED)
+def test_bf16_isolated_ties_exact(kt, op):
+    """Each x/2-tie input (|x| < 2^-125, odd last bit) ALONE in its warp's
+    chunk among ordinary values, at a different lane position each time: the
+    streaming kernel's screen must flag the chunk from that one input (its
+    |argument| anywhere below 2^-125), in K-GELU, K-Swish and the fused pass."""
+    ties = [w | s for w in range(1, 0x100, 2) for s in (0, 0x8000)]
+    span = 8192                                   # > any chunk (2048 elements at 4 vectors per lane)
+    rng = np.random.default_rng(29)
+    base = (rng.standard_normal(len(ties) * span) * 2 + 3).astype(np.float32)   # |x| >> 2^-125
+    bits = (base.view(np.uint32) >> 16).astype(np.uint16)
+    for k, w in enumerate(ties):
+        bits[k * span + (k * 997) % span] = w
+    x = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+    want = oracle_bf16(op, bits)
+    check(op, "bf16", u16(call(kt, op, "bf16", x)), want, f"{op} isolated ties")
+    g, sw = kt.kgelu_swish_bf16(x)
+    check("gelu", "bf16", u16(g), oracle_bf16("gelu", bits), "dual gelu isolated ties")
+    check("swish", "bf16", u16(sw), oracle_bf16("swish", bits), "dual swish isolated ties")
+
+
 def test_binding_validates_caller_outputs(kt):
     """every caller-supplied output is checked (dtype, size, device,
     layout) before its pointer reaches the C ABI, which cannot bound-check it."""

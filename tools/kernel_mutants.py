@@ -66,6 +66,21 @@ MUTANTS = [
      "h = __fsub_rn(h, k != 0 ? 0.2f : 0.0f);", "tests/test_gpu_apx.py"),
     ("pade comparator saturation", APX, "return a >= w.xsat ? 1.0f : y;", "return a > 2.0f * w.xsat ? 1.0f : y;",
      "tests/test_gpu_apx.py"),
+    # round 2: the exact outer step (R-DERIVED) and the per-kernel unroll
+    ("tie patch direction", D, "const uint32_t inc = (s == 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;",
+     "const uint32_t inc = (s != 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;", PARITY),
+    ("tie screen threshold", D, "return (kmin & 0xFF00u) == 0 || (kmin & 0xFF000000u) == 0;",
+     "return (kmin & 0xFF80u) == 0 || (kmin & 0xFF800000u) == 0;", PARITY),
+    ("outer_exact rounds both ways", D,
+     "const uint32_t up = hset2_gt(r, 0u) & hset2_ne(t, 0u) & kOnex2;     // 1.0 where the t-term rounds up",
+     "const uint32_t up = hset2_ne(r, 0u) & hset2_ne(t, 0u) & kOnex2;", PARITY),
+    ("f32 outer tie ignored", D, "const float c = (r > 0.0f && t != 0.0f) ? __fadd_rn(hx, r) : hx;",
+     "const float c = hx;", "tests/test_gpu_exhaustive_f32.py"),
+    ("dual tie fix-up dropped", KK, "    tie_fixup_dual<U>(x + hb, yg + hb, ys + hb, base, nvec);   // rare",
+     "    (void)0;", PARITY),
+    ("map grid for a larger chunk", KK,
+     "  constexpr int U = map_unroll<OP, FMT>();\n  const uint64_t nchunks = (nvec + 32 * U - 1) / (32 * U);",
+     "  constexpr int U = map_unroll<OP, FMT>();\n  const uint64_t nchunks = (nvec + 64 * U - 1) / (64 * U);", PARITY),
     ("host pipeline chunk offset", API,
      "KT_CK(cudaMemcpyAsync(yh + off * es, dy, cnt * es, cudaMemcpyDeviceToHost, d2h), \"D2H\");",
      "KT_CK(cudaMemcpyAsync(yh + off * es, dy, (cnt - (cnt > 1)) * es, cudaMemcpyDeviceToHost, d2h), \"D2H\");",
