@@ -1,7 +1,11 @@
 """Small calls of every library entry point, for compute-sanitizer (dev tool):
 ragged sizes, unaligned heads/tails, mismatched alignment, in place, LSTM
-gates and cell (vector and element paths), backward, GEMM + epilogue,
-host pipeline."""
+gates and cell (vector and element paths; KT_CELL_KERNEL=1 for the staged
+ring), backward, GEMM + epilogue, host pipeline, and inputs with x/2 ties
+(the K-Swish / K-GELU tie screen and its out-of-line fix-up).
+
+  compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_smoke.py
+"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -20,7 +24,15 @@ for n in (1, 17, 1000, 4099):
                 getattr(kt, f"k{op}_bwd_{sfx}")(x, x.clone(), out=out[off:off + n])
             z = x.clone()
             kt.ktanh_bf16(z, out=z) if sfx == "bf16" else kt.ktanh_f32(z, out=z)
-for rows, H in ((3, 16), (5, 10), (2, 1024)):
+ties = torch.tensor([w | s for w in range(1, 0x100, 2) for s in (0, 0x8000)], dtype=torch.int32)
+for n in (4096, 70000):
+    xb = (torch.randn(n, device=dev) * 2).to(torch.bfloat16)
+    xi = xb.view(torch.int16)
+    xi[torch.arange(0, n, 61, device=dev)[:ties.numel()]] = ties[: len(range(0, n, 61))].to(torch.int16).to(dev)
+    for op in ("swish", "gelu"):
+        getattr(kt, f"k{op}_bf16")(xb)
+    kt.kgelu_swish_bf16(xb)
+for rows, H in ((3, 16), (5, 10), (2, 1024), (7, 256), (40, 1024)):
     g = (torch.randn(rows, 4 * H, device=dev) * 1.5).to(torch.bfloat16)
     kt.klstm_gates_bf16(g, H, 2)
     c = torch.randn(rows, H, device=dev)
