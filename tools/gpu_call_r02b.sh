@@ -1,8 +1,8 @@
-# round-2 dev call: new isolated-tie test, kernel mutants, full F32 derived sweep
+# round-2 dev call: compute-sanitizer over every entry point (incl. tie fix-up and the staged cell ring)
 set -x
-timeout 600 python -m pytest tests/test_gpu_parity.py -k "ties or lstm_cell" -x -q -p no:cacheprovider > gpurun_out/gputest_r02j.log 2>&1
-tail -2 gpurun_out/gputest_r02j.log
-timeout 2400 python tools/kernel_mutants.py run > gpurun_out/kernel_mutants_r02.txt 2>&1
-tail -30 gpurun_out/kernel_mutants_r02.txt
-timeout 1800 python tools/f32_derived_sweep.py > gpurun_out/f32_derived_sweep_r02.txt 2>&1
-cat gpurun_out/f32_derived_sweep_r02.txt
+CS=/usr/local/cuda/bin/compute-sanitizer
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize_smoke.py > gpurun_out/sanitize_${tool}_r02.txt 2>&1; echo "$tool rc=$?" >> gpurun_out/sanitize_r02.txt
+  KT_CELL_KERNEL=1 timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize_smoke.py > gpurun_out/sanitize_${tool}_ring_r02.txt 2>&1; echo "$tool (KT_CELL_KERNEL=1) rc=$?" >> gpurun_out/sanitize_r02.txt
+done
+cat gpurun_out/sanitize_r02.txt
