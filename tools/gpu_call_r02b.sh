@@ -1,8 +1,9 @@
-# round-2 dev call: compute-sanitizer over every entry point (incl. tie fix-up and the staged cell ring)
+# round-2 dev call: K-GELU occupancy / unroll A/B
 set -x
-CS=/usr/local/cuda/bin/compute-sanitizer
-for tool in memcheck racecheck synccheck initcheck; do
-  timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize_smoke.py > gpurun_out/sanitize_${tool}_r02.txt 2>&1; echo "$tool rc=$?" >> gpurun_out/sanitize_r02.txt
-  KT_CELL_KERNEL=1 timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize_smoke.py > gpurun_out/sanitize_${tool}_ring_r02.txt 2>&1; echo "$tool (KT_CELL_KERNEL=1) rc=$?" >> gpurun_out/sanitize_r02.txt
-done
-cat gpurun_out/sanitize_r02.txt
+R=$GRAFT_REPO_ROOT
+L="c5_ffn_2p30:kgelu_bf16 c3_f32_2p28:ktanh_f32"
+for rep in 1 2; do for v in default m5 g3 g3m5 g6; do
+  unset KT_LIB; [ $v != default ] && export KT_LIB=$R/abtmp/lib_$v.so
+  echo "{\"variant\": \"$v\"}" >> gpurun_out/ab_r02k.jsonl
+  timeout 400 python tools/ab_stream.py $L >> gpurun_out/ab_r02k.jsonl 2>> gpurun_out/ab_r02k.err
+done; done
