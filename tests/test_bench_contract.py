@@ -89,3 +89,20 @@ def test_multirank_path_under_torchrun_stub():
     # value = all ranks' elements / the slowest rank's (median) window
     assert max(p["ms_per_step"] for p in pr) <= d["ms_per_step"] * 1.5 + 1e-3
     assert abs(d["value"] - 2 * (1 << 16) / (d["ms_per_step"] / 1e3) / 1e9) <= 1e-3 * d["value"] + 1e-3
+
+
+def test_traffic_is_read_per_workload_from_committed_captures():
+    """roofline.traffic comes from the committed range-replay capture of the
+    bench line's OWN workload and call (the c2 capture must not
+    stand in for another config); every capture is within 2% of the
+    algorithmic bytes per launch."""
+    sys.path.insert(0, ROOT)
+    import bench
+    alg = {("c5_ffn_2p30", "kgelu_bf16"): 4 << 30, ("c5_ffn_2p30", "kswish_bf16"): 4 << 30,
+           ("c5_ffn_2p30", "kgelu_swish_bf16"): 6 << 30, ("c3_f32_2p28", "ktanh_f32"): 8 << 28,
+           ("c2_bf16_2p24", "ktanh_bf16"): 4 << 24, ("c4_lstm_gates", "lstm"): 4 * 128 * 50 * 4096}
+    for (key, op), a in alg.items():
+        t, src = bench.load_traffic(key, op)
+        assert t is not None and f"_{key}_{op}_r" in src, (key, op, src)
+        assert 0.98 * a <= t <= 1.02 * a, (key, op, t, a)
+    assert bench.load_traffic("c5_ffn_2p30", "no_such_call") == (None, None)

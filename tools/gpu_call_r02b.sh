@@ -1,9 +1,10 @@
-# round-2 dev call: K-GELU occupancy / unroll A/B
+# round-2 functional check of bench.py's N > 1 path on real CUDA (2 ranks on the pool's one GPU:
+# NOT a measurement -- the ranks share the GPU), plus smoke()
 set -x
-R=$GRAFT_REPO_ROOT
-L="c5_ffn_2p30:kgelu_bf16 c3_f32_2p28:ktanh_f32"
-for rep in 1 2; do for v in default m5 g3 g3m5 g6; do
-  unset KT_LIB; [ $v != default ] && export KT_LIB=$R/abtmp/lib_$v.so
-  echo "{\"variant\": \"$v\"}" >> gpurun_out/ab_r02k.jsonl
-  timeout 400 python tools/ab_stream.py $L >> gpurun_out/ab_r02k.jsonl 2>> gpurun_out/ab_r02k.err
-done; done
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r02.txt 2>&1; tail -2 gpurun_out/smoke_r02.txt
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 20 --warmup 3 > gpurun_out/bench_n2_functional_r02.json 2> gpurun_out/bench_n2_functional_r02.err
+echo rc=$?
+tail -c 1500 gpurun_out/bench_n2_functional_r02.json
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --impl reference --gpus 2 --steps 3 --warmup 3 > gpurun_out/bench_n2_ref_r02.json 2>&1
+echo rc=$?
+cat gpurun_out/bench_n2_ref_r02.json | tail -2
