@@ -838,3 +838,37 @@ def test_binding_validates_caller_outputs(kt):
     with pytest.raises(TypeError):
         kt.apply("tanh", torch.zeros(64, dtype=torch.float16, device="cuda"))
     torch.cuda.synchronize()
+
+
+def test_lstm_cell_staged_ring_kernel():
+    """The shared-memory-staged LSTM cell (KT_CELL_KERNEL=1, the persistent
+    cp.async.bulk / mbarrier ring kept for A/B) is bit-exact
+    too: a fresh process (the kernel choice is read once per process) over
+    shapes with multi-row tiles, ragged tails and in-place c."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, "tests")
+import oracle as O, paper_1909_07729_b200 as kt
+from _cmp import assert_bitexact
+def u16(t): return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+def u32(t): return t.contiguous().view(torch.int32).cpu().numpy().view(np.uint32)
+for rows, hidden in ((3, 256), (41, 272), (1000, 528), (2, 4096), (640, 1024)):
+    g = torch.Generator(device="cuda").manual_seed(rows + hidden)
+    gates = (torch.randn(rows, 4 * hidden, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    c = torch.randn(rows, hidden, device="cuda", generator=g) * 2
+    cn, hn = kt.klstm_cell_bf16(gates, c, hidden)
+    wc, wh = O.lstm_cell_bf16(u16(gates), u32(c), hidden)
+    assert_bitexact(u32(cn), wc, 32, ctx="ring c_next")
+    assert_bitexact(u16(hn), wh, 16, nan_by_class=True, ctx="ring h_next")
+    c2 = c.clone()
+    kt.klstm_cell_bf16(gates, c2, hidden, c_next=c2)
+    assert_bitexact(u32(c2), wc, 32, ctx="ring in place")
+print("ring ok")
+'''
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=dict(os.environ, KT_CELL_KERNEL="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ring ok" in r.stdout, r.stderr[-2000:]
