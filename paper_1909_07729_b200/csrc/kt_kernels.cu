@@ -226,6 +226,9 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
       }
     }
   }
+  // all U loads were issued before any arithmetic and all stores follow it
+  // (the ld/st asm statements are volatile, so storing a vector early would
+  // also delay the next vector's load: fewer bytes in flight)
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint64_t i = base + (uint64_t)u * 32;
