@@ -1,10 +1,7 @@
-# round-2 functional check of bench.py's N > 1 path on real CUDA (2 ranks on the pool's one GPU:
-# NOT a measurement -- the ranks share the GPU), plus smoke()
+# round-2: headline repeatability (three default bench runs back to back on one box)
 set -x
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r02.txt 2>&1; tail -2 gpurun_out/smoke_r02.txt
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 20 --warmup 3 > gpurun_out/bench_n2_functional_r02.json 2> gpurun_out/bench_n2_functional_r02.err
-echo rc=$?
-tail -c 1500 gpurun_out/bench_n2_functional_r02.json
-timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --impl reference --gpus 2 --steps 3 --warmup 3 > gpurun_out/bench_n2_ref_r02.json 2>&1
-echo rc=$?
-cat gpurun_out/bench_n2_ref_r02.json | tail -2
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit,temperature.gpu --format=csv
+for k in 1 2 3; do
+  timeout 600 python bench.py --no-extra > gpurun_out/bench_rep${k}_r02.json 2> gpurun_out/bench_rep${k}_r02.err
+  python -c "import json;d=json.loads(open('gpurun_out/bench_rep${k}_r02.json').read().strip().splitlines()[-1]);print('rep $k', d['value'], d['roofline']['frac'], d['clocks'])"
+done
