@@ -715,6 +715,40 @@ def oracle_check(x, y, op, m=1 << 16, seed=0, stub=False):
     return int(bad.sum()), int(idx.size)
 
 
+def full_shard_check(x, y, op):
+    """--full-check (opt-in, part of the cpu_baseline leg): EVERY element of
+    this rank's output against the oracle, on all host cores (SURVEY.md 8(d):
+    "check all shards"); returns (mismatches, elements, seconds)."""
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    bf16 = x.dtype == torch.bfloat16
+    iv, nv = (torch.int16, np.uint16) if bf16 else (torch.int32, np.uint32)
+    xs = x.reshape(-1).view(iv).cpu().numpy().view(nv)
+    ys = y.reshape(-1).view(iv).cpu().numpy().view(nv)
+    n = xs.size
+    nthr = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    step = 1 << 22
+    bits = 16 if bf16 else 32
+    mag = (1 << (bits - 1)) - 1
+    nan_lo = 0x7F80 if bf16 else 0x7F800000
+
+    def part(a):
+        b = min(n, a + step)
+        want = O.map_bf16(op, xs[a:b]) if bf16 else O.map_f32(op, xs[a:b])
+        got = ys[a:b]
+        bad = got != want
+        g64, w64 = got.astype(np.int64), want.astype(np.int64)
+        if op != "tanh":
+            bad &= ~(((g64 & mag) > nan_lo) & ((w64 & mag) > nan_lo))
+        if op in ("swish", "gelu"):
+            bad &= ~(((g64 & mag) == 0) & ((w64 & mag) == 0))
+        return int(bad.sum())
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(nthr) as pool:
+        bad = sum(pool.map(part, range(0, n, step)))
+    return bad, n, time.perf_counter() - t0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -726,6 +760,8 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(HEADS),
                     help="workload of the headline line (default c5: BASELINE.json configs[4], "
                          "the configuration the metric is quoted on at 1/2/4/8 GPUs)")
+    ap.add_argument("--full-check", action="store_true",
+                    help="also check every element of each rank's output against the oracle (all host cores)")
     ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -783,6 +819,9 @@ def main():
     bad = checked = 0
     if not args.no_cpu and head_oracle_op != "lstm":
         bad, checked = oracle_check(step.xs[0], step.ys[0], head_oracle_op, seed=rank, stub=args.stub)
+    if args.full_check and not args.stub and head_oracle_op != "lstm":
+        fbad, fn, fsec = full_shard_check(step.xs[0], step.ys[0], head_oracle_op)
+        bad, checked = bad + fbad, checked + fn
     per_rank = _kd().gather_over_ranks([rank, dev_index, own_ms, bad, checked]) if world > 1 else \
         [[rank, dev_index, own_ms, bad, checked]]
     eager_ms = ms if args.stub else time_eager(step, K, device)
@@ -817,7 +856,9 @@ def main():
         cpu = cpu_baseline(hcfg, head_oracle_op, device)
     if cpu is not None:
         cpu["check"] = {"what": "every rank: seeded sample of its own GPU output vs the oracle on the "
-                                "same input bytes, after the timed region",
+                                "same input bytes, after the timed region" +
+                                ("; plus EVERY element of each rank's output (--full-check)"
+                                 if args.full_check else ""),
                         "samples_per_rank": int(per_rank[0][4]),
                         "mismatches": int(sum(r[3] for r in per_rank))}
 
