@@ -106,14 +106,47 @@ __device__ __forceinline__ uint32_t epi_word(uint32_t w, uint32_t lw) {
 
 // 32 fp32 accumulators (TMEM columns c..c+31 of one row) -> RN_bf16 -> op ->
 // two 16-element output vectors.
+// K-Swish / K-GELU: the plain-fma outer step, exact unless the chunk holds an
+// x/2 tie (R-DERIVED, kt_device.cuh).  The 16 packed pre-activations are
+// screened first (|x| via abs.bf16x2 and a packed-u16 min: a warp-uniform
+// branch on "some |x| below 2^-125, or a zero"), then the whole chunk takes
+// the plain fma or the exact outer step -- 1.5 ops per pair instead of the
+// exact step's 6.  KT_GEMM_EXACT_EPI=1 (dev A/B): the exact step always.
+#ifndef KT_GEMM_EXACT_EPI
+#define KT_GEMM_EXACT_EPI 0
+#endif
 template <int EPI>
 __device__ __forceinline__ void epi_chunk32(const uint32_t *r, uint32_t (&o0)[8], uint32_t (&o1)[8],
                                             uint32_t lw) {
+  uint32_t w0[8], w1[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);
-    o1[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 17]), __uint_as_float(r[2 * j + 16])),
-                          lw);
+    w0[j] = pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j]));
+    w1[j] = pack_bf16x2(__uint_as_float(r[2 * j + 17]), __uint_as_float(r[2 * j + 16]));
+  }
+  if ((EPI == OP_SWISH || EPI == OP_GELU) && !KT_GEMM_EXACT_EPI) {
+    uint32_t kmin = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t a0, a1;
+      asm("abs.bf16x2 %0, %1;" : "=r"(a0) : "r"(w0[j]));
+      asm("abs.bf16x2 %0, %1;" : "=r"(a1) : "r"(w1[j]));
+      kmin = umin16x2(kmin, umin16x2(a0, a1));
+    }
+    if (!__any_sync(0xffffffffu, tie_possible(kmin))) {
+      uint32_t m;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o0[j] = EPI == OP_GELU ? kgelu_bf16x2_fast(w0[j], lw, m) : kswish_bf16x2_fast(w0[j], lw, m);
+        o1[j] = EPI == OP_GELU ? kgelu_bf16x2_fast(w1[j], lw, m) : kswish_bf16x2_fast(w1[j], lw, m);
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    o0[j] = epi_word<EPI>(w0[j], lw);
+    o1[j] = epi_word<EPI>(w1[j], lw);
   }
 }
 
