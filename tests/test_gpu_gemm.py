@@ -195,3 +195,32 @@ def test_ffn_gemm_full_size(kt):
     got = O.bf16_to_f64(u16(plain[torch.from_numpy(r).cuda(), torch.from_numpy(c).cuda()]))
     bound = np.abs(exact) * 2.0 ** -8 + K * 2.0 ** -23 * (np.abs(a) * np.abs(b)).sum(axis=1) + 1e-30
     assert np.all(np.abs(got - exact) <= bound)
+
+
+@pytest.mark.parametrize("epi", ["swish", "gelu"])
+@pytest.mark.parametrize("M", [128, 256])
+def test_gemm_epilogue_tiny_preactivations(kt, epi, M):
+    """Pre-activations below 2^-125 (the x/2 ties of R-DERIVED) in some rows
+    and ordinary values in others: the epilogue's screen must send those
+    chunks through the exact outer step.  A[i, 0] = m_i 2^-70 with odd m_i,
+    B[j, 0] = 2^-63, so A B^T holds m_i 2^-133 exactly (a BF16 subnormal tie
+    candidate) unless the MMA flushes it; either way the fused output equals
+    the oracle applied to the plain GEMM output, bit for bit."""
+    N, K = 256, 64
+    a = np.zeros((M, K), np.float32)
+    b = np.zeros((N, K), np.float32)
+    rng = np.random.default_rng(M)
+    tiny_rows = np.arange(0, M, 2)
+    a[tiny_rows, 0] = (2 * rng.integers(0, 128, tiny_rows.size) + 1).astype(np.float32) * 2.0 ** -70
+    a[tiny_rows, 0] *= np.where(rng.random(tiny_rows.size) < 0.5, -1.0, 1.0).astype(np.float32)
+    b[:, 0] = 2.0 ** -63
+    a[1::2, 1:] = rng.standard_normal((M // 2, K - 1)).astype(np.float32) * 0.5
+    b[:, 1:] = rng.standard_normal((N, K - 1)).astype(np.float32) * 0.5
+    A = torch.from_numpy(a).cuda().to(torch.bfloat16)
+    B = torch.from_numpy(b).cuda().to(torch.bfloat16)
+    plain = u16(kt.kgemm_bf16(A, B))
+    fused = u16(kt.kgemm_bf16(A, B, epilogue=epi))
+    assert_bitexact(fused, O.map_bf16(epi, plain), 16, nan_by_class=True, zero_by_value=True,
+                    ctx=f"gemm {epi} tiny pre-activations")
+    ties = int(np.count_nonzero(((plain & 0x7FFF) < 0x100) & ((plain & 1) == 1)))
+    print(f"gemm {epi} M={M}: {ties} x/2-tie pre-activations in the output")
