@@ -62,6 +62,15 @@ template <int FMT>
 __host__ __device__ constexpr int dual_unroll() {
   return FMT == FMT_BF16 ? KT_UNROLL_DUAL : kUnroll;
 }
+// Threads per CTA of k_map: K-GELU BF16 (54 registers) fits 9 CTAs of 128
+// threads per SM (36 warps) but only 4 of 256 (32 warps); the other maps use 256.
+#ifndef KT_MAP_TPB_GELU
+#define KT_MAP_TPB_GELU 128
+#endif
+template <int OP, int FMT>
+__host__ __device__ constexpr int map_threads() {
+  return (FMT == FMT_BF16 && OP == OP_GELU) ? KT_MAP_TPB_GELU : kThreads;
+}
 #ifndef KT_UNROLL_BWD
 #define KT_UNROLL_BWD 2
 #endif
@@ -170,11 +179,11 @@ __device__ __noinline__ void tie_fixup_dual(const uint8_t *xb, uint8_t *gb, uint
 // elements precede the first 32-B boundary of x (and of y: same offset mod
 // 32, checked on the host); nvec vectors follow; then `tail` elements.
 #ifdef KT_MAP_MINB
-template <int OP, int FMT, bool NC, bool PF, int U>
-__global__ void __launch_bounds__(kThreads, KT_MAP_MINB)
+template <int OP, int FMT, bool NC, bool PF, int U, int TPB>
+__global__ void __launch_bounds__(TPB, KT_MAP_MINB)
 #else
-template <int OP, int FMT, bool NC, bool PF, int U>
-__global__ void __launch_bounds__(kThreads)
+template <int OP, int FMT, bool NC, bool PF, int U, int TPB>
+__global__ void __launch_bounds__(TPB)
 #endif
 k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
       uint32_t pf_blocks, uint32_t pf_depth, const __grid_constant__ LutWords lut) {
@@ -183,11 +192,12 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
   const uint32_t lane = threadIdx.x & 31;
   const uint8_t *xb = x + (size_t)head * es;
   uint8_t *yb = y + (size_t)head * es;
-  const uint64_t c = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);   // this warp's chunk
+  constexpr int kW = TPB / 32;                                             // warps per CTA
+  const uint64_t c = (uint64_t)blockIdx.x * kW + (threadIdx.x >> 5);       // this warp's chunk
   // only the first resident wave can be waiting behind a predecessor's tail
   if (PF && blockIdx.x < pf_blocks && lane < pf_depth) {
     // lane d prefetches the chunk of the warp d resident waves later
-    const uint64_t cc = c + (uint64_t)lane * pf_blocks * kWarps;
+    const uint64_t cc = c + (uint64_t)lane * pf_blocks * kW;
     if (cc * (32 * U) < nvec) {
       const uint64_t left = nvec - cc * (32 * U);
       prefetch_l2(xb + cc * (32 * U) * kVecBytes,
@@ -812,10 +822,11 @@ static uint32_t prefetch_depth() {
 }
 
 template <typename... KArgs, typename... Args>
-static cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, cudaStream_t s, Args... args) {
+static cudaError_t launch_tpb(void (*kernel)(KArgs...), unsigned grid, unsigned tpb, cudaStream_t s,
+                              Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(tpb);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -828,10 +839,15 @@ static cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, cudaStream_t 
   return e;
 }
 
+template <typename... KArgs, typename... Args>
+static cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, cudaStream_t s, Args... args) {
+  return launch_tpb(kernel, grid, kThreads, s, args...);
+}
+
 template <class K>
-static int resident_blocks(K kernel) {
+static int resident_blocks(K kernel, int tpb = kThreads) {
   int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, tpb, 0) != cudaSuccess || b < 1)
     b = 1;
   return b;
 }
@@ -867,20 +883,21 @@ static cudaError_t launch_op(const void *x, void *y, size_t n, const LutWords &l
   const uint64_t nvec = body / (kVecBytes / es);
   const uint32_t tail = (uint32_t)(body - nvec * (kVecBytes / es));
   constexpr int U = map_unroll<OP, FMT>();
+  constexpr int TPB = map_threads<OP, FMT>(), kW = TPB / 32;
   const uint64_t nchunks = (nvec + 32 * U - 1) / (32 * U);
-  if (nchunks / kWarps >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
-  const unsigned grid = flat_grid(nchunks);
+  if (nchunks / kW >= 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, (nchunks + kW - 1) / kW);
   if (x != y) {
     if (prefetch_enabled() && !sysmem) {   // L2 prefetch is for HBM inputs only
-      static const int bps = resident_blocks(k_map<OP, FMT, true, true, U>);
+      static const int bps = resident_blocks(k_map<OP, FMT, true, true, U, TPB>, TPB);
       const uint32_t pf_blocks = (uint32_t)(li.sm_count * bps);
-      return launch(k_map<OP, FMT, true, true, U>, grid, s, xp, yp, (uint32_t)head, nvec, tail,
+      return launch_tpb(k_map<OP, FMT, true, true, U, TPB>, grid, TPB, s, xp, yp, (uint32_t)head, nvec, tail,
                     pf_blocks, prefetch_depth(), lut);
     }
-    return launch(k_map<OP, FMT, true, false, U>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
+    return launch_tpb(k_map<OP, FMT, true, false, U, TPB>, grid, TPB, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
                   lut);
   }
-  return launch(k_map<OP, FMT, false, false, U>, grid, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
+  return launch_tpb(k_map<OP, FMT, false, false, U, TPB>, grid, TPB, s, xp, yp, (uint32_t)head, nvec, tail, 0u, 0u,
                 lut);
 }
 

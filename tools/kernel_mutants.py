@@ -79,8 +79,8 @@ MUTANTS = [
     ("dual tie fix-up dropped", KK, "    tie_fixup_dual<U>(x + hb, yg + hb, ys + hb, base, nvec);   // rare",
      "    (void)0;", PARITY),
     ("map grid for a larger chunk", KK,
-     "  constexpr int U = map_unroll<OP, FMT>();\n  const uint64_t nchunks = (nvec + 32 * U - 1) / (32 * U);",
-     "  constexpr int U = map_unroll<OP, FMT>();\n  const uint64_t nchunks = (nvec + 64 * U - 1) / (64 * U);", PARITY),
+     "  const uint64_t nchunks = (nvec + 32 * U - 1) / (32 * U);\n  if (nchunks / kW >= 0x7FFFFFFFull)",
+     "  const uint64_t nchunks = (nvec + 64 * U - 1) / (64 * U);\n  if (nchunks / kW >= 0x7FFFFFFFull)", PARITY),
     ("host pipeline chunk offset", API,
      "KT_CK(cudaMemcpyAsync(yh + off * es, dy, cnt * es, cudaMemcpyDeviceToHost, d2h), \"D2H\");",
      "KT_CK(cudaMemcpyAsync(yh + off * es, dy, (cnt - (cnt > 1)) * es, cudaMemcpyDeviceToHost, d2h), \"D2H\");",
