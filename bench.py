@@ -434,9 +434,9 @@ HEADS = {"c1": ("c1_exhaustive_bf16", "ktanh_bf16", "tanh"), "c2": ("c2_bf16_2p2
          "c5": ("c5_ffn_2p30", "kgelu_bf16", "gelu")}
 DTYPE_NAME = {torch.bfloat16: "bf16", torch.float32: "f32"}
 
-# demangled names as ncu lists them (profiles/launches_r02.csv): <OP, FMT, NC, PF, unroll>
-KERNEL_NAME = {"ktanh_bf16": "kt::k_map<0, 0, 1, 1, 2>", "ktanh_f32": "kt::k_map<0, 1, 1, 1, 4>",
-               "kgelu_bf16": "kt::k_map<3, 0, 1, 1, 4>", "kswish_bf16": "kt::k_map<2, 0, 1, 1, 2>",
+# demangled names as ncu lists them: <OP, FMT, NC, PF, unroll, threads per CTA>
+KERNEL_NAME = {"ktanh_bf16": "kt::k_map<0, 0, 1, 1, 2, 256>", "ktanh_f32": "kt::k_map<0, 1, 1, 1, 4, 256>",
+               "kgelu_bf16": "kt::k_map<3, 0, 1, 1, 4, 128>", "kswish_bf16": "kt::k_map<2, 0, 1, 1, 2, 256>",
                "lstm": "kt::k_lstm<1>"}
 
 EXTRA = [("c2_bf16_2p24", "ktanh_bf16"), ("c2_bf16_2p24", "ktanh64_bf16"), ("c3_f32_2p28", "ktanh_f32"),
