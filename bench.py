@@ -435,7 +435,7 @@ HEADS = {"c1": ("c1_exhaustive_bf16", "ktanh_bf16", "tanh"), "c2": ("c2_bf16_2p2
 DTYPE_NAME = {torch.bfloat16: "bf16", torch.float32: "f32"}
 
 # demangled names as ncu lists them: <OP, FMT, NC, PF, unroll, threads per CTA>
-KERNEL_NAME = {"ktanh_bf16": "kt::k_map<0, 0, 1, 1, 2, 256>", "ktanh_f32": "kt::k_map<0, 1, 1, 1, 4, 256>",
+KERNEL_NAME = {"ktanh_bf16": "kt::k_map<0, 0, 1, 1, 2, 256>", "ktanh_f32": "kt::k_map<0, 1, 1, 1, 4, 256>", "ktanh_f32_via_bf16": "kt::k_map<4, 1, 1, 1, 4, 128>",
                "kgelu_bf16": "kt::k_map<3, 0, 1, 1, 4, 128>", "kswish_bf16": "kt::k_map<2, 0, 1, 1, 2, 256>",
                "lstm": "kt::k_lstm<1>"}
 

@@ -62,14 +62,15 @@ template <int FMT>
 __host__ __device__ constexpr int dual_unroll() {
   return FMT == FMT_BF16 ? KT_UNROLL_DUAL : kUnroll;
 }
-// Threads per CTA of k_map: K-GELU BF16 (54 registers) fits 9 CTAs of 128
-// threads per SM (36 warps) but only 4 of 256 (32 warps); the other maps use 256.
+// Threads per CTA of k_map: K-GELU BF16 and F32-through-BF16 (50-54
+// registers at U = 4) fit 9 CTAs of 128 threads per SM (36 warps) but only 4
+// of 256 (32 warps); for the other maps both sizes give the same warps per SM.
 #ifndef KT_MAP_TPB_GELU
 #define KT_MAP_TPB_GELU 128
 #endif
 template <int OP, int FMT>
 __host__ __device__ constexpr int map_threads() {
-  return (FMT == FMT_BF16 && OP == OP_GELU) ? KT_MAP_TPB_GELU : kThreads;
+  return ((FMT == FMT_BF16 && OP == OP_GELU) || OP == OP_TANH_VIA_BF16) ? KT_MAP_TPB_GELU : kThreads;
 }
 #ifndef KT_UNROLL_BWD
 #define KT_UNROLL_BWD 2
