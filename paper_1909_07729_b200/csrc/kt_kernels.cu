@@ -44,7 +44,8 @@ constexpr int kChunkVecs = 32 * kUnroll;      // vectors per warp-chunk
 // cap, profiles/unroll_r02.txt): the ALU-heavier maps keep more loads in
 // flight per warp -- K-GELU BF16 and every F32 map 4 (+6% / +11% over 2);
 // K-TanH / K-Sigmoid / K-Swish BF16 and the LSTM gates 2; the fused
-// K-GELU + K-Swish pass (40 registers, 6 CTAs/SM) 1 (+6% over 2).
+// K-GELU + K-Swish pass 2 at 48 registers (5 CTAs/SM; +7% over one vector
+// at 40 registers / 6 CTAs per SM, which itself beat two vectors at 40).
 #ifndef KT_UNROLL_GELU
 #define KT_UNROLL_GELU 4
 #endif
@@ -52,7 +53,7 @@ constexpr int kChunkVecs = 32 * kUnroll;      // vectors per warp-chunk
 #define KT_UNROLL_F32 4
 #endif
 #ifndef KT_UNROLL_DUAL
-#define KT_UNROLL_DUAL 1
+#define KT_UNROLL_DUAL 2
 #endif
 template <int OP, int FMT>
 __host__ __device__ constexpr int map_unroll() {
@@ -346,7 +347,7 @@ __device__ __forceinline__ void dual_span(const uint8_t *xp, uint8_t *gp, uint8_
 }
 
 #ifndef KT_DUAL_MINB
-#define KT_DUAL_MINB 6   // 40 regs: 6 CTAs/SM (+5% on config 5, profiles/sweep_flat_r01.txt)
+#define KT_DUAL_MINB 5   // 48 regs: 5 CTAs/SM with two vectors per lane (profiles/unroll_r02.txt)
 #endif
 #ifndef KT_BWD_MINB
 #define KT_BWD_MINB 5    // 48 regs: 5 CTAs/SM (+17% on config 5 backward)
