@@ -554,12 +554,16 @@ k_lstm(const uint8_t *x, uint8_t *y, uint32_t nvec, uint32_t vpr, uint32_t vpq, 
 // gates + 64 B of c in, 64 B of c' + 32 B of h out (18 B per cell).
 // NCC: c_prev read on the non-coherent path; the launcher picks the coherent
 // instantiation when c_next == c_prev (in place), as launch_op does for x == y.
+#ifndef KT_CELL_TPB
+#define KT_CELL_TPB 256
+#endif
+constexpr int kCellTPB = KT_CELL_TPB, kCellW = KT_CELL_TPB / 32;
 #ifdef KT_CELL_MINB
 template <bool NCC>
-__global__ void __launch_bounds__(kThreads, KT_CELL_MINB)
+__global__ void __launch_bounds__(kCellTPB, KT_CELL_MINB)
 #else
 template <bool NCC>
-__global__ void __launch_bounds__(kThreads)   // (kThreads, 1) lets ptxas take > 64 regs: slower
+__global__ void __launch_bounds__(kCellTPB)   // (kThreads, 1) lets ptxas take > 64 regs: slower
 #endif
 k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_t *h_next,
             uint32_t nvec, uint32_t vpr, uint32_t hidden, uint32_t pf_blocks,
@@ -572,7 +576,7 @@ k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_
   // effect on the values later loads see.  (Round 1 tried prefetching the NEXT
   // wave's data instead: slower, 26.3 vs 20.8 us.)
   if (blockIdx.x < pf_blocks && (threadIdx.x & 31) < 5) {
-    const uint32_t v2 = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32;
+    const uint32_t v2 = (blockIdx.x * kCellW + (threadIdx.x >> 5)) * 32;
     if (v2 < nvec) {
       const uint32_t row2 = v2 / vpr, j2 = v2 - row2 * vpr;
       const uint32_t cnt = min(min(32u, nvec - v2), vpr - j2);
@@ -585,7 +589,7 @@ k_lstm_cell(const uint8_t *gates, const uint8_t *c_prev, uint8_t *c_next, uint8_
     }
   }
   pdl_enter();
-  const uint32_t v = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32 + (threadIdx.x & 31);
+  const uint32_t v = (blockIdx.x * kCellW + (threadIdx.x >> 5)) * 32 + (threadIdx.x & 31);
   const bool on = v < nvec;
   const uint32_t row = on ? v / vpr : 0, j16 = on ? v - row * vpr : 0;
   const uint8_t *gr = gates + ((size_t)row * 4 * hidden + (size_t)j16 * 16) * 2;
@@ -1108,8 +1112,8 @@ cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *
   }
   if (aligned && hidden % 16 == 0 && nvec < (1ull << 31)) {
     const uint64_t nwarps = (nvec + 31) / 32;
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, (nwarps + kWarps - 1) / kWarps);
-    static const int bps = resident_blocks(k_lstm_cell<true>);
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, (nwarps + kCellW - 1) / kCellW);
+    static const int bps = resident_blocks(k_lstm_cell<true>, kCellTPB);
     static const int pf_on = [] {
       const char *e = getenv("KT_CELL_PF");     // dev A/B: 0 = no first-wave L2 prefetch
       return e ? atoi(e) : 1;
@@ -1117,10 +1121,10 @@ cudaError_t launch_lstm_cell(const uint16_t *gates, const float *c_prev, float *
     const uint32_t pf_blocks = (pf_on && prefetch_enabled()) ? (uint32_t)(li.sm_count * bps) : 0u;
     auto kern = (static_cast<const void *>(c_next) == static_cast<const void *>(c_prev)) ? k_lstm_cell<false>
                                                                                          : k_lstm_cell<true>;
-    return launch(kern, grid, s, reinterpret_cast<const uint8_t *>(gates),
-                  reinterpret_cast<const uint8_t *>(c_prev), reinterpret_cast<uint8_t *>(c_next),
-                  reinterpret_cast<uint8_t *>(h_next), (uint32_t)nvec, (uint32_t)(hidden / 16),
-                  (uint32_t)hidden, pf_blocks, lut);
+    return launch_tpb(kern, grid, kCellTPB, s, reinterpret_cast<const uint8_t *>(gates),
+                      reinterpret_cast<const uint8_t *>(c_prev), reinterpret_cast<uint8_t *>(c_next),
+                      reinterpret_cast<uint8_t *>(h_next), (uint32_t)nvec, (uint32_t)(hidden / 16),
+                      (uint32_t)hidden, pf_blocks, lut);
   }
   static const int bps = resident_blocks(k_lstm_cell_elem);
   const unsigned grid = grid_for((n + 31) / 32, li.sm_count, bps);
