@@ -227,11 +227,7 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
         uint32_t m0, m1;
         v[u][j] = apply_word_fast<OP, FMT>(v[u][j], L, m0);
         v[u][j + 1] = apply_word_fast<OP, FMT>(v[u][j + 1], L, m1);
-#if defined(KT_TIE_SERIAL) && KT_TIE_SERIAL
-        kmin = umin16x2(umin16x2(kmin, m0), m1);          // dev A/B: serial chain
-#else
         kmin = umin16x2(kmin, umin16x2(m0, m1));          // one VIMNMX3 per two pairs
-#endif
       } else {
         v[u][j] = apply_word<OP, FMT>(v[u][j], L);
         v[u][j + 1] = apply_word<OP, FMT>(v[u][j + 1], L);
