@@ -698,3 +698,51 @@ def test_rn32_exact_sum_single_rounding():
     # the double-rounding case a plain binary64 evaluation gets wrong
     tie = (1.0 + float(np.nextafter(np.float32(1.0), np.float32(2.0)))) / 2
     assert O.rn32_exact_sum(tie, 2.0 ** -80) > 1.0 and np.float32(tie + 2.0 ** -80) == np.float32(1.0)
+
+
+# --------------------------------------------------------------------------
+# Worked examples and whole-map digests computed outside oracle/
+# (tests/golden/worked_examples.txt: SPEC.md's hand executions of Alg. 1 with
+# Table 1 rows, SURVEY.md 8(c)'s own scripts)
+# --------------------------------------------------------------------------
+def _worked(kind):
+    rows = []
+    for row in read_golden("worked_examples.txt"):
+        if row[0] == kind:
+            toks = []
+            for t in row[1:]:
+                if t.startswith("#"):
+                    break                     # inline comment
+                toks.append(t)
+            rows.append(toks)
+    return rows
+
+
+def test_worked_examples_bf16_and_f32():
+    for x, y in _worked("bf16"):
+        got = O.map_bf16("tanh", np.array([int(x, 16)], np.uint16))[0]
+        assert int(got) == int(y, 16), (x, hex(int(got)), y)
+    for x, y in _worked("f32"):
+        got = O.map_f32("tanh", np.array([int(x, 16)], np.uint32))[0]
+        assert int(got) == int(y, 16), (x, hex(int(got)), y)
+
+
+def test_whole_map_digests():
+    """SHA-256 of the full BF16 K-TanH and K-Sigmoid maps and of the F32
+    native map on inputs i << 12 (independently computed)."""
+    import hashlib
+    want = {name: digest for name, digest in _worked("sha")}
+    y = O.map_bf16("tanh", W)
+    assert hashlib.sha256(y.astype("<u2").tobytes()).hexdigest() == want["ktanh_bf16_all"]
+    s = O.map_bf16("sigmoid", W).copy()
+    s[(s & 0x7FFF) > 0x7F80] = 0x7FC0
+    assert hashlib.sha256(s.astype("<u2").tobytes()).hexdigest() == want["ksigmoid_bf16_all"]
+    x = (np.arange(1 << 20, dtype=np.uint64) << 12).astype(np.uint32)
+    f = O.map_f32("tanh", x)
+    assert hashlib.sha256(f.astype("<u4").tobytes()).hexdigest() == want["ktanh_f32_i12"]
+
+
+def test_bounds_hand_values():
+    """Sec. 2.4 bounds at the two corners SPEC.md works by hand."""
+    for r, v, lo, hi in _worked("bounds"):
+        assert O.bounds(int(r), int(v)) == (int(lo), int(hi))
