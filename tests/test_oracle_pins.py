@@ -746,3 +746,22 @@ def test_bounds_hand_values():
     """Sec. 2.4 bounds at the two corners SPEC.md works by hand."""
     for r, v, lo, hi in _worked("bounds"):
         assert O.bounds(int(r), int(v)) == (int(lo), int(hi))
+
+
+def test_derived_max_errors_match_survey():
+    """The derived maps' maximum errors against the functions they approximate
+    equal SURVEY.md 8(c)'s independent computation to its printed digits."""
+    ex = _survey_exact()
+    fin = FINITE
+    with np.errstate(over="ignore", invalid="ignore"):
+        s = O.bf16_to_f64(O.map_bf16("sigmoid", W))
+        e = np.where(fin, np.abs(s - 1 / (1 + np.exp(-XV))), 0.0)
+        i = int(np.argmax(e))
+        assert round(float(e[i]), 6) == float(ex["sigmoid_max_err"][0]) and i == int(ex["sigmoid_argmax"][0], 16)
+        m5 = fin & (np.abs(XV) <= 5)
+        x = XV[m5]
+        g = O.bf16_to_f64(O.map_bf16("gelu", W))[m5]
+        exact = np.array([v / 2 * (1 + math.erf(v / math.sqrt(2))) for v in x])
+        assert round(float(np.max(np.abs(g - exact))), 5) == float(ex["gelu_exact_max_err_abs5"][0])
+        sw = O.bf16_to_f64(O.map_bf16("swish", W))[m5]
+        assert round(float(np.max(np.abs(sw - x / (1 + np.exp(-x))))), 4) == float(ex["swish_max_err_abs5"][0])
