@@ -67,6 +67,29 @@ def test_ktanh_bf16_past_2p32_misaligned(kt):
                     ctx="ktanh_bf16 n > 2^32")
 
 
+def test_kgelu_bf16_past_2p32_misaligned(kt):
+    """K-GELU BF16 takes its own launch shape (4 vectors per lane, 128-thread
+    CTAs) and the tie screen: past 2^32 elements, from an odd element offset."""
+    n = (1 << 32) + (1 << 20) + 5
+    base = rand_bf16(n + 3, 11)
+    x = base[3:]
+    y = kt.kgelu_bf16(x)
+    idx = sample_idx(n, seed=11)
+    assert_bitexact(bits16(take(y, idx)), O.map_bf16("gelu", bits16(take(x, idx))), 16,
+                    nan_by_class=True, zero_by_value=True, ctx="kgelu_bf16 n > 2^32")
+
+
+def test_ktanh_f32_via_bf16_past_2p31(kt):
+    """The F32-through-BF16 map (128-thread CTAs, 4 vectors per lane) past 2^31."""
+    n = (1 << 31) + 13
+    g = torch.Generator(device="cuda").manual_seed(12)
+    x = torch.randn(n, device="cuda", generator=g).mul_(3)
+    y = kt.ktanh_f32_via_bf16(x)
+    idx = sample_idx(n, seed=12)
+    assert_bitexact(bits32(take(y, idx)), O.map_f32("tanh_via_bf16", bits32(take(x, idx))), 32,
+                    nan_by_class=True, ctx="ktanh_f32_via_bf16 n > 2^31")
+
+
 def test_ksigmoid_f32_past_2p31(kt):
     n = (1 << 31) + 9
     g = torch.Generator(device="cuda").manual_seed(2)

@@ -1,7 +1,3 @@
 set -x
-R=$GRAFT_REPO_ROOT
-for rep in 1 2; do for v in default ct128 ct128m9 ct128m10 ct64m18; do
-  unset KT_LIB; [ $v != default ] && export KT_LIB=$R/abtmp/lib_$v.so
-  echo "{\"variant\": \"$v\"}" >> gpurun_out/ab_r02s.jsonl
-  timeout 400 python tools/ab_stream.py c4_lstm_gates:lstm_cell >> gpurun_out/ab_r02s.jsonl 2>> gpurun_out/ab_r02s.err
-done; done
+timeout 1200 python -m pytest tests/test_gpu_large.py -q -p no:cacheprovider > gpurun_out/gputest_r02t.log 2>&1
+tail -3 gpurun_out/gputest_r02t.log
