@@ -148,7 +148,7 @@ class Step:
         es = self.cfg.elem_bytes
         self.bwd = "_bwd_" in op
         self.cell = op == "lstm_cell"
-        self.dual = op == "kgelu_swish_bf16"
+        self.dual = op in ("kgelu_swish_bf16", "kgelu_swish_f32")
         # algorithmic bytes: read x (+ dy for a backward) + write y
         self.bytes_per_step = (3 if self.bwd else 2) * n * es
         if self.cell:   # gates 8 B + c 4 B in, c' 4 B + h 2 B out per cell (n/4 cells)
@@ -208,7 +208,7 @@ class Step:
         elif self.bwd:
             getattr(self.kt, self.op)(self.xs[s], self.ds[s], out=self.ys[s])
         elif self.dual:
-            self.kt.kgelu_swish_bf16(self.xs[s], out_gelu=self.ys[s], out_swish=self.y2s[s])
+            getattr(self.kt, self.op)(self.xs[s], out_gelu=self.ys[s], out_swish=self.y2s[s])
         else:
             self.fn(self.xs[s], self.ys[s])
 

@@ -184,15 +184,20 @@ __device__ __forceinline__ uint32_t ktanh64_bf16x2(uint32_t x, uint32_t w0, uint
 // bypass (|x| < T1 or NaN) is ONE unsigned range test
 // (u2 - 2 T1) > (2 inf - 2 T1); the sign is ORed in once after the
 // saturation select.  6 ALU-pipe ops instead of 10.
-__device__ __forceinline__ uint32_t ktanh_f32(uint32_t u, uint32_t lk, uint32_t lc) {
+__device__ __forceinline__ uint32_t ktanh_f32(uint32_t u, uint32_t lk, uint32_t lc, uint32_t &u2out) {
   const uint32_t K = shfl_lut(lk, u >> 20);        // line 6-7, t = bits [24:20]
   const uint32_t C = shfl_lut(lc, u >> 20);
   const uint32_t u2 = u << 1;
+  u2out = u2;                                      // |x| << 1 (the tie screen's key)
   const uint32_t ym = __umulhi(u2, K) + C;         // line 8: C_t + (|x| >> r_t)
   uint32_t y = (u2 > (kT2f << 1)) ? 0x3F800000u : ym;                  // line 4
   y |= u & 0x80000000u;                                                // s_o = s_i
   const bool byp = (u2 - (kT1f << 1)) > ((kInff << 1) - (kT1f << 1));  // line 3, or NaN (A6)
   return byp ? u : y;
+}
+__device__ __forceinline__ uint32_t ktanh_f32(uint32_t u, uint32_t lk, uint32_t lc) {
+  uint32_t u2;
+  return ktanh_f32(u, lk, lc, u2);
 }
 
 // ------------------------------------------------------- derived (Sec. 1) --
@@ -350,6 +355,31 @@ __device__ __forceinline__ uint32_t kgelu_f32(uint32_t u, uint32_t lk, uint32_t 
   return __float_as_uint(outer_exact_f32(x, hx, t));
 }
 
+// F32 streaming forms with the tie screen (as for BF16): the plain fma, and
+// key = |argument| << 1 from the core; a key below 2^-125 << 1 (or a zero)
+// sends the warp's chunk through tie_patch_f32.
+constexpr uint32_t kTieKeyF32 = 0x01000000u << 1;   // (2^-125 bits) << 1
+__device__ __forceinline__ uint32_t kswish_f32_fast(uint32_t u, uint32_t lk, uint32_t lc, uint32_t &key) {
+  const float hx = __fmul_rn(__uint_as_float(u), 0.5f);
+  const float t = __uint_as_float(ktanh_f32(__float_as_uint(hx), lk, lc, key));
+  return __float_as_uint(__fmaf_rn(hx, t, hx));
+}
+__device__ __forceinline__ uint32_t kgelu_f32_fast(uint32_t u, uint32_t lk, uint32_t lc, uint32_t &key) {
+  const float x = __uint_as_float(u);
+  const float t = __uint_as_float(ktanh_f32(__float_as_uint(gelu_arg(x)), lk, lc, key));
+  const float hx = __fmul_rn(x, 0.5f);
+  return __float_as_uint(__fmaf_rn(hx, t, hx));
+}
+// closed form for |x| < 2^-125 (bits m < 0x01000000 linear in 2^-149 units),
+// as tie_patch for BF16
+template <int OP>
+__device__ __forceinline__ uint32_t tie_patch_f32(uint32_t x, uint32_t y) {
+  const uint32_t m = x & 0x7FFFFFFFu, s = x & 0x80000000u;
+  if (m >= 0x01000000u) return y;
+  const uint32_t inc = (s == 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;
+  return s | ((m + inc) >> 1);
+}
+
 // ------------------------------------------------------- backward (NEXT-1) --
 // Reading R-BWD: derivative of the approximated function, taken
 // through the K-TanH value; fp32 with a fixed op order, one rounding to the
@@ -482,12 +512,40 @@ template <int OP, int FMT>
 __device__ __forceinline__ uint32_t apply_word_fast(uint32_t w, const LaneLut &L, uint32_t &mag) {
   mag = 0xFFFFFFFFu;
   if (FMT == FMT_BF16) return apply_bf16x2_fast<OP>(w, L, mag);
+#if KT_TIE_MODE != 1
+  uint32_t k = 0xFFFFFFFFu, r;
+  if (OP == OP_SWISH) r = kswish_f32_fast(w, L.k32, L.c32, k);
+  else if (OP == OP_GELU) r = kgelu_f32_fast(w, L.k32, L.c32, k);
+  else r = apply_f32<OP>(w, L);
+  if (KT_TIE_MODE == 0) mag = k;
+  return r;
+#else
   return apply_f32<OP>(w, L);
+#endif
+}
+// the tie screen's running minimum and test, per format: BF16 keys are two
+// packed u16 magnitudes, F32 keys one |argument| << 1
+template <int FMT>
+__device__ __forceinline__ uint32_t key_min(uint32_t a, uint32_t b) {
+  return FMT == FMT_BF16 ? umin16x2(a, b) : (a < b ? a : b);
+}
+template <int FMT>
+__device__ __forceinline__ bool tie_possible_fmt(uint32_t kmin) {
+  return FMT == FMT_BF16 ? tie_possible(kmin) : kmin < kTieKeyF32;
+}
+// closed-form patch of one word (x in, plain-fma y in) for the format
+template <int OP, int FMT>
+__device__ __forceinline__ uint32_t tie_patch_word(uint32_t x, uint32_t y) {
+  return FMT == FMT_BF16 ? tie_patch<OP>(x, y) : tie_patch_f32<OP>(x, y);
+}
+template <int FMT>
+__device__ __forceinline__ bool tie_word_candidate(uint32_t w) {   // some |x| < 2^-125 in the word
+  return FMT == FMT_BF16 ? ((w & 0x7F00u) == 0 || (w & 0x7F000000u) == 0) : (w & 0x7F000000u) == 0;
 }
 // does apply_word_fast need the tie screen for this op/format?
 template <int OP, int FMT>
 __host__ __device__ constexpr bool needs_tie_screen() {
-  return FMT == FMT_BF16 && (OP == OP_SWISH || OP == OP_GELU);
+  return OP == OP_SWISH || OP == OP_GELU;
 }
 
 template <int OP, int FMT>

@@ -55,9 +55,13 @@ constexpr int kChunkVecs = 32 * kUnroll;      // vectors per warp-chunk
 #ifndef KT_UNROLL_DUAL
 #define KT_UNROLL_DUAL 2
 #endif
+#ifndef KT_UNROLL_F32D
+#define KT_UNROLL_F32D 4
+#endif
 template <int OP, int FMT>
 __host__ __device__ constexpr int map_unroll() {
-  return FMT == FMT_F32 ? KT_UNROLL_F32 : (OP == OP_GELU ? KT_UNROLL_GELU : kUnroll);
+  return FMT == FMT_F32 ? ((OP == OP_SWISH || OP == OP_GELU) ? KT_UNROLL_F32D : KT_UNROLL_F32)
+                        : (OP == OP_GELU ? KT_UNROLL_GELU : kUnroll);
 }
 template <int FMT>
 __host__ __device__ constexpr int dual_unroll() {
@@ -140,7 +144,7 @@ __device__ __forceinline__ void scalar_span(const uint8_t *xp, uint8_t *yp, uint
 // BF16 pairs with |x| < 2^-125 from the closed form.  Out of line and word by
 // word so that it costs the streaming kernels no registers; plain (coherent)
 // loads see the lane's own preceding stores.  Out-of-place calls only.
-template <int OP, int U>
+template <int OP, int FMT, int U>
 __device__ __noinline__ void tie_fixup(const uint8_t *xb, uint8_t *yb, uint64_t base, uint64_t nvec) {
 #pragma unroll 1
   for (int u = 0; u < U; ++u) {
@@ -151,12 +155,12 @@ __device__ __noinline__ void tie_fixup(const uint8_t *xb, uint8_t *yb, uint64_t 
 #pragma unroll 1
     for (int j = 0; j < 8; ++j) {
       const uint32_t w = xs[j];
-      if ((w & 0x7F00u) == 0 || (w & 0x7F000000u) == 0) ys[j] = tie_patch<OP>(w, ys[j]);
+      if (tie_word_candidate<FMT>(w)) ys[j] = tie_patch_word<OP, FMT>(w, ys[j]);
     }
   }
 }
 
-template <int U>
+template <int FMT, int U>
 __device__ __noinline__ void tie_fixup_dual(const uint8_t *xb, uint8_t *gb, uint8_t *sb, uint64_t base,
                                             uint64_t nvec) {
 #pragma unroll 1
@@ -169,9 +173,9 @@ __device__ __noinline__ void tie_fixup_dual(const uint8_t *xb, uint8_t *gb, uint
 #pragma unroll 1
     for (int j = 0; j < 8; ++j) {
       const uint32_t w = xs[j];
-      if ((w & 0x7F00u) == 0 || (w & 0x7F000000u) == 0) {
-        gs[j] = tie_patch<OP_GELU>(w, gs[j]);
-        ss[j] = tie_patch<OP_SWISH>(w, ss[j]);
+      if (tie_word_candidate<FMT>(w)) {
+        gs[j] = tie_patch_word<OP_GELU, FMT>(w, gs[j]);
+        ss[j] = tie_patch_word<OP_SWISH, FMT>(w, ss[j]);
       }
     }
   }
@@ -227,7 +231,7 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
         uint32_t m0, m1;
         v[u][j] = apply_word_fast<OP, FMT>(v[u][j], L, m0);
         v[u][j + 1] = apply_word_fast<OP, FMT>(v[u][j + 1], L, m1);
-        kmin = umin16x2(kmin, umin16x2(m0, m1));          // one VIMNMX3 per two pairs
+        kmin = key_min<FMT>(kmin, key_min<FMT>(m0, m1));  // one 3-input min per two words
       } else {
         v[u][j] = apply_word<OP, FMT>(v[u][j], L);
         v[u][j + 1] = apply_word<OP, FMT>(v[u][j + 1], L);
@@ -242,8 +246,8 @@ k_map(const uint8_t *x, uint8_t *y, uint32_t head, uint64_t nvec, uint32_t tail,
     const uint64_t i = base + (uint64_t)u * 32;
     st256(yb + i * kVecBytes, v[u], i < nvec);
   }
-  if (kScreen && __any_sync(0xffffffffu, tie_possible(kmin)))
-    tie_fixup<OP, U>(xb, yb, base, nvec);   // rare: an |argument| < 2^-125 (or a zero) in the chunk
+  if (kScreen && __any_sync(0xffffffffu, tie_possible_fmt<FMT>(kmin)))
+    tie_fixup<OP, FMT, U>(xb, yb, base, nvec);   // rare: an |argument| < 2^-125 (or a zero) in the chunk
   if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
     scalar_span<OP, FMT>(x, y, head, L);
     const size_t toff = ((size_t)head + (size_t)nvec * (kVecBytes / es)) * es;
@@ -382,7 +386,7 @@ k_dual(const uint8_t *x, uint8_t *yg, uint8_t *ys, uint32_t head, uint64_t nvec,
         uint32_t m, munused;
         g[j] = apply_word_fast<OP_GELU, FMT>(v[u][j], L, m);
         sw[j] = apply_word_fast<OP_SWISH, FMT>(v[u][j], L, munused);
-        kmin = umin16x2(kmin, m);
+        kmin = key_min<FMT>(kmin, m);
       } else {
         g[j] = apply_word<OP_GELU, FMT>(v[u][j], L);
         sw[j] = apply_word<OP_SWISH, FMT>(v[u][j], L);
@@ -392,8 +396,8 @@ k_dual(const uint8_t *x, uint8_t *yg, uint8_t *ys, uint32_t head, uint64_t nvec,
     st256(yg + hb + i * kVecBytes, g, i < nvec);
     st256(ys + hb + i * kVecBytes, sw, i < nvec);
   }
-  if (kScreen && __any_sync(0xffffffffu, tie_possible(kmin)))
-    tie_fixup_dual<U>(x + hb, yg + hb, ys + hb, base, nvec);   // rare
+  if (kScreen && __any_sync(0xffffffffu, tie_possible_fmt<FMT>(kmin)))
+    tie_fixup_dual<FMT, U>(x + hb, yg + hb, ys + hb, base, nvec);   // rare
   if ((head | tail) != 0 && blockIdx.x == 0 && threadIdx.x < 32) {
     dual_span<FMT>(x, yg, ys, head, L);
     const size_t toff = ((size_t)head + (size_t)nvec * (kVecBytes / es)) * es;

@@ -810,6 +810,31 @@ def test_bf16_isolated_ties_exact(kt, op):
     check("swish", "bf16", u16(sw), oracle_bf16("swish", bits), "dual swish isolated ties")
 
 
+@pytest.mark.parametrize("op", DERIVED)
+def test_f32_isolated_ties_exact(kt, op):
+    """F32 K-Swish / K-GELU stream with the same tie screen as BF16 (an
+    |argument| << 1 minimum per warp): each x/2-tie input (|x| < 2^-125, odd
+    last bit; 512 of them incl. the largest, 0x00FFFFFF, and the smallest)
+    ALONE in its warp's chunk among ordinary values, single op and fused pass."""
+    rng = np.random.default_rng(31)
+    odd = np.concatenate([[1, 3, 5, 0x7FFFFF, 0x800001, 0xFFFFFD, 0xFFFFFF],
+                          rng.integers(0, 1 << 23, 249) * 2 + 1]).astype(np.uint32)
+    ties = np.concatenate([odd, odd | np.uint32(0x80000000)])
+    span = 8192
+    base = (rng.standard_normal(ties.size * span) * 2 + 3).astype(np.float32).view(np.uint32).copy()
+    for k, w in enumerate(ties):
+        base[k * span + (k * 613) % span] = w
+    x = torch.from_numpy(base.view(np.int32)).cuda().view(torch.float32)
+    want = O.map_f32(op, base)
+    check(op, "f32", u32(call(kt, op, "f32", x)), want, f"{op} f32 isolated ties")
+    xi = x.clone()                       # in place: the branch-free exact outer step
+    call(kt, op, "f32", xi, out=xi)
+    check(op, "f32", u32(xi), want, f"{op} f32 isolated ties in place")
+    g, sw = kt.kgelu_swish_f32(x)
+    check("gelu", "f32", u32(g), O.map_f32("gelu", base), "dual f32 gelu isolated ties")
+    check("swish", "f32", u32(sw), O.map_f32("swish", base), "dual f32 swish isolated ties")
+
+
 def test_binding_validates_caller_outputs(kt):
     """every caller-supplied output is checked (dtype, size, device,
     layout) before its pointer reaches the C ABI, which cannot bound-check it."""

@@ -43,8 +43,8 @@ MUTANTS = [
     ("64-entry half select", D, "const uint32_t Ll = (x & 0x100u) ? l1 : l0;",
      "const uint32_t Ll = (x & 0x80u) ? l1 : l0;", PARITY),
     ("gemm epilogue column order", G,
-     "o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j])), lw);",
-     "o0[j] = epi_word<EPI>(pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), lw);",
+     "w0[j] = pack_bf16x2(__uint_as_float(r[2 * j + 1]), __uint_as_float(r[2 * j]));",
+     "w0[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));",
      "tests/test_gpu_gemm.py"),
     ("gemm cell gate order", G,
      "const uint32_t gf = pack_bf16x2(__uint_as_float(r[32 + 2 * k + 1]), __uint_as_float(r[32 + 2 * k]));",
@@ -67,16 +67,20 @@ MUTANTS = [
     ("pade comparator saturation", APX, "return a >= w.xsat ? 1.0f : y;", "return a > 2.0f * w.xsat ? 1.0f : y;",
      "tests/test_gpu_apx.py"),
     # round 2: the exact outer step (R-DERIVED) and the per-kernel unroll
-    ("tie patch direction", D, "const uint32_t inc = (s == 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;",
-     "const uint32_t inc = (s != 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;", PARITY),
+    ("tie patch direction", D, "      const uint32_t inc = (s == 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;",
+     "      const uint32_t inc = (s != 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;", PARITY),
+    ("f32 tie patch direction", D, "\n  const uint32_t inc = (s == 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;",
+     "\n  const uint32_t inc = (s != 0 && (OP == OP_GELU || m >= 2)) ? 1u : 0u;", PARITY),
     ("tie screen threshold", D, "return (kmin & 0xFF00u) == 0 || (kmin & 0xFF000000u) == 0;",
      "return (kmin & 0xFF80u) == 0 || (kmin & 0xFF800000u) == 0;", PARITY),
     ("outer_exact rounds both ways", D,
      "const uint32_t up = hset2_gt(r, 0u) & hset2_ne(t, 0u) & kOnex2;     // 1.0 where the t-term rounds up",
      "const uint32_t up = hset2_ne(r, 0u) & hset2_ne(t, 0u) & kOnex2;", PARITY),
     ("f32 outer tie ignored", D, "const float c = (r > 0.0f && t != 0.0f) ? __fadd_rn(hx, r) : hx;",
-     "const float c = hx;", "tests/test_gpu_exhaustive_f32.py"),
-    ("dual tie fix-up dropped", KK, "    tie_fixup_dual<U>(x + hb, yg + hb, ys + hb, base, nvec);   // rare",
+     "const float c = hx;", PARITY),
+    ("f32 tie screen threshold", D, "constexpr uint32_t kTieKeyF32 = 0x01000000u << 1;",
+     "constexpr uint32_t kTieKeyF32 = 0x00800000u << 1;", PARITY),
+    ("dual tie fix-up dropped", KK, "    tie_fixup_dual<FMT, U>(x + hb, yg + hb, ys + hb, base, nvec);   // rare",
      "    (void)0;", PARITY),
     ("map grid for a larger chunk", KK,
      "  const uint64_t nchunks = (nvec + 32 * U - 1) / (32 * U);\n  if (nchunks / kW >= 0x7FFFFFFFull)",
