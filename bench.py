@@ -700,20 +700,21 @@ def oracle_check(x, y, op, m=1 << 16, seed=0, stub=False):
     else:
         import oracle as O
         want = O.map_bf16(op, xs) if bf16 else O.map_f32(op, xs)
-    bits = 16 if bf16 else 32
-    mag = (1 << (bits - 1)) - 1
+    return mismatches(ys, want, op, bf16), int(idx.size)
 
-    def isnan(w):
-        return (w.astype(np.int64) & mag) > (0x7F80 if bf16 else 0x7F800000)
-    def iszero(w):
-        return (w.astype(np.int64) & mag) == 0
 
-    bad = ys != want
+def mismatches(got, want, op, bf16):
+    """Elements of got != want, NaN compared by class (not for K-TanH: it
+    passes NaN through unchanged) and +-0 by value for K-Swish / K-GELU."""
+    mag = 0x7FFF if bf16 else 0x7FFFFFFF
+    nan_lo = 0x7F80 if bf16 else 0x7F800000
+    g, w = got.astype(np.int64) & mag, want.astype(np.int64) & mag
+    bad = got != want
     if op != "tanh":
-        bad &= ~(isnan(ys) & isnan(want))
+        bad &= ~((g > nan_lo) & (w > nan_lo))
     if op in ("swish", "gelu"):
-        bad &= ~(iszero(ys) & iszero(want))
-    return int(bad.sum()), int(idx.size)
+        bad &= ~((g == 0) & (w == 0))
+    return int(bad.sum())
 
 
 def full_shard_check(x, y, op):
@@ -729,21 +730,11 @@ def full_shard_check(x, y, op):
     n = xs.size
     nthr = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     step = 1 << 22
-    bits = 16 if bf16 else 32
-    mag = (1 << (bits - 1)) - 1
-    nan_lo = 0x7F80 if bf16 else 0x7F800000
 
     def part(a):
         b = min(n, a + step)
         want = O.map_bf16(op, xs[a:b]) if bf16 else O.map_f32(op, xs[a:b])
-        got = ys[a:b]
-        bad = got != want
-        g64, w64 = got.astype(np.int64), want.astype(np.int64)
-        if op != "tanh":
-            bad &= ~(((g64 & mag) > nan_lo) & ((w64 & mag) > nan_lo))
-        if op in ("swish", "gelu"):
-            bad &= ~(((g64 & mag) == 0) & ((w64 & mag) == 0))
-        return int(bad.sum())
+        return mismatches(ys[a:b], want, op, bf16)
     t0 = time.perf_counter()
     with ThreadPoolExecutor(nthr) as pool:
         bad = sum(pool.map(part, range(0, n, step)))

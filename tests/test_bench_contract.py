@@ -106,3 +106,21 @@ def test_traffic_is_read_per_workload_from_committed_captures():
         assert t is not None and f"_{key}_{op}_r" in src, (key, op, src)
         assert 0.98 * a <= t <= 1.02 * a, (key, op, t, a)
     assert bench.load_traffic("c5_ffn_2p30", "no_such_call") == (None, None)
+
+
+def test_bench_mismatch_rule():
+    """bench.py's per-rank oracle check compares bit-exactly, NaN by class
+    except for K-TanH (which passes NaN bits through), +-0 by value for the
+    derived ops only."""
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    w = np.array([0x7FC0, 0x8000, 0x3F80], np.uint16)
+    g = np.array([0x7FC1, 0x0000, 0x3F80], np.uint16)
+    assert bench.mismatches(g, w, "gelu", True) == 0
+    assert bench.mismatches(g, w, "sigmoid", True) == 1        # -0 vs +0 counts outside swish/gelu
+    assert bench.mismatches(g, w, "tanh", True) == 2           # NaN payload and zero sign both count
+    wf = np.array([0x7FC00000, 0x80000000], np.uint32)
+    gf = np.array([0xFFC00000, 0x00000000], np.uint32)
+    assert bench.mismatches(gf, wf, "swish", False) == 0
+    assert bench.mismatches(gf + np.uint32(1), wf, "swish", False) == 1   # 0x00000001 is not zero
