@@ -1,5 +1,5 @@
 set -x
-timeout 900 python -m pytest tests/test_bench_contract.py -q -p no:cacheprovider > gpurun_out/gputest_r02x.log 2>&1
-tail -2 gpurun_out/gputest_r02x.log
-timeout 900 python bench.py --no-extra --full-check > gpurun_out/bench_fullcheck_r02b.json 2> gpurun_out/bench_fullcheck_r02b.err
-python -c "import json;d=json.loads(open('gpurun_out/bench_fullcheck_r02b.json').read().strip().splitlines()[-1]);print(d['value'], d['roofline']['frac'], d['per_rank'], d['clocks'])"
+for c in c1 c2 c3 c4; do
+  timeout 600 python bench.py --config $c --no-extra --steps 50 > gpurun_out/bench_cfg_$c.json 2> gpurun_out/bench_cfg_$c.err; echo "$c rc=$?"
+  python -c "import json;d=json.loads(open('gpurun_out/bench_cfg_$c.json').read().strip().splitlines()[-1]);print('$c', d['value'], d['roofline']['frac'], d['roofline']['traffic'], d['e2e']['value'], d['config']['l2'])"
+done
