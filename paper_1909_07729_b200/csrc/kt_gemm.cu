@@ -90,6 +90,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t *r) {
       : "r"(taddr));
 }
 
+// 8 consecutive TMEM columns of this warp's 32 lanes -> r[0..7] (async)
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t *r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+}
+
 // Epilogue id for the LSTM gate block (config 4): K-TanH on the tanh
 // quarter's columns, K-Sigmoid elsewhere; the quarter is uniform per tile
 // (hidden % 256 == 0), so each tile resolves to OP_TANH or OP_SIGMOID.
@@ -170,6 +178,14 @@ __device__ __forceinline__ void epi_tile_chunk(const uint32_t *r, uint32_t (&o0)
 // tmem_full[2] (MMA -> epilogue), tmem_empty[2] (epilogue -> MMA, 8 arrivals).
 constexpr int kEpiWarps = 8;
 constexpr int kGemmPThreads = 64 + 32 * kEpiWarps;
+// LSTM cell epilogue warps: each warp of a TMEM lane quarter takes 64 / (W/4)
+// hidden units of the tile in rounds of 8 (4 x 8 TMEM columns, 123 registers
+// at W = 8, no spills; profiles/gemm_cell_epi_r02.txt).  W = 16 (88
+// registers) was 4% slower on the fused step (dev A/B: -DKT_GEMM_CELL_WARPS=16).
+#ifndef KT_GEMM_CELL_WARPS
+#define KT_GEMM_CELL_WARPS 8
+#endif
+static_assert(KT_GEMM_CELL_WARPS == 8 || KT_GEMM_CELL_WARPS == 16, "cell epilogue: 8 or 16 warps");
 constexpr int kGroupM = 16;
 
 __device__ __forceinline__ void tile_coords(uint32_t t, uint32_t mt, uint32_t ntiles_n, uint32_t &mb,
@@ -218,6 +234,10 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
 }
 
 constexpr int kEpiCell = 9;   // the LSTM cell epilogue (see kgemm_lstm_cell_bf16)
+template <int EPI>
+__host__ __device__ constexpr int epi_warps() { return EPI == kEpiCell ? KT_GEMM_CELL_WARPS : kEpiWarps; }
+template <int EPI>
+__host__ __device__ constexpr int gemm_threads() { return 64 + 32 * epi_warps<EPI>(); }
 
 struct GemmArgs {
   uint16_t *C;                 // output of the activation epilogues (unused for the cell)
@@ -258,40 +278,31 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
         : "memory");
 }
 
-// LSTM cell of this thread's row for 32 hidden units: r = gates i, f, g, o
-// (32 TMEM columns each), cp = c_prev (32 floats) -> c_next, h_next.
-__device__ __forceinline__ void cell_epilogue(const uint32_t *r, const uint32_t (&cp)[4][8],
-                                              float *c_next, uint16_t *h_next, size_t cbase,
-                                              const LaneLut &L) {
-  uint32_t cn[4][8], h[16];
+// LSTM cell of this thread's row for 8 hidden units: r = gates i, f, g, o (8
+// TMEM columns each), cp = c_prev (8 floats) -> c_next, h_next.
+__device__ __forceinline__ void cell_epilogue8(const uint32_t *r, const uint32_t (&cp)[8], float *c_next,
+                                               uint16_t *h_next, size_t cbase, const LaneLut &L) {
+  uint32_t cn[8], h[4];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {                                    // units 2k, 2k + 1
+  for (int k = 0; k < 4; ++k) {                                     // units 2k, 2k + 1
     const uint32_t gi = pack_bf16x2(__uint_as_float(r[2 * k + 1]), __uint_as_float(r[2 * k]));
-    const uint32_t gf = pack_bf16x2(__uint_as_float(r[32 + 2 * k + 1]), __uint_as_float(r[32 + 2 * k]));
-    const uint32_t gg = pack_bf16x2(__uint_as_float(r[64 + 2 * k + 1]), __uint_as_float(r[64 + 2 * k]));
-    const uint32_t go = pack_bf16x2(__uint_as_float(r[96 + 2 * k + 1]), __uint_as_float(r[96 + 2 * k]));
+    const uint32_t gf = pack_bf16x2(__uint_as_float(r[8 + 2 * k + 1]), __uint_as_float(r[8 + 2 * k]));
+    const uint32_t gg = pack_bf16x2(__uint_as_float(r[16 + 2 * k + 1]), __uint_as_float(r[16 + 2 * k]));
+    const uint32_t go = pack_bf16x2(__uint_as_float(r[24 + 2 * k + 1]), __uint_as_float(r[24 + 2 * k]));
     float2 cnv;
-    h[k] = lstm_cell2(gi, gf, gg, go,
-                      make_float2(__uint_as_float(cp[k >> 2][(2 * k) & 7]),
-                                  __uint_as_float(cp[k >> 2][(2 * k + 1) & 7])),
+    h[k] = lstm_cell2(gi, gf, gg, go, make_float2(__uint_as_float(cp[2 * k]), __uint_as_float(cp[2 * k + 1])),
                       cnv, L);
-    cn[k >> 2][(2 * k) & 7] = __float_as_uint(cnv.x);
-    cn[k >> 2][(2 * k + 1) & 7] = __float_as_uint(cnv.y);
+    cn[2 * k] = __float_as_uint(cnv.x);
+    cn[2 * k + 1] = __float_as_uint(cnv.y);
   }
-#pragma unroll
-  for (int v = 0; v < 4; ++v) st256(c_next + cbase + 8 * v, cn[v], true);
-  uint32_t h0[8], h1[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    h0[j] = h[j];
-    h1[j] = h[8 + j];
-  }
-  st256(h_next + cbase, h0, true);
-  st256(h_next + cbase + 16, h1, true);
+  st256(c_next + cbase, cn, true);
+  asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(h_next + cbase), "r"(h[0]),
+               "r"(h[1]), "r"(h[2]), "r"(h[3])
+               : "memory");
 }
 
 template <int EPI, int CTAS>
-__global__ void __launch_bounds__(kGemmPThreads, 1)
+__global__ void __launch_bounds__(gemm_threads<EPI>(), 1)
 k_gemm_t(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
          const GemmArgs g, const __grid_constant__ LutWords lut) {
   using Sh = GemmShape<CTAS>;
@@ -320,7 +331,7 @@ k_gemm_t(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUte
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar + 8 * a, 1);
-      mbar_init(tempty_bar + 8 * a, CTAS * kEpiWarps);
+      mbar_init(tempty_bar + 8 * a, CTAS * epi_warps<EPI>());
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -422,23 +433,28 @@ k_gemm_t(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUte
       const uint32_t a = i & 1;
       const uint32_t row = mb * 128 * CTAS + rank * 128 + 32 * q + lane;
       if (kCell) {
-        const size_t cbase = (size_t)row * g.H + nb * 64 + half * 32;
+        constexpr int kParts = epi_warps<EPI>() / 4, kUnits = 64 / kParts, kRounds = kUnits / 8;
+        const uint32_t part = (warp - 2) >> 2;                      // kUnits hidden units of the tile
+        const size_t cbase = (size_t)row * g.H + nb * 64 + part * kUnits;
         // c_prev, before the wait.  Non-coherent loads are safe even when
-        // c_next == c_prev: the only write to these 32 elements is this
+        // c_next == c_prev: the only write to these elements is this
         // thread's own c' store, issued after this read; other threads may
         // write other elements of the same lines, which this read never uses.
-        uint32_t cp[4][8];
+        uint32_t cp[kRounds][8];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) ld256<true>(g.c_prev + cbase + 8 * v, cp[v], true);
+        for (int v = 0; v < kRounds; ++v) ld256<true>(g.c_prev + cbase + 8 * v, cp[v], true);
         mbar_wait(tfull_bar + 8 * a, (i / 2) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint32_t r[128];                                            // i, f, g, o x 32 units
-        const uint32_t tbase = tmem + ((32 * q) << 16) + a * kTmemCols + half * 32;
+        const uint32_t tbase = tmem + ((32 * q) << 16) + a * kTmemCols + part * kUnits;
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq) tmem_ld32(tbase + 64 * gq, r + 32 * gq);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        release(a);
-        cell_epilogue(r, cp, g.c_next, g.h_next, cbase, L);
+        for (int rd = 0; rd < kRounds; ++rd) {
+          uint32_t r[32];                                           // i, f, g, o x 8 units
+#pragma unroll
+          for (int gq = 0; gq < 4; ++gq) tmem_ld8(tbase + 64 * gq + 8 * rd, r + 8 * gq);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (rd == kRounds - 1) release(a);
+          cell_epilogue8(r, cp[rd], g.c_next, g.h_next, cbase + 8 * rd, L);
+        }
         continue;
       }
       mbar_wait(tfull_bar + 8 * a, (i / 2) & 1);
@@ -567,7 +583,7 @@ static cudaError_t launch_t(const CUtensorMap &ma, const CUtensorMap &mb, const 
   const unsigned grid = (unsigned)(CTAS * (tiles < units ? tiles : units));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemmPThreads);
+  cfg.blockDim = dim3(gemm_threads<EPI>());
   cfg.dynamicSmemBytes = Sh::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
