@@ -177,7 +177,6 @@ __device__ __forceinline__ void epi_tile_chunk(const uint32_t *r, uint32_t (&o0)
 // tile i + 1.  Barriers: smem ring full/empty (continuous across tiles),
 // tmem_full[2] (MMA -> epilogue), tmem_empty[2] (epilogue -> MMA, 8 arrivals).
 constexpr int kEpiWarps = 8;
-constexpr int kGemmPThreads = 64 + 32 * kEpiWarps;
 // LSTM cell epilogue warps: each warp of a TMEM lane quarter takes 64 / (W/4)
 // hidden units of the tile in rounds of 8 (4 x 8 TMEM columns, 123 registers
 // at W = 8, no spills; profiles/gemm_cell_epi_r02.txt).  W = 16 (88
