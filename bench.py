@@ -439,7 +439,8 @@ KERNEL_NAME = {"ktanh_bf16": "kt::k_map<0, 0, 1, 1, 2, 256>", "ktanh_f32": "kt::
                "kgelu_bf16": "kt::k_map<3, 0, 1, 1, 4, 128>", "kswish_bf16": "kt::k_map<2, 0, 1, 1, 2, 256>",
                "lstm": "kt::k_lstm<1>"}
 
-EXTRA = [("c2_bf16_2p24", "ktanh_bf16"), ("c2_bf16_2p24", "ktanh64_bf16"), ("c3_f32_2p28", "ktanh_f32"),
+EXTRA = [("c2_bf16_2p24", "ktanh_bf16"), ("c2_bf16_2p24", "ksigmoid_bf16"), ("c2_bf16_2p24", "ktanh64_bf16"),
+         ("c3_f32_2p28", "ktanh_f32"), ("c3_f32_2p28", "ksigmoid_f32"),
          ("c3_f32_2p28", "ktanh_f32:p23"), ("c3_f32_2p28", "ktanh_f32_via_bf16"),
          ("c3_f32_2p28", "kgelu_f32"), ("c3_f32_2p28", "kswish_f32"),
          ("c4_lstm_gates", "lstm"), ("c5_ffn_2p30", "kgelu_bf16"), ("c5_ffn_2p30", "kswish_bf16"),
