@@ -456,6 +456,24 @@ def test_lstm_cell_specials(kt):
     assert_bitexact(u16(hn), want_h, 16, nan_by_class=True, ctx="h_next specials")
 
 
+@pytest.mark.parametrize("q", [0, 1, 2, 3])
+def test_lstm_cell_every_gate_pattern(kt, q):
+    """Gate q (i, f, g, o) takes every BF16 pattern once (65,536 cells, H = 16),
+    the other gates and c random: the cell's K-Sigmoid (run on x with its own
+    words, no x/2 multiply) and K-TanH gates against the oracle, bit-exact."""
+    H, rows = 16, 4096
+    g = torch.Generator(device="cuda").manual_seed(700 + q)
+    gates = (torch.randn(rows, 4, H, device="cuda", generator=g) * 3).to(torch.bfloat16)
+    x = WL.make_input("c1_exhaustive_bf16", device="cuda").view(rows, H)
+    gates[:, q, :] = x
+    gates = gates.reshape(rows, 4 * H).contiguous()
+    c = torch.randn(rows, H, device="cuda", generator=g) * 2
+    cn, hn = kt.klstm_cell_bf16(gates, c, H)
+    want_c, want_h = O.lstm_cell_bf16(u16(gates), u32(c), H)
+    assert_bitexact(u32(cn), want_c, 32, nan_by_class=True, ctx=f"c_next, gate {q} exhaustive")
+    assert_bitexact(u16(hn), want_h, 16, nan_by_class=True, ctx=f"h_next, gate {q} exhaustive")
+
+
 # ------------------------------------------------ fused K-GELU + K-Swish ----
 @pytest.mark.parametrize("fmt", ["bf16", "f32"])
 def test_gelu_swish_fused_equals_single_ops(kt, fmt):
