@@ -75,10 +75,25 @@ def lstm_cell():
     torch.cuda.synchronize()
     print("lstm_cell ok", flush=True)
 
+def gemm_cell():
+    """bench.py's LSTM GEMM line with the whole cell fused (kgemm_lstm_cell_bf16)."""
+    H = WL.LSTM_HIDDEN
+    M = 128 * 50
+    A = WL.make_input("c4_lstm_gates", device="cuda", numel=M * H).reshape(M, H)
+    B = (WL.make_input("c4_lstm_gates", device="cuda", numel=4 * H * H, seed=9).reshape(4 * H, H) * 0.05
+         ).to(torch.bfloat16)
+    c = torch.randn(M, H, device="cuda")
+    cn, hn = torch.empty_like(c), torch.empty(M, H, dtype=torch.bfloat16, device="cuda")
+    for _ in range(4):
+        kt.kgemm_lstm_cell_bf16(A, B, c, H, c_next=cn, h_next=hn)
+    torch.cuda.synchronize()
+    print("gemm_cell ok", flush=True)
+
+
 if __name__ == "__main__":
     names = sys.argv[1:] or list(TARGETS) + ["gemm_gelu", "lstm_cell"]
     for name in names:
-        if name in ("gemm_gelu", "lstm_cell", "tanh_bf16_steady", "gelu_swish", "apx_minimax3"):
+        if name in ("gemm_gelu", "gemm_cell", "lstm_cell", "tanh_bf16_steady", "gelu_swish", "apx_minimax3"):
             globals()[name]()
             continue
         key, fn = TARGETS[name]
