@@ -47,8 +47,8 @@ MUTANTS = [
      "w0[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));",
      "tests/test_gpu_gemm.py"),
     ("gemm cell gate order", G,
-     "const uint32_t gf = pack_bf16x2(__uint_as_float(r[32 + 2 * k + 1]), __uint_as_float(r[32 + 2 * k]));",
-     "const uint32_t gf = pack_bf16x2(__uint_as_float(r[96 + 2 * k + 1]), __uint_as_float(r[96 + 2 * k]));",
+     "const uint32_t gf = pack_bf16x2(__uint_as_float(r[8 + 2 * k + 1]), __uint_as_float(r[8 + 2 * k]));",
+     "const uint32_t gf = pack_bf16x2(__uint_as_float(r[24 + 2 * k + 1]), __uint_as_float(r[24 + 2 * k]));",
      "tests/test_gpu_gemm.py"),
     ("p = 23 table word", API,
      "((int64_t)E[t] << 23) + (int64_t)b[t] - ((int64_t)e_in(t) << (23 - r[t]));",
