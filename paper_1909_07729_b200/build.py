@@ -68,8 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libktanh.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
+    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:   # registers / spills per kernel
+        f.write("".join(ln for ln in r.stderr.splitlines(keepends=True) if "Compile time" not in ln))
     os.replace(tmp, LIB)
     return LIB
 
